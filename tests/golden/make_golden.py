@@ -1,0 +1,178 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py [/root/reference/pkg/src]
+
+It imports the reference package ``powerba`` (read-only source tree; bytecode
+writing disabled) and records, for a handful of small problems, the outputs of
+the reference's own hot-path functions: ``blocks._sorted_observation_order``,
+``blocks.linearize`` / ``assemble_from_observations``, ``Linearization.damp``,
+``DampedSystem.b_tilde``, ``power_series_solve``, ``back_substitute``,
+``lm.residual_cost`` and ``lm.run`` (reference ``pkg/src/powerba``).  The GPU
+box never sees /root/reference; tests only read the .npz files written here.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+sys.dont_write_bytecode = True
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF = sys.argv[1] if len(sys.argv) > 1 else "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(os.path.dirname(REF), "tests"))
+
+import numpy as np  # noqa: E402
+from powerba import bal_io, blocks, lm, synthetic  # noqa: E402
+from powerba.power_series import back_substitute, power_series_solve  # noqa: E402
+
+import helpers  # noqa: E402  (the reference's own test oracles: random_block_system)
+
+
+def problem_arrays(p):
+    return dict(camera_params=p.camera_params, points=p.points, cam_indices=p.cam_indices,
+                pt_indices=p.pt_indices, pixels=p.pixels)
+
+
+def lin_outputs(lin, prefix="", store=True):
+    st = lin.store
+    out = {
+        prefix + "cam_sorted": st.cam_sorted, prefix + "pt_sorted": st.pt_sorted,
+        prefix + "group_k": np.array([g.k for g in st.groups]),
+        prefix + "group_start": np.array([g.obs_start for g in st.groups]),
+        prefix + "group_n": np.array([g.n for g in st.groups]),
+        prefix + "U0": lin.U0, prefix + "V0": lin.V0, prefix + "b_p": lin.b_p,
+        prefix + "b_l": lin.b_l, prefix + "D_p": lin.D_p, prefix + "D_l": lin.D_l,
+        prefix + "n_invalid": np.array(lin.n_invalid),
+    }
+    if store:
+        out[prefix + "storage"] = st.storage_obs
+    return out
+
+
+def system_outputs(sys_, tag, solves):
+    out = {f"{tag}_U_inv": sys_.U_inv, f"{tag}_V_inv": sys_.V_inv,
+           f"{tag}_b_tilde": sys_.b_tilde()}
+    for j, (eps, m) in enumerate(solves):
+        r = power_series_solve(sys_, epsilon=eps, max_order=m)
+        out[f"{tag}_solve{j}_eps"] = np.array(eps)
+        out[f"{tag}_solve{j}_m"] = np.array(m)
+        out[f"{tag}_solve{j}_delta_p"] = r.delta_p
+        out[f"{tag}_solve{j}_order"] = np.array(r.order_used)
+        out[f"{tag}_solve{j}_converged"] = np.array(r.converged)
+        out[f"{tag}_solve{j}_delta_l"] = back_substitute(sys_, r.delta_p)
+    return out
+
+
+def trace_outputs(trace, tag):
+    its = trace.iterations
+    return {f"{tag}_cost": np.array([i.cost for i in its]),
+            f"{tag}_lam": np.array([i.lam for i in its]),
+            f"{tag}_order": np.array([i.order_m for i in its]),
+            f"{tag}_accepted": np.array([i.accepted for i in its]),
+            f"{tag}_n_invalid": np.array([i.n_invalid for i in its]),
+            f"{tag}_peak_bytes": np.array([i.peak_bytes for i in its]),
+            f"{tag}_converged": np.array(trace.converged)}
+
+
+def bundle(name, p, *, lams, solves, lm_cfgs, store=True, save_inputs=True):
+    out = {"name": np.array(name)}
+    if save_inputs:
+        out.update(problem_arrays(p))
+    from paper_2204_12834_b200.problem import Problem
+    out["fingerprint"] = np.array(Problem(**problem_arrays(p)).fingerprint())
+    cs, ps, order = blocks._sorted_observation_order(p.cam_indices, p.pt_indices, p.n_points)
+    out["order"] = order
+    lin = blocks.linearize(p)
+    out.update(lin_outputs(lin, store=store))
+    out["cost0"] = np.array(lm.residual_cost(p, lm.BaState.from_problem(p)))
+    for j, lam in enumerate(lams):
+        out[f"lam{j}"] = np.array(lam)
+        out.update(system_outputs(lin.damp(lam), f"sys{j}", solves))
+    for tag, cfg in lm_cfgs.items():
+        tr = lm.run(p, cfg)
+        out.update(trace_outputs(tr, tag))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"wrote {name}.npz ({p.n_cameras} cams, {p.n_points} pts, {p.n_observations} obs)")
+
+
+def explicit_bundle():
+    """Systems built by assemble_from_observations (the reference's test seam)."""
+    out = {}
+    for j, (seed, lam) in enumerate([(0, 1e-4), (1, 1e-2), (2, 1.0), (4, 1e-2)]):
+        rng = np.random.default_rng(seed)
+        n_cam = int(rng.integers(2, 11))
+        n_pt = int(rng.integers(8, 51))
+        # same recipe as helpers.random_block_system (tests/helpers.py:200-233)
+        cam_idx = list(np.repeat(np.arange(n_cam), n_pt))
+        pt_idx = list(np.tile(np.arange(n_pt), n_cam))
+        nv = len(cam_idx)
+        jp = [rng.normal(size=(nv, 2, 9))]
+        jl = [rng.normal(size=(nv, 2, 3))]
+        res = [rng.normal(size=(nv, 2))]
+        for c in range(n_cam):
+            cam_idx.extend([c] * 5)
+            pt_idx.extend(int(rng.integers(n_pt)) for _ in range(5))
+            jp.append(3.0 * rng.normal(size=(5, 2, 9)))
+            jl.append(np.zeros((5, 2, 3)))
+            res.append(rng.normal(size=(5, 2)))
+        cam_idx = np.array(cam_idx)
+        pt_idx = np.array(pt_idx)
+        jp, jl, res = np.concatenate(jp), np.concatenate(jl), np.concatenate(res)
+        # duplicates (anchor rows repeat a visible pair) are allowed by this seam
+        lin = blocks.assemble_from_observations(cam_idx, pt_idx, jp, jl, res, n_cam, n_pt)
+        sys_ = lin.damp(lam)
+        ref_sys = helpers.random_block_system(seed, lam=lam)
+        assert np.array_equal(ref_sys.b_tilde(), sys_.b_tilde())
+        pre = f"e{j}_"
+        out.update({pre + "cam_idx": cam_idx, pre + "pt_idx": pt_idx, pre + "jp": jp,
+                    pre + "jl": jl, pre + "res": res, pre + "n_cam": np.array(n_cam),
+                    pre + "n_pt": np.array(n_pt), pre + "lam": np.array(lam)})
+        out.update(lin_outputs(lin, pre, store=False))
+        out.update(system_outputs(sys_, pre + "sys", [(1e-14, 200), (1e-300, 6), (0.01, 20)]))
+    # decoupled system: J_l = 0 (tests/test_power_series.py:82-94)
+    rng = np.random.default_rng(3)
+    jp = rng.normal(size=(6, 2, 9))
+    jl = np.zeros((6, 2, 3))
+    res = rng.normal(size=(6, 2))
+    ci, pi = np.array([0, 0, 0, 1, 1, 1]), np.array([0, 1, 2, 0, 1, 2])
+    lin = blocks.assemble_from_observations(ci, pi, jp, jl, res, 2, 3)
+    sys_ = lin.damp(1e-2)
+    r = power_series_solve(sys_, epsilon=1e-12)
+    out.update({"dec_jp": jp, "dec_jl": jl, "dec_res": res, "dec_cam_idx": ci, "dec_pt_idx": pi,
+                "dec_delta_p": r.delta_p, "dec_order": np.array(r.order_used),
+                "dec_u_inv_minus_bt": sys_.apply_u_inv(-sys_.b_tilde())})
+    np.savez_compressed(os.path.join(HERE, "explicit.npz"), **out)
+    print("wrote explicit.npz")
+
+
+def main():
+    from paper_2204_12834_b200 import configs
+    oracle = bal_io.perturb(synthetic.make_random_problem(3, 5, seed=1), 0.01, seed=0)
+    bundle("rand3x5", oracle, lams=[1e-4, 1.0],
+           solves=[(1e-12, 3), (1e-14, 50), (0.01, 20), (1e-300, 10)],
+           lm_cfgs={"lm_poba": lm.LmConfig(solver="poba")})
+    noisy = bal_io.perturb(synthetic.make_random_problem(4, 60, seed=5, pixel_noise=1.0), 0.01, seed=0)
+    bundle("noisy4x60", noisy, lams=[1e-4, 1e-2],
+           solves=[(0.01, 20), (1e-300, 12)],
+           lm_cfgs={"lm_poba": lm.LmConfig(solver="poba")})
+    rig = synthetic.make_rig_problem(pixel_noise=1.0)
+    bundle("rig49", rig, lams=[1e-4], solves=[(0.01, 20), (1e-300, 32)],
+           lm_cfgs={"lm_poba": lm.LmConfig(solver="poba", max_outer_iterations=50)}, store=False)
+    c1 = configs.make_config("c1")
+    bundle("c1", c1, lams=[1e-4], solves=[(0.01, 32), (1e-300, 32)],
+           lm_cfgs={"lm_c1": lm.LmConfig(solver="poba", max_outer_iterations=10, max_order=32)},
+           store=False)
+    c2 = configs.make_config("c2")
+    bundle("c2", c2, lams=[1e-4], solves=[(1e-6, 32)],
+           lm_cfgs={"lm_c2": lm.LmConfig(solver="poba", max_outer_iterations=20, max_order=32,
+                                         epsilon=1e-6)},
+           store=False, save_inputs=False)
+    explicit_bundle()
+
+
+if __name__ == "__main__":
+    main()
