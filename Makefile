@@ -1,0 +1,25 @@
+# libpoba: sm_100a only.  `make` builds paper_2204_12834_b200/lib/libpoba.so in-tree.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+SRC := $(wildcard paper_2204_12834_b200/csrc/*.cu)
+OBJ := $(patsubst paper_2204_12834_b200/csrc/%.cu,build/%.o,$(SRC))
+LIB := paper_2204_12834_b200/lib/libpoba.so
+
+all: $(LIB)
+
+build/%.o: paper_2204_12834_b200/csrc/%.cu paper_2204_12834_b200/csrc/poba_internal.h include/poba.h
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(OBJ)
+	@mkdir -p paper_2204_12834_b200/lib
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart -ldl
+
+ptxas:
+	@for f in $(SRC); do $(NVCC) $(NVFLAGS) -Xptxas -v -c $$f -o /dev/null 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" ; done
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean ptxas

@@ -1,0 +1,159 @@
+/*
+ * libpoba -- B200-native (sm_100a, fp64) power-series Schur solve for bundle
+ * adjustment, the hot path of Power Bundle Adjustment (arXiv 2204.12834).
+ *
+ * Plain C ABI: opaque context, plain pointers and sizes, no torch types.  The
+ * Python host layer (paper_2204_12834_b200/_lib.py) binds it with ctypes.  The
+ * reference is a pure-Python package; each entry point below replaces the
+ * reference function cited beside it (paths relative to
+ * /root/reference/pkg/src/powerba/), and INTEGRATION.md shows the ctypes
+ * binding a powerba maintainer would add.
+ *
+ * Every function returns a status code (POBA_OK = 0).  On failure
+ * poba_last_error() returns a thread-local message; the Python layer maps
+ * POBA_EINVAL / POBA_ENOTSPD / POBA_ENONFINITE / POBA_EVANISH to ValueError
+ * with the reference's own messages.
+ *
+ * Arrays: observation arrays are in the caller's (file) order, cameras are
+ * (n_cam, 9) row-major BAL order [rotvec, t, f, k1, k2], points (n_pt, 3),
+ * pixels (n_obs, 2), pose vectors 9*n_cam, landmark vectors 3*n_pt -- exactly
+ * the reference's BalProblem layout (bal_io.py:55-78).  Inputs are copied at
+ * call time and never aliased after return.
+ */
+#ifndef POBA_H
+#define POBA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POBA_OK 0
+#define POBA_EINVAL 1     /* invalid argument / problem structure         */
+#define POBA_ENOTSPD 2    /* damped pose or point block not SPD           */
+#define POBA_ENONFINITE 3 /* non-finite series iterate (order in message) */
+#define POBA_ECUDA 4      /* CUDA runtime error                            */
+#define POBA_ENCCL 5      /* NCCL error                                    */
+#define POBA_EVANISH 6    /* vanishing iterate norm with nonzero rhs       */
+
+typedef struct poba_ctx poba_ctx;
+
+/* thread-local message of the last failing call on this thread */
+const char* poba_last_error(void);
+int poba_version(void);
+
+/* ---- context ------------------------------------------------------------
+ * One context per process and GPU.  poba_create_sharded() joins an NCCL
+ * communicator of nranks processes (one per GPU); landmarks and their
+ * observations are partitioned across ranks, cameras are replicated, and
+ * every series term ends in one all-reduce of the 9*n_cam camera vector.   */
+int poba_create(int device, poba_ctx** out);
+int poba_nccl_unique_id(void* out_128_bytes);
+int poba_create_sharded(int device, int rank, int nranks, const void* nccl_id_128_bytes,
+                        poba_ctx** out);
+int poba_destroy(poba_ctx* ctx);
+
+/* ---- K0: observation store structure -------------------------------------
+ * Replaces blocks._sorted_observation_order (blocks.py:362-372) and
+ * blocks._build_groups (blocks.py:405-417): canonical (k, landmark, camera)
+ * order by a stable device radix sort, landmark-aligned tiles, the chunked
+ * camera-slot map used by the deterministic camera reductions, and (sharded)
+ * this rank's landmark range.  pixels may be NULL (explicit-Jacobian use).   */
+int poba_set_problem(poba_ctx* ctx, int64_t n_cam, int64_t n_pt, int64_t n_obs,
+                     const int64_t* cam_idx, const int64_t* pt_idx, const double* pixels);
+/* info[0..15]: n_groups, n_tiles, n_chunks, n_partials, obs_lo, obs_hi, lm_lo,
+ * lm_hi, max_slots, n_long, device_bytes, k_max, n_cam, n_pt, n_obs, rank   */
+int poba_problem_info(poba_ctx* ctx, int64_t* info);
+/* order / cam_sorted / pt_sorted (n_obs each): bit-exact with the reference */
+int poba_get_ordering(poba_ctx* ctx, int64_t* order, int64_t* cam_sorted, int64_t* pt_sorted);
+/* k-groups (k ascending): group k, first canonical observation, #landmarks */
+int poba_get_groups(poba_ctx* ctx, int64_t cap, int64_t* n_groups, int64_t* group_k,
+                    int64_t* group_start, int64_t* group_n);
+
+/* ---- K1-K3: linearization -------------------------------------------------
+ * blocks.linearize (blocks.py:293-324) + _finish_linearization (375-402):
+ * residual + analytic Jacobians (camera.evaluate, camera.py:67-135), the
+ * landmark-major store, V0/b_l per landmark, U0/b_p per camera (deterministic
+ * segmented reductions, no atomics), Marquardt diagonals D_p/D_l.
+ * points == NULL uses the device-resident points (poba_set_points).        */
+int poba_linearize(poba_ctx* ctx, const double* cam_params, const double* points,
+                   int64_t* n_invalid);
+/* blocks.assemble_from_observations (blocks.py:333-352): explicit per-observation
+ * j_pose (n_obs,2,9), j_point (n_obs,2,3), residuals (n_obs,2) in file order.  */
+int poba_linearize_explicit(poba_ctx* ctx, const double* j_pose, const double* j_point,
+                            const double* residuals);
+
+/* ---- K2-K4: damping ---------------------------------------------------------
+ * DampedSystem.__init__ (blocks.py:164-192) with _spd_block_inverse (277-285):
+ * U = U0 + lam diag(D_p^2), V = V0 + lam diag(D_l^2) (identity != 0: D = 1),
+ * batched 9x9 / 3x3 Cholesky inverses.                                       */
+int poba_damp(poba_ctx* ctx, double lam, int identity);
+
+/* ---- K4-K6: power-series solve ---------------------------------------------
+ * power_series_solve (power_series.py:53-77): b_tilde = b_p - W V^-1 b_l
+ * (blocks.py:256-260), t0 = U^-1(-b_tilde), t_i = U^-1 W V^-1 W^T t_{i-1},
+ * x_i = x_{i-1} + t_i, stop when (i+1)||x_i - x_{i-1}||/||x_i|| < epsilon
+ * (power_series.py:29-42) -- evaluated on the device, the whole loop enqueued
+ * (CUDA graph) without host round trips.  ratios (nullable, max_order+1
+ * doubles) receives the stop ratio per order (NaN where not evaluated).      */
+int poba_series_solve(poba_ctx* ctx, double epsilon, int max_order, double* delta_p,
+                      int* order_used, int* converged, double* ratios);
+/* apply_series_inverse (power_series.py:80-91): fixed order, no stop test.  */
+int poba_series_apply(poba_ctx* ctx, const double* v, int order, double* out);
+
+/* ---- K7: back-substitution (power_series.py:94-100) -------------------------
+ * dx_l = -V^-1 (b_l + W^T dx_p); delta_p NULL = the last series solution.
+ * delta_l (nullable) is scattered to point-index order (3*n_pt; sharded: only
+ * this rank's landmarks are written).  nonzero: 1 if dx_p or dx_l != 0.      */
+int poba_back_substitute(poba_ctx* ctx, const double* delta_p, double* delta_l, int* nonzero);
+
+/* ---- K8: cost (lm.residual_cost, lm.py:107-119) ------------------------------
+ * 0.5 sum ||r||^2 and the invalid count.  points NULL: device points, plus
+ * the last back-substituted delta_l when trial != 0 (lm.apply_update,
+ * lm.py:132-144, points part).                                               */
+int poba_cost(poba_ctx* ctx, const double* cam_params, const double* points, int trial,
+              double* cost, int64_t* n_invalid);
+
+/* ---- device-resident landmark state ------------------------------------------ */
+int poba_set_points(poba_ctx* ctx, const double* points);
+int poba_accept_points(poba_ctx* ctx); /* points += last delta_l (lm.py:140) */
+int poba_get_points(poba_ctx* ctx, double* points);
+
+/* ---- operator passes (DampedSystem.apply_*, blocks.py:214-254) --------------- */
+#define POBA_OP_W 0      /* (3 n_pt) -> (9 n_cam)   */
+#define POBA_OP_WT 1     /* (9 n_cam) -> (3 n_pt)   */
+#define POBA_OP_U_INV 2  /* (9 n_cam) -> (9 n_cam)  */
+#define POBA_OP_V_INV 3  /* (3 n_pt) -> (3 n_pt)    */
+#define POBA_OP_U 4      /* (9 n_cam) -> (9 n_cam)  */
+#define POBA_OP_SCHUR 5  /* (9 n_cam) -> (9 n_cam)  */
+int poba_apply(poba_ctx* ctx, int op, const double* in, double* out);
+
+/* ---- read-back of assembled quantities (parity tests, attributes) ----------- */
+#define POBA_READ_U0 0      /* n_cam x 9 x 9 */
+#define POBA_READ_V0 1      /* n_pt x 3 x 3  */
+#define POBA_READ_B_P 2     /* 9 n_cam       */
+#define POBA_READ_B_L 3     /* 3 n_pt        */
+#define POBA_READ_D_P 4     /* n_cam x 9     */
+#define POBA_READ_D_L 5     /* n_pt x 3      */
+#define POBA_READ_U 6       /* n_cam x 9 x 9 (damped) */
+#define POBA_READ_V 7       /* n_pt x 3 x 3  */
+#define POBA_READ_U_INV 8   /* n_cam x 9 x 9 */
+#define POBA_READ_V_INV 9   /* n_pt x 3 x 3  */
+#define POBA_READ_B_TILDE 10 /* 9 n_cam      */
+#define POBA_READ_STORAGE 11 /* n_obs x 2 x 13, canonical order (local obs) */
+int poba_read(poba_ctx* ctx, int what, double* dst);
+
+/* ---- instrumentation ------------------------------------------------------------
+ * Time `reps` forced series terms (no stop test) with CUDA events on the
+ * library stream; ms_per_term receives the mean.  launches: kernel launches
+ * per term.  Used by bench.py for the roofline figure.                       */
+int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_term_kernel,
+                    int* launches);
+/* kernel launches issued by the library since creation (all entry points)  */
+int64_t poba_launch_count(poba_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POBA_H */

@@ -1,0 +1,495 @@
+// C-ABI entry points of libpoba (see include/poba.h for the contract and the
+// reference function each entry point replaces).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <dlfcn.h>
+
+#include "poba_internal.h"
+
+struct poba_ctx {
+  poba::Ctx c;
+  std::vector<int> lm_pt_host;  // local landmark -> point id (host copy)
+};
+
+namespace poba {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static int state = 0;  // 0 untried, 1 ok, -1 failed
+  static std::string why;
+  if (state == 1) return &api;
+  if (state == -1) {
+    set_error(why);
+    return nullptr;
+  }
+  void* h = nullptr;
+  const char* env = getenv("POBA_NCCL_LIB");
+  if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // already in the process (e.g. PyTorch's)
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    state = -1;
+    why = std::string("cannot load libnccl.so.2: ") + dlerror();
+    set_error(why);
+    return nullptr;
+  }
+  bool ok = true;
+  auto sym = [&](const char* name) -> void* {
+    void* p = dlsym(h, name);
+    if (!p) ok = false;
+    return p;
+  };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+  api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  if (!ok) {
+    state = -1;
+    why = "libnccl.so.2 lacks a required symbol";
+    set_error(why);
+    return nullptr;
+  }
+  state = 1;
+  return &api;
+}
+
+int allreduce_sum(Ctx& c, double* d_buf, size_t n) {
+  if (c.nranks <= 1) return POBA_OK;
+  PNCCL(AllReduce(d_buf, d_buf, n, ncclFloat64, ncclSum, c.comm, c.stream));
+  return POBA_OK;
+}
+
+namespace {
+
+void unpack9(const double* p45, double* out81) {
+  for (int i = 0; i < 9; ++i)
+    for (int j = i; j < 9; ++j) {
+      const double v = p45[i * 9 - i * (i - 1) / 2 + (j - i)];
+      out81[i * 9 + j] = v;
+      out81[j * 9 + i] = v;
+    }
+}
+
+void unpack3(const double* p6, double* out9) {
+  const int idx[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+  for (int q = 0; q < 9; ++q) out9[q] = p6[idx[q]];
+}
+
+int copy_down(Ctx& c, const DBuf& src, size_t bytes, std::vector<double>& out) {
+  out.resize(bytes / 8);
+  PCK(cudaMemcpyAsync(out.data(), src.p, bytes, cudaMemcpyDeviceToHost, c.stream));
+  PCK(cudaStreamSynchronize(c.stream));
+  return POBA_OK;
+}
+
+}  // namespace
+
+}  // namespace poba
+
+using poba::Ctx;
+using poba::DBuf;
+
+#define CTX_CHECK(ctx)                                                              \
+  do {                                                                              \
+    if (!(ctx)) return poba::fail(POBA_EINVAL, "null context");                    \
+    cudaError_t e_ = cudaSetDevice((ctx)->c.device);                                \
+    if (e_ != cudaSuccess) return poba::fail(POBA_ECUDA, cudaGetErrorString(e_));   \
+  } while (0)
+#define NEED(cond, msg)                                   \
+  do {                                                    \
+    if (!(cond)) return poba::fail(POBA_EINVAL, (msg));   \
+  } while (0)
+
+extern "C" {
+
+const char* poba_last_error(void) { return poba::g_err.c_str(); }
+int poba_version(void) { return 1; }
+
+static int create_common(int device, poba_ctx** out) {
+  if (!out) return poba::fail(POBA_EINVAL, "null output pointer");
+  int n = 0;
+  PCK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return poba::fail(POBA_EINVAL, "no such CUDA device");
+  PCK(cudaSetDevice(device));
+  poba_ctx* x = new poba_ctx();
+  x->c.device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&x->c.stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete x;
+    return poba::fail(POBA_ECUDA, cudaGetErrorString(e));
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) x->c.n_sm = prop.multiProcessorCount;
+  *out = x;
+  return POBA_OK;
+}
+
+int poba_create(int device, poba_ctx** out) { return create_common(device, out); }
+
+int poba_nccl_unique_id(void* out) {
+  if (!out) return poba::fail(POBA_EINVAL, "null output pointer");
+  ncclUniqueId id;
+  PNCCL(GetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return POBA_OK;
+}
+
+int poba_create_sharded(int device, int rank, int nranks, const void* nccl_id, poba_ctx** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return poba::fail(POBA_EINVAL, "bad rank / nranks");
+  PTRY(create_common(device, out));
+  Ctx& c = (*out)->c;
+  c.rank = rank;
+  c.nranks = nranks;
+  if (nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    const poba::NcclApi* api = poba::nccl_api();
+    ncclResult_t r = api ? api->CommInitRank(&c.comm, nranks, id, rank) : ncclSystemError;
+    if (r != ncclSuccess) {
+      std::string msg = api ? std::string("ncclCommInitRank: ") + api->GetErrorString(r) : poba::g_err;
+      poba_destroy(*out);
+      *out = nullptr;
+      return poba::fail(POBA_ENCCL, msg);
+    }
+  }
+  return POBA_OK;
+}
+
+int poba_destroy(poba_ctx* ctx) {
+  if (!ctx) return POBA_OK;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.comm && poba::nccl_api()) poba::nccl_api()->CommDestroy(ctx->c.comm);
+  if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+  return POBA_OK;
+}
+
+int poba_set_problem(poba_ctx* ctx, int64_t n_cam, int64_t n_pt, int64_t n_obs, const int64_t* cam_idx,
+                     const int64_t* pt_idx, const double* pixels) {
+  CTX_CHECK(ctx);
+  NEED(n_cam > 0 && n_pt > 0 && n_obs > 0, "problem has no observations");
+  NEED(cam_idx && pt_idx, "null index arrays");
+  Ctx& c = ctx->c;
+  c.n_cam = n_cam;
+  c.n_pt = n_pt;
+  c.n_obs = n_obs;
+  c.have_problem = false;
+  PTRY(poba::build_structure(c, cam_idx, pt_idx, pixels));
+  ctx->lm_pt_host.resize(c.n_lm_l);
+  PCK(cudaMemcpy(ctx->lm_pt_host.data(), c.lm_pt.p, c.n_lm_l * 4, cudaMemcpyDeviceToHost));
+  return POBA_OK;
+}
+
+int poba_problem_info(poba_ctx* ctx, int64_t* info) {
+  CTX_CHECK(ctx);
+  NEED(info, "null output");
+  const Ctx& c = ctx->c;
+  size_t bytes = 0;
+  for (const DBuf* b : {&c.order, &c.cam_file, &c.pt_file, &c.cam_l, &c.pix_l, &c.file_l, &c.lm_pt, &c.lm_off,
+                        &c.pt_to_lm, &c.tiles, &c.chunks, &c.perm, &c.seg_start, &c.seg_slot, &c.part_cam_off,
+                        &c.part_idx, &c.cperm, &c.cc_start, &c.cc_cam_off, &c.J, &c.Rz, &c.cams, &c.cams_prep,
+                        &c.U0, &c.bp, &c.Dp, &c.Uinv, &c.Ud, &c.bt, &c.tvec, &c.xvec, &c.rvec, &c.cc_part,
+                        &c.partials, &c.points, &c.V0, &c.bl, &c.Dl, &c.Vinv, &c.Vd, &c.dl, &c.ltmp})
+    bytes += b->bytes;
+  const int64_t v[16] = {(int64_t)c.grp_k.size(), c.n_tiles, c.n_chunks, c.n_partials, c.obs_lo, c.obs_hi,
+                         c.lm_lo, c.lm_hi, c.max_slots, c.n_long, (int64_t)bytes, c.k_max, c.n_cam, c.n_pt,
+                         c.n_obs, c.rank};
+  std::memcpy(info, v, sizeof(v));
+  return POBA_OK;
+}
+
+int poba_get_ordering(poba_ctx* ctx, int64_t* order, int64_t* cam_sorted, int64_t* pt_sorted) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_problem, "no problem set");
+  const int64_t n = c.n_obs;
+  std::vector<int> o(n), cf, pf;
+  PCK(cudaMemcpy(o.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
+  if (cam_sorted) {
+    cf.resize(n);
+    PCK(cudaMemcpy(cf.data(), c.cam_file.p, n * 4, cudaMemcpyDeviceToHost));
+  }
+  if (pt_sorted) {
+    pf.resize(n);
+    PCK(cudaMemcpy(pf.data(), c.pt_file.p, n * 4, cudaMemcpyDeviceToHost));
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (order) order[i] = o[i];
+    if (cam_sorted) cam_sorted[i] = cf[o[i]];
+    if (pt_sorted) pt_sorted[i] = pf[o[i]];
+  }
+  return POBA_OK;
+}
+
+int poba_get_groups(poba_ctx* ctx, int64_t cap, int64_t* n_groups, int64_t* k, int64_t* start, int64_t* n) {
+  CTX_CHECK(ctx);
+  const Ctx& c = ctx->c;
+  NEED(c.have_problem, "no problem set");
+  *n_groups = (int64_t)c.grp_k.size();
+  for (int64_t g = 0; g < std::min<int64_t>(cap, *n_groups); ++g) {
+    if (k) k[g] = c.grp_k[g];
+    if (start) start[g] = c.grp_start[g];
+    if (n) n[g] = c.grp_n[g];
+  }
+  return POBA_OK;
+}
+
+int poba_set_points(poba_ctx* ctx, const double* points) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_problem, "no problem set");
+  NEED(points, "null points");
+  PTRY(poba::points_gather_from_host(c, points, c.points.as<double>()));
+  PCK(cudaStreamSynchronize(c.stream));
+  c.have_points = true;
+  return POBA_OK;
+}
+
+int poba_get_points(poba_ctx* ctx, double* points) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_points, "no device points");
+  return poba::points_scatter_to_host(c, c.points.as<double>(), points);
+}
+
+int poba_accept_points(poba_ctx* ctx) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_points && c.have_delta_l, "no back-substituted landmark step");
+  return poba::points_accept_device(c);
+}
+
+int poba_linearize(poba_ctx* ctx, const double* cam_params, const double* points, int64_t* n_invalid) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_problem, "no problem set");
+  NEED(c.have_pixels, "problem was set without pixels");
+  NEED(cam_params, "null camera parameters");
+  if (points) PTRY(poba_set_points(ctx, points));
+  NEED(c.have_points, "no points (pass them or call poba_set_points)");
+  PCK(cudaMemcpyAsync(c.cams.p, cam_params, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
+  PTRY(poba::linearize_device(c, false, nullptr, nullptr, nullptr));
+  if (n_invalid) *n_invalid = c.n_invalid;
+  return POBA_OK;
+}
+
+int poba_linearize_explicit(poba_ctx* ctx, const double* jp, const double* jl, const double* res) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_problem, "no problem set");
+  NEED(jp && jl && res, "null Jacobian arrays");
+  PTRY(poba::linearize_device(c, true, jp, jl, res));
+  return POBA_OK;
+}
+
+int poba_damp(poba_ctx* ctx, double lam, int identity) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_lin, "no linearization");
+  if (!(lam >= 0)) return poba::fail(POBA_EINVAL, "lambda must be non-negative");
+  return poba::damp_device(c, lam, identity ? 1 : 0);
+}
+
+int poba_series_solve(poba_ctx* ctx, double epsilon, int max_order, double* delta_p, int* order_used,
+                      int* converged, double* ratios) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  if (max_order < 0) return poba::fail(POBA_EINVAL, "max_order must be non-negative");
+  if (!(epsilon > 0)) return poba::fail(POBA_EINVAL, "epsilon must be positive");
+  int ou = 0, cv = 0;
+  PTRY(poba::series_device(c, epsilon, max_order, false, &ou, &cv));
+  if (order_used) *order_used = ou;
+  if (converged) *converged = cv;
+  if (delta_p) {
+    PCK(cudaMemcpyAsync(delta_p, c.xvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToHost, c.stream));
+  }
+  if (ratios) {
+    PCK(cudaMemcpyAsync(ratios, c.ratios.p, (size_t)(max_order + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+  }
+  PCK(cudaStreamSynchronize(c.stream));
+  return POBA_OK;
+}
+
+int poba_series_apply(poba_ctx* ctx, const double* v, int order, double* out) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  if (order < 0) return poba::fail(POBA_EINVAL, "order must be non-negative");
+  NEED(v && out, "null vectors");
+  PCK(cudaMemcpyAsync(c.ctmp.p, v, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
+  PTRY(poba::series_apply_device(c, c.ctmp.as<double>(), order, c.ctmp2.as<double>()));
+  PCK(cudaMemcpy(out, c.ctmp2.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToHost));
+  return POBA_OK;
+}
+
+int poba_back_substitute(poba_ctx* ctx, const double* delta_p, double* delta_l, int* nonzero) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  const double* d_dp = c.xvec.as<double>();
+  if (delta_p) {
+    PCK(cudaMemcpyAsync(c.ctmp.p, delta_p, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
+    d_dp = c.ctmp.as<double>();
+  } else {
+    NEED(c.have_solution, "no series solution on the device");
+  }
+  int nz = 0;
+  PTRY(poba::back_substitute_device(c, d_dp, &nz));
+  if (nonzero) *nonzero = nz;
+  if (delta_l) PTRY(poba::points_scatter_to_host(c, c.dl.as<double>(), delta_l));
+  return POBA_OK;
+}
+
+int poba_cost(poba_ctx* ctx, const double* cam_params, const double* points, int trial, double* cost,
+              int64_t* n_invalid) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_problem && c.have_pixels, "no problem with pixels");
+  NEED(cam_params, "null camera parameters");
+  PCK(cudaMemcpyAsync(c.cams_trial.p, cam_params, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
+  PTRY(poba::cameras_prep(c, c.cams_trial.as<double>(), c.trial_prep.as<double>()));
+  if (trial) NEED(c.have_delta_l, "no landmark step for the trial cost");
+  double v = 0;
+  int64_t bad = 0;
+  if (points) {
+    // explicit points: evaluate on a scratch copy, device state untouched
+    DBuf saved;
+    PTRY(saved.alloc(std::max<int64_t>(c.n_lm_l, 1) * 24));
+    PCK(cudaMemcpyAsync(saved.p, c.points.p, c.n_lm_l * 24, cudaMemcpyDeviceToDevice, c.stream));
+    PTRY(poba::points_gather_from_host(c, points, c.points.as<double>()));
+    int st = poba::cost_device(c, trial != 0, &v, &bad);
+    cudaMemcpyAsync(c.points.p, saved.p, c.n_lm_l * 24, cudaMemcpyDeviceToDevice, c.stream);
+    cudaStreamSynchronize(c.stream);
+    PTRY(st);
+  } else {
+    NEED(c.have_points, "no device points");
+    PTRY(poba::cost_device(c, trial != 0, &v, &bad));
+  }
+  if (cost) *cost = v;
+  if (n_invalid) *n_invalid = bad;
+  return POBA_OK;
+}
+
+int poba_apply(poba_ctx* ctx, int op, const double* in, double* out) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(in && out, "null vectors");
+  NEED(c.have_lin, "no linearization");
+  const bool in_lm = (op == POBA_OP_W || op == POBA_OP_V_INV);
+  const bool out_lm = (op == POBA_OP_WT || op == POBA_OP_V_INV);
+  if (op != POBA_OP_W && op != POBA_OP_WT) NEED(c.have_damp, "no damped system");
+  DBuf din, dout;
+  PTRY(din.alloc((in_lm ? std::max<int64_t>(c.n_lm_l, 1) * 3 : c.n_cam * 9) * 8));
+  PTRY(dout.alloc((out_lm ? std::max<int64_t>(c.n_lm_l, 1) * 3 : c.n_cam * 9) * 8));
+  if (in_lm) PTRY(poba::points_gather_from_host(c, in, din.as<double>()));
+  else PCK(cudaMemcpyAsync(din.p, in, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
+  PTRY(poba::apply_op_device(c, op, din.as<double>(), dout.as<double>()));
+  if (op == POBA_OP_W && c.nranks > 1) PTRY(poba::allreduce_sum(c, dout.as<double>(), c.n_cam * 9));
+  if (out_lm) {
+    PTRY(poba::points_scatter_to_host(c, dout.as<double>(), out));
+  } else {
+    PCK(cudaMemcpyAsync(out, dout.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToHost, c.stream));
+    PCK(cudaStreamSynchronize(c.stream));
+  }
+  return POBA_OK;
+}
+
+int poba_read(poba_ctx* ctx, int what, double* dst) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(dst, "null output");
+  NEED(c.have_lin, "no linearization");
+  std::vector<double> h;
+  const int64_t nc = c.n_cam, nl = c.n_lm_l;
+  auto scatter_lm = [&](const std::vector<double>& src, int width) {
+    for (int64_t j = 0; j < nl; ++j)
+      std::memcpy(dst + (int64_t)ctx->lm_pt_host[j] * width, src.data() + j * width, width * 8);
+  };
+  auto lm_sym = [&](const DBuf& b) -> int {
+    PTRY(poba::copy_down(c, b, nl * 6 * 8, h));
+    std::vector<double> full(nl * 9);
+    for (int64_t j = 0; j < nl; ++j) poba::unpack3(h.data() + j * 6, full.data() + j * 9);
+    scatter_lm(full, 9);
+    return POBA_OK;
+  };
+  auto cam_sym = [&](const DBuf& b) -> int {
+    PTRY(poba::copy_down(c, b, nc * 45 * 8, h));
+    for (int64_t q = 0; q < nc; ++q) poba::unpack9(h.data() + q * 45, dst + q * 81);
+    return POBA_OK;
+  };
+  const bool damped = what == POBA_READ_U || what == POBA_READ_V || what == POBA_READ_U_INV ||
+                      what == POBA_READ_V_INV || what == POBA_READ_B_TILDE;
+  if (damped) NEED(c.have_damp, "no damped system");
+  switch (what) {
+    case POBA_READ_U0: return cam_sym(c.U0);
+    case POBA_READ_U: return cam_sym(c.Ud);
+    case POBA_READ_U_INV: return cam_sym(c.Uinv);
+    case POBA_READ_V0: return lm_sym(c.V0);
+    case POBA_READ_V: return lm_sym(c.Vd);
+    case POBA_READ_V_INV: return lm_sym(c.Vinv);
+    case POBA_READ_B_P:
+      PTRY(poba::copy_down(c, c.bp, nc * 72, h));
+      std::memcpy(dst, h.data(), nc * 72);
+      return POBA_OK;
+    case POBA_READ_D_P:
+      PTRY(poba::copy_down(c, c.Dp, nc * 72, h));
+      std::memcpy(dst, h.data(), nc * 72);
+      return POBA_OK;
+    case POBA_READ_B_L:
+      PTRY(poba::copy_down(c, c.bl, nl * 24, h));
+      scatter_lm(h, 3);
+      return POBA_OK;
+    case POBA_READ_D_L:
+      PTRY(poba::copy_down(c, c.Dl, nl * 24, h));
+      scatter_lm(h, 3);
+      return POBA_OK;
+    case POBA_READ_B_TILDE: {
+      // b_tilde = b_p - W V^-1 b_l (blocks.py:256-260), recomputed on demand
+      PTRY(poba::b_tilde_device(c));
+      PTRY(poba::copy_down(c, c.bt, nc * 72, h));
+      std::memcpy(dst, h.data(), nc * 72);
+      return POBA_OK;
+    }
+    case POBA_READ_STORAGE: {
+      const int64_t n = c.n_obs_l, pad = c.obs_pad;
+      std::vector<double> J((size_t)poba::kJPlanes * pad * 2), R(pad * 2);
+      PCK(cudaMemcpy(J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
+      PCK(cudaMemcpy(R.data(), c.Rz.p, R.size() * 8, cudaMemcpyDeviceToHost));
+      for (int64_t o = 0; o < n; ++o)
+        for (int a = 0; a < 2; ++a) {
+          double* row = dst + (o * 2 + a) * 13;
+          for (int j = 0; j < 12; ++j) row[j] = J[((size_t)j * pad + o) * 2 + a];
+          row[12] = R[o * 2 + a];
+        }
+      return POBA_OK;
+    }
+    default:
+      return poba::fail(POBA_EINVAL, "unknown read target");
+  }
+}
+
+int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_term_kernel, int* launches) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  NEED(reps > 0, "reps must be positive");
+  return poba::time_terms_device(c, reps, ms_per_term, ms_term_kernel, launches);
+}
+
+int64_t poba_launch_count(poba_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,523 @@
+// K1-K3 and K8: residual + analytic Jacobian, the landmark-major store, the
+// V0/b_l and U0/b_p reductions, Marquardt diagonals, and the cost.
+//
+// Reference (paths relative to /root/reference/pkg/src/powerba/):
+//   camera.evaluate            camera.py:67-135  (projection, residual, J_pose, J_point)
+//   camera.rotation_matrices   camera.py:49-51   (scipy from_rotvec().as_matrix())
+//   blocks.linearize           blocks.py:293-324 (store rows in canonical order)
+//   blocks._finish_linearization blocks.py:375-402 (U0, V0, b_p, b_l, D clamp)
+//   blocks.assemble_from_observations blocks.py:333-352
+//   lm.residual_cost           lm.py:107-119
+//
+// All reductions are in fp64 and in a fixed order (no floating-point
+// atomics), so every result is bitwise reproducible run to run.
+#include "poba_internal.h"
+
+namespace poba {
+
+namespace {
+
+constexpr double kMinDepth = 1e-12;   // camera.py:22
+constexpr double kClampLo = 1e-6;     // blocks.py:36
+constexpr double kClampHi = 1e6;      // blocks.py:37
+
+// Rotation matrix of an axis-angle vector through the unit quaternion, the
+// same construction scipy uses (from_rotvec -> as_matrix).
+__device__ void rotvec_to_matrix(double wx, double wy, double wz, double* R) {
+  const double a2 = wx * wx + wy * wy + wz * wz;
+  const double angle = sqrt(a2);
+  double scale;
+  if (angle <= 1e-3) {
+    scale = 0.5 - a2 / 48.0 + a2 * a2 / 3840.0;
+  } else {
+    scale = sin(angle / 2.0) / angle;
+  }
+  const double x = wx * scale, y = wy * scale, z = wz * scale, w = cos(angle / 2.0);
+  const double x2 = x * x, y2 = y * y, z2 = z * z, w2 = w * w;
+  const double xy = x * y, zw = z * w, xz = x * z, yw = y * w, yz = y * z, xw = x * w;
+  R[0] = x2 - y2 - z2 + w2;
+  R[1] = 2.0 * (xy - zw);
+  R[2] = 2.0 * (xz + yw);
+  R[3] = 2.0 * (xy + zw);
+  R[4] = -x2 + y2 - z2 + w2;
+  R[5] = 2.0 * (yz - xw);
+  R[6] = 2.0 * (xz - yw);
+  R[7] = 2.0 * (yz + xw);
+  R[8] = -x2 - y2 + z2 + w2;
+}
+
+__global__ void k_cam_prep(const double* __restrict__ cams, int64_t n_cam, double* __restrict__ prep) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n_cam) return;
+  const double* q = cams + c * 9;
+  double* o = prep + c * 16;
+  double R[9];
+  rotvec_to_matrix(q[0], q[1], q[2], R);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) o[i] = R[i];
+#pragma unroll
+  for (int i = 3; i < 9; ++i) o[i + 6] = q[i];
+  o[15] = 0.0;
+}
+
+struct ObsModel {
+  double r0, r1;
+  double jp0[9], jp1[9];  // J_pose rows
+  double jl0[3], jl1[3];  // J_point rows
+  bool valid;
+};
+
+// camera.evaluate for one observation (camera.py:85-135)
+template <bool kJac>
+__device__ __forceinline__ void evaluate_obs(const double* __restrict__ cp, double X0, double X1, double X2,
+                                             double2 pix, ObsModel& m) {
+  const double* R = cp;
+  const double P0 = R[0] * X0 + R[1] * X1 + R[2] * X2 + cp[9];
+  const double P1 = R[3] * X0 + R[4] * X1 + R[5] * X2 + cp[10];
+  const double P2 = R[6] * X0 + R[7] * X1 + R[8] * X2 + cp[11];
+  const double f = cp[12], k1 = cp[13], k2 = cp[14];
+  m.valid = fabs(P2) >= kMinDepth;
+  const double zs = m.valid ? P2 : 1.0;
+  const double p0 = -P0 / zs, p1 = -P1 / zs;
+  const double s = p0 * p0 + p1 * p1;
+  const double d = 1.0 + s * (k1 + k2 * s);
+  const double fd = f * d;
+  m.r0 = m.valid ? fd * p0 - pix.x : 0.0;
+  m.r1 = m.valid ? fd * p1 - pix.y : 0.0;
+  if (!kJac) return;
+  if (!m.valid) {
+#pragma unroll
+    for (int j = 0; j < 9; ++j) m.jp0[j] = m.jp1[j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) m.jl0[j] = m.jl1[j] = 0.0;
+    return;
+  }
+  const double iz = 1.0 / zs;
+  // dp/dP = [[-iz, 0, P0 iz^2], [0, -iz, P1 iz^2]]
+  const double e02 = P0 * iz * iz, e12 = P1 * iz * iz;
+  // dproj/dp = f (d I + p g^T), g = (2 k1 + 4 k2 s) p
+  const double gs = 2.0 * k1 + 4.0 * k2 * s;
+  const double g0 = gs * p0, g1 = gs * p1;
+  const double a00 = f * (d + p0 * g0), a01 = f * (p0 * g1);
+  const double a10 = f * (p1 * g0), a11 = f * (d + p1 * g1);
+  // A = dproj/dp @ dp/dP  (2x3)
+  const double A00 = -a00 * iz, A01 = -a01 * iz, A02 = a00 * e02 + a01 * e12;
+  const double A10 = -a10 * iz, A11 = -a11 * iz, A12 = a10 * e02 + a11 * e12;
+  // J_point = A R
+  m.jl0[0] = A00 * R[0] + A01 * R[3] + A02 * R[6];
+  m.jl0[1] = A00 * R[1] + A01 * R[4] + A02 * R[7];
+  m.jl0[2] = A00 * R[2] + A01 * R[5] + A02 * R[8];
+  m.jl1[0] = A10 * R[0] + A11 * R[3] + A12 * R[6];
+  m.jl1[1] = A10 * R[1] + A11 * R[4] + A12 * R[7];
+  m.jl1[2] = A10 * R[2] + A11 * R[5] + A12 * R[8];
+  // rotation (right increment): A (-R [X]x) = -(A R) [X]x
+  m.jp0[0] = -(m.jl0[1] * X2 - m.jl0[2] * X1);
+  m.jp0[1] = -(m.jl0[2] * X0 - m.jl0[0] * X2);
+  m.jp0[2] = -(m.jl0[0] * X1 - m.jl0[1] * X0);
+  m.jp1[0] = -(m.jl1[1] * X2 - m.jl1[2] * X1);
+  m.jp1[1] = -(m.jl1[2] * X0 - m.jl1[0] * X2);
+  m.jp1[2] = -(m.jl1[0] * X1 - m.jl1[1] * X0);
+  m.jp0[3] = A00; m.jp0[4] = A01; m.jp0[5] = A02;
+  m.jp1[3] = A10; m.jp1[4] = A11; m.jp1[5] = A12;
+  m.jp0[6] = d * p0;  m.jp1[6] = d * p1;
+  const double fs = f * s;
+  m.jp0[7] = fs * p0; m.jp1[7] = fs * p1;
+  m.jp0[8] = fs * s * p0; m.jp1[8] = fs * s * p1;
+}
+
+// Store + per-observation V0/b_l contributions + per-landmark sums (in
+// canonical order; matches np.add.at's sequential fold, blocks.py:394,396).
+template <bool kExplicit>
+__global__ void __launch_bounds__(kTile)
+k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const int* __restrict__ file_l,
+           const double2* __restrict__ pix_l, const double* __restrict__ prep,
+           const double* __restrict__ points, const double* __restrict__ ejp, const double* __restrict__ ejl,
+           const double* __restrict__ eres, double2* __restrict__ J, double2* __restrict__ Rz, int64_t pad,
+           double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
+           unsigned long long* __restrict__ n_invalid) {
+  __shared__ double contrib[kTile * 9];
+  __shared__ int bad_count;
+  const Tile t = tiles[blockIdx.x];
+  const int i = threadIdx.x;
+  if (i == 0) bad_count = 0;
+  __syncthreads();
+  if (i < t.n) {
+    const int o = t.obs0 + i;
+    ObsModel m;
+    if (kExplicit) {
+      const int f = file_l[o];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        m.jp0[j] = ejp[(int64_t)f * 18 + j];
+        m.jp1[j] = ejp[(int64_t)f * 18 + 9 + j];
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        m.jl0[j] = ejl[(int64_t)f * 6 + j];
+        m.jl1[j] = ejl[(int64_t)f * 6 + 3 + j];
+      }
+      m.r0 = eres[(int64_t)f * 2];
+      m.r1 = eres[(int64_t)f * 2 + 1];
+      m.valid = true;
+    } else {
+      const int lm = t.lm0 + (t.k > kTile ? 0 : i / t.k);
+      const double* X = points + (int64_t)lm * 3;
+      evaluate_obs<true>(prep + (int64_t)cam_l[o] * 16, X[0], X[1], X[2], pix_l[o], m);
+      if (!m.valid) atomicAdd(&bad_count, 1);
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) J[j * pad + o] = make_double2(m.jp0[j], m.jp1[j]);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) J[(9 + b) * pad + o] = make_double2(m.jl0[b], m.jl1[b]);
+    Rz[o] = make_double2(m.r0, m.r1);
+    double* cc = contrib + i * 9;
+    cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
+    cc[1] = m.jl0[0] * m.jl0[1] + m.jl1[0] * m.jl1[1];
+    cc[2] = m.jl0[0] * m.jl0[2] + m.jl1[0] * m.jl1[2];
+    cc[3] = m.jl0[1] * m.jl0[1] + m.jl1[1] * m.jl1[1];
+    cc[4] = m.jl0[1] * m.jl0[2] + m.jl1[1] * m.jl1[2];
+    cc[5] = m.jl0[2] * m.jl0[2] + m.jl1[2] * m.jl1[2];
+    cc[6] = m.jl0[0] * m.r0 + m.jl1[0] * m.r1;
+    cc[7] = m.jl0[1] * m.r0 + m.jl1[1] * m.r1;
+    cc[8] = m.jl0[2] * m.r0 + m.jl1[2] * m.r1;
+  }
+  __syncthreads();
+  if (i == 0 && bad_count) atomicAdd(n_invalid, (unsigned long long)bad_count);
+  if (t.k > kTile) return;  // long landmarks are reduced by k_lin_long
+  // (landmark, component) per thread
+  for (int q = i; q < t.nlm * 9; q += kTile) {
+    const int j = q / 9, comp = q - j * 9;
+    double acc = 0.0;
+    for (int r = 0; r < t.k; ++r) acc += contrib[(j * t.k + r) * 9 + comp];
+    const int lm = t.lm0 + j;
+    if (comp < 6) V0[(int64_t)lm * 6 + comp] = acc; else bl[(int64_t)lm * 3 + comp - 6] = acc;
+    if (comp == 0 || comp == 3 || comp == 5) {
+      const double c2 = fmin(fmax(acc, kClampLo * kClampLo), kClampHi * kClampHi);
+      Dl[(int64_t)lm * 3 + (comp == 0 ? 0 : comp == 3 ? 1 : 2)] = sqrt(c2);
+    }
+  }
+}
+
+// V0/b_l of landmarks longer than a tile, straight from the stored rows
+__global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restrict__ lm_off,
+                           const double2* __restrict__ J, const double2* __restrict__ Rz, int64_t pad,
+                           double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl) {
+  const int lm = long_lm[blockIdx.x];
+  const int o0 = lm_off[lm], o1 = lm_off[lm + 1];
+  const int comp = threadIdx.x;  // 9 threads
+  if (comp >= 9) return;
+  double acc = 0.0;
+  for (int o = o0; o < o1; ++o) {
+    const double2 a = J[(9 + 0) * pad + o], b = J[(9 + 1) * pad + o], c = J[(9 + 2) * pad + o];
+    const double2 r = Rz[o];
+    double v;
+    switch (comp) {
+      case 0: v = a.x * a.x + a.y * a.y; break;
+      case 1: v = a.x * b.x + a.y * b.y; break;
+      case 2: v = a.x * c.x + a.y * c.y; break;
+      case 3: v = b.x * b.x + b.y * b.y; break;
+      case 4: v = b.x * c.x + b.y * c.y; break;
+      case 5: v = c.x * c.x + c.y * c.y; break;
+      case 6: v = a.x * r.x + a.y * r.y; break;
+      case 7: v = b.x * r.x + b.y * r.y; break;
+      default: v = c.x * r.x + c.y * r.y; break;
+    }
+    acc += v;
+  }
+  if (comp < 6) V0[(int64_t)lm * 6 + comp] = acc; else bl[(int64_t)lm * 3 + comp - 6] = acc;
+  if (comp == 0 || comp == 3 || comp == 5) {
+    const double c2 = fmin(fmax(acc, kClampLo * kClampLo), kClampHi * kClampHi);
+    Dl[(int64_t)lm * 3 + (comp == 0 ? 0 : comp == 3 ? 1 : 2)] = sqrt(c2);
+  }
+}
+
+__device__ __forceinline__ int find_camera(const int* __restrict__ off, int n_cam, int cc) {
+  int lo = 0, hi = n_cam;  // last camera with off[c] <= cc
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (off[mid] <= cc) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// U0 (packed upper 45) and b_p (9) partial sums over chunks of <= 128 observations
+// of one camera, walked in camera-major order; fixed warp-butterfly reduction.
+__global__ void __launch_bounds__(256)
+k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cam_start,
+                   const int* __restrict__ cperm, const double2* __restrict__ J,
+                   const double2* __restrict__ Rz, int64_t pad, int n_cam, int n_cc,
+                   double* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_cc) return;
+  const int cam = find_camera(cc_cam_off, n_cam, warp);
+  const int p0 = cam_start[cam] + (warp - cc_cam_off[cam]) * kCamChunk;
+  const int p1 = min(p0 + kCamChunk, cam_start[cam + 1]);
+  double acc[54];
+#pragma unroll
+  for (int q = 0; q < 54; ++q) acc[q] = 0.0;
+  for (int p = p0 + lane; p < p1; p += 32) {
+    const int o = cperm[p];
+    double a[9], b[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const double2 v = J[j * pad + o];
+      a[j] = v.x;
+      b[j] = v.y;
+    }
+    const double2 r = Rz[o];
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int j = i; j < 9; ++j) acc[q++] += a[i] * a[j] + b[i] * b[j];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) acc[45 + i] += a[i] * r.x + b[i] * r.y;
+  }
+#pragma unroll
+  for (int q = 0; q < 54; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int s = 16; s; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+    acc[q] = v;
+  }
+  double* dst = out + (int64_t)warp * 54;
+#pragma unroll
+  for (int q = 0; q < 54; ++q)
+    if ((q & 31) == lane) dst[q] = acc[q];
+}
+
+// per camera: sum its chunk partials in chunk order -> U0 packed, b_p
+__global__ void k_cam_merge54(const int* __restrict__ cc_cam_off, const double* __restrict__ part, int n_cam,
+                              double* __restrict__ U0, double* __restrict__ bp) {
+  const int cam = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (cam >= n_cam) return;
+  const int c0 = cc_cam_off[cam], c1 = cc_cam_off[cam + 1];
+  for (int q = lane; q < 54; q += 32) {
+    double acc = 0.0;
+    for (int cc = c0; cc < c1; ++cc) acc += part[(int64_t)cc * 54 + q];
+    if (q < 45) U0[(int64_t)cam * 45 + q] = acc; else bp[(int64_t)cam * 9 + q - 45] = acc;
+  }
+}
+
+__device__ __forceinline__ int diag_index9(int i) { return i * 9 - i * (i - 1) / 2; }
+
+__global__ void k_cam_dp(const double* __restrict__ U0, int64_t n_cam, double* __restrict__ Dp) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_cam * 9) return;
+  const int64_t cam = q / 9;
+  const int i = (int)(q - cam * 9);
+  const double v = U0[cam * 45 + diag_index9(i)];
+  Dp[q] = sqrt(fmin(fmax(v, kClampLo * kClampLo), kClampHi * kClampHi));
+}
+
+// 0.5 sum ||r||^2 per tile (fixed tree), invalid counts
+__global__ void __launch_bounds__(kTile)
+k_cost_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const double2* __restrict__ pix_l,
+            const double* __restrict__ prep, const double* __restrict__ points,
+            const double* __restrict__ dl, double* __restrict__ tile_sum, unsigned long long* __restrict__ n_invalid) {
+  __shared__ double red[kTile];
+  __shared__ int bad_count;
+  const Tile t = tiles[blockIdx.x];
+  const int i = threadIdx.x;
+  if (i == 0) bad_count = 0;
+  __syncthreads();
+  double v = 0.0;
+  if (i < t.n) {
+    const int o = t.obs0 + i;
+    const int lm = t.lm0 + (t.k > kTile ? 0 : i / t.k);
+    double X0 = points[(int64_t)lm * 3], X1 = points[(int64_t)lm * 3 + 1], X2 = points[(int64_t)lm * 3 + 2];
+    if (dl) {
+      X0 += dl[(int64_t)lm * 3];
+      X1 += dl[(int64_t)lm * 3 + 1];
+      X2 += dl[(int64_t)lm * 3 + 2];
+    }
+    ObsModel m;
+    evaluate_obs<false>(prep + (int64_t)cam_l[o] * 16, X0, X1, X2, pix_l[o], m);
+    if (!m.valid) atomicAdd(&bad_count, 1);
+    v = m.r0 * m.r0 + m.r1 * m.r1;
+  }
+  red[i] = v;
+  __syncthreads();
+  for (int s = kTile / 2; s > 0; s >>= 1) {
+    if (i < s) red[i] += red[i + s];
+    __syncthreads();
+  }
+  if (i == 0) {
+    tile_sum[blockIdx.x] = red[0];
+    if (bad_count) atomicAdd(n_invalid, (unsigned long long)bad_count);
+  }
+}
+
+// fixed-order sum of n values by one CTA (strided partial sums, then a tree)
+__global__ void k_sum_fixed(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+  __shared__ double red[1024];
+  const int i = threadIdx.x;
+  double acc = 0.0;
+  for (int64_t q = i; q < n; q += blockDim.x) acc += v[q];
+  red[i] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (i < s) red[i] += red[i + s];
+    __syncthreads();
+  }
+  if (i == 0) out[0] = red[0];
+}
+
+__global__ void k_points_gather(const double* __restrict__ full, const int* __restrict__ lm_pt, int64_t n_lm,
+                                double* __restrict__ local) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_lm * 3) return;
+  const int64_t j = q / 3;
+  local[q] = full[(int64_t)lm_pt[j] * 3 + (q - j * 3)];
+}
+
+__global__ void k_points_scatter(const double* __restrict__ local, const int* __restrict__ lm_pt, int64_t n_lm,
+                                 double* __restrict__ full) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_lm * 3) return;
+  const int64_t j = q / 3;
+  full[(int64_t)lm_pt[j] * 3 + (q - j * 3)] = local[q];
+}
+
+}  // namespace
+
+int cameras_prep(Ctx& c, const double* d_cams, double* d_prep) {
+  k_cam_prep<<<grid_for(c.n_cam, 128), 128, 0, c.stream>>>(d_cams, c.n_cam, d_prep);
+  c.launches++;
+  PCK(cudaGetLastError());
+  return POBA_OK;
+}
+
+int points_gather_from_host(Ctx& c, const double* h_pts, double* d_local) {
+  PTRY(c.scratch_a.alloc(c.n_pt * 3 * 8));
+  PCK(cudaMemcpyAsync(c.scratch_a.p, h_pts, c.n_pt * 3 * 8, cudaMemcpyHostToDevice, c.stream));
+  k_points_gather<<<grid_for(c.n_lm_l * 3, 256), 256, 0, c.stream>>>(c.scratch_a.as<double>(), c.lm_pt.as<int>(),
+                                                                    c.n_lm_l, d_local);
+  c.launches++;
+  PCK(cudaGetLastError());
+  return POBA_OK;
+}
+
+int points_scatter_to_host(Ctx& c, const double* d_local, double* h_full) {
+  // host array is (n_pt, 3); only this shard's landmarks are written
+  PTRY(c.scratch_a.alloc(c.n_pt * 3 * 8));
+  PCK(cudaMemcpyAsync(c.scratch_a.p, h_full, c.n_pt * 3 * 8, cudaMemcpyHostToDevice, c.stream));
+  k_points_scatter<<<grid_for(c.n_lm_l * 3, 256), 256, 0, c.stream>>>(d_local, c.lm_pt.as<int>(), c.n_lm_l,
+                                                                     c.scratch_a.as<double>());
+  c.launches++;
+  PCK(cudaMemcpyAsync(h_full, c.scratch_a.p, c.n_pt * 3 * 8, cudaMemcpyDeviceToHost, c.stream));
+  PCK(cudaStreamSynchronize(c.stream));
+  return POBA_OK;
+}
+
+int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, const double* h_res) {
+  cudaStream_t s = c.stream;
+  const int64_t pad = c.obs_pad;
+  DBuf ejp, ejl, eres;
+  if (expl) {
+    PTRY(ejp.alloc(c.n_obs * 18 * 8));
+    PTRY(ejl.alloc(c.n_obs * 6 * 8));
+    PTRY(eres.alloc(c.n_obs * 2 * 8));
+    PCK(cudaMemcpyAsync(ejp.p, h_jp, c.n_obs * 18 * 8, cudaMemcpyHostToDevice, s));
+    PCK(cudaMemcpyAsync(ejl.p, h_jl, c.n_obs * 6 * 8, cudaMemcpyHostToDevice, s));
+    PCK(cudaMemcpyAsync(eres.p, h_res, c.n_obs * 2 * 8, cudaMemcpyHostToDevice, s));
+  } else {
+    PTRY(cameras_prep(c, c.cams.as<double>(), c.cams_prep.as<double>()));
+  }
+  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 32);
+  PCK(cudaMemsetAsync(d_bad, 0, 8, s));
+  if (expl)
+    k_lin_tile<true><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.file_l.as<int>(),
+                                                 c.pix_l.as<double2>(), nullptr, nullptr, ejp.as<double>(),
+                                                 ejl.as<double>(), eres.as<double>(), c.J.as<double2>(),
+                                                 c.Rz.as<double2>(), pad, c.V0.as<double>(), c.bl.as<double>(),
+                                                 c.Dl.as<double>(), d_bad);
+  else
+    k_lin_tile<false><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.file_l.as<int>(),
+                                                  c.pix_l.as<double2>(), c.cams_prep.as<double>(),
+                                                  c.points.as<double>(), nullptr, nullptr, nullptr,
+                                                  c.J.as<double2>(), c.Rz.as<double2>(), pad, c.V0.as<double>(),
+                                                  c.bl.as<double>(), c.Dl.as<double>(), d_bad);
+  c.launches++;
+  PCK(cudaGetLastError());
+  if (c.n_long) {
+    k_lin_long<<<c.n_long, 32, 0, s>>>(c.long_lm.as<int>(), c.lm_off.as<int>(), c.J.as<double2>(),
+                                       c.Rz.as<double2>(), pad, c.V0.as<double>(), c.bl.as<double>(),
+                                       c.Dl.as<double>());
+    c.launches++;
+  }
+  // camera side: U0 / b_p via camera-major chunks, then a fixed-order merge
+  if (c.n_cchunks) {
+    k_cam_chunk_reduce<<<grid_for((int64_t)c.n_cchunks * 32, 256), 256, 0, s>>>(
+        c.cc_cam_off.as<int>(), c.cc_start.as<int>(), c.cperm.as<int>(), c.J.as<double2>(), c.Rz.as<double2>(),
+        pad, (int)c.n_cam, c.n_cchunks, c.cc_part.as<double>());
+    c.launches++;
+  }
+  k_cam_merge54<<<grid_for(c.n_cam * 32, 256), 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_part.as<double>(),
+                                                            (int)c.n_cam, c.U0.as<double>(), c.bp.as<double>());
+  c.launches++;
+  PCK(cudaGetLastError());
+  if (c.nranks > 1) {
+    PTRY(allreduce_sum(c, c.U0.as<double>(), c.n_cam * 45));
+    PTRY(allreduce_sum(c, c.bp.as<double>(), c.n_cam * 9));
+  }
+  k_cam_dp<<<grid_for(c.n_cam * 9, 256), 256, 0, s>>>(c.U0.as<double>(), c.n_cam, c.Dp.as<double>());
+  c.launches++;
+  unsigned long long bad = 0;
+  PCK(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, s));
+  PCK(cudaStreamSynchronize(s));
+  if (c.nranks > 1) {
+    double b = (double)bad;
+    PTRY(c.scratch_b.alloc(8));
+    PCK(cudaMemcpyAsync(c.scratch_b.p, &b, 8, cudaMemcpyHostToDevice, s));
+    PTRY(allreduce_sum(c, c.scratch_b.as<double>(), 1));
+    PCK(cudaMemcpyAsync(&b, c.scratch_b.p, 8, cudaMemcpyDeviceToHost, s));
+    PCK(cudaStreamSynchronize(s));
+    bad = (unsigned long long)b;
+  }
+  c.n_invalid = (int64_t)bad;
+  c.have_lin = true;
+  c.have_damp = c.have_solution = c.have_delta_l = false;
+  return POBA_OK;
+}
+
+int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid) {
+  cudaStream_t s = c.stream;
+  PTRY(c.scratch_c.alloc((c.n_tiles + 8) * 8));
+  unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 40);
+  PCK(cudaMemsetAsync(d_bad, 0, 8, s));
+  k_cost_tile<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.pix_l.as<double2>(),
+                                          c.trial_prep.as<double>(), c.points.as<double>(),
+                                          trial ? c.dl.as<double>() : nullptr, c.scratch_c.as<double>(), d_bad);
+  k_sum_fixed<<<1, 1024, 0, s>>>(c.scratch_c.as<double>(), c.n_tiles, c.red.as<double>());
+  c.launches += 2;
+  PCK(cudaGetLastError());
+  double sum = 0;
+  unsigned long long bad = 0;
+  PCK(cudaMemcpyAsync(&sum, c.red.p, 8, cudaMemcpyDeviceToHost, s));
+  PCK(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, s));
+  PCK(cudaStreamSynchronize(s));
+  if (c.nranks > 1) {
+    // per-rank partials gathered and summed in rank order (deterministic)
+    std::vector<double> mine = {sum, (double)bad};
+    PTRY(c.scratch_b.alloc(2 * 8 * (c.nranks + 1)));
+    PCK(cudaMemcpyAsync(c.scratch_b.p, mine.data(), 16, cudaMemcpyHostToDevice, s));
+    PNCCL(AllGather(c.scratch_b.p, c.scratch_b.as<double>() + 2, 2, ncclFloat64, c.comm, s));
+    std::vector<double> all(2 * c.nranks);
+    PCK(cudaMemcpyAsync(all.data(), c.scratch_b.as<double>() + 2, 16 * c.nranks, cudaMemcpyDeviceToHost, s));
+    PCK(cudaStreamSynchronize(s));
+    sum = 0;
+    bad = 0;
+    for (int r = 0; r < c.nranks; ++r) {
+      sum += all[2 * r];
+      bad += (unsigned long long)all[2 * r + 1];
+    }
+  }
+  *cost = 0.5 * sum;
+  *n_invalid = (int64_t)bad;
+  return POBA_OK;
+}
+
+}  // namespace poba

@@ -1,0 +1,104 @@
+"""CPU-only checks: the C-ABI library loads and exports its header, host logic,
+generators, error contract of the host layer.  No kernel is launched here."""
+from __future__ import annotations
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import REPO
+
+
+def header_symbols():
+    txt = open(os.path.join(REPO, "include", "poba.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(poba_\w+)\s*\(", txt, re.M)))
+
+
+def test_library_loads_and_exports_header():
+    from paper_2204_12834_b200 import _lib
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+    assert lib.poba_version() == 1
+
+
+def test_library_is_sm100a():
+    so = os.path.join(REPO, "paper_2204_12834_b200", "lib", "libpoba.so")
+    data = open(so, "rb").read()
+    assert b"sm_100a" in data
+
+
+def test_no_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    from paper_2204_12834_b200 import _lib
+    with pytest.raises(_lib.PobaError):
+        _lib.Device(0)
+
+
+def test_problem_validation_messages():
+    from paper_2204_12834_b200.problem import Problem
+    cams = np.zeros((2, 9))
+    pts = np.zeros((2, 3))
+    with pytest.raises(ValueError, match="duplicate"):
+        Problem(cams, pts, [0, 0, 1, 1], [0, 0, 1, 0], np.zeros((4, 2)))
+    with pytest.raises(ValueError, match="every camera"):
+        Problem(cams, pts, [0, 0], [0, 1], np.zeros((2, 2)))
+    with pytest.raises(ValueError, match="every point"):
+        Problem(cams, pts, [0, 1], [0, 0], np.zeros((2, 2)))
+    with pytest.raises(ValueError, match="out of range"):
+        Problem(cams, pts, [0, 2], [0, 1], np.zeros((2, 2)))
+
+
+@pytest.mark.parametrize("name,scale", [("c1", 1.0), ("c2", 1.0), ("c3", 0.05), ("c4", 0.01), ("c5", 0.005)])
+def test_generators_are_valid_and_deterministic(name, scale):
+    from paper_2204_12834_b200 import configs
+    a = configs.make_config(name, scale)
+    b = configs.make_config(name, scale)
+    assert a.fingerprint() == b.fingerprint()
+    k = np.bincount(a.pt_indices, minlength=a.n_points)
+    assert k.min() >= 2 or name == "c5"
+    # every observation in front of its camera at the generating geometry: the
+    # perturbed state must still evaluate finite residuals
+    from oracle import poba_oracle as O
+    c, bad = O.cost(a.cam_indices, a.pt_indices, a.pixels, a.camera_params, a.points)
+    assert np.isfinite(c) and bad == 0
+
+
+def test_track_statistics_match_configs():
+    from paper_2204_12834_b200 import configs
+    p1 = configs.make_config("c1")
+    assert p1.n_cameras == 16 and p1.n_points == 1000
+    assert 3.6 < p1.n_observations / p1.n_points < 4.4      # 2 + Poisson(2), clipped
+    p2 = configs.make_config("c2")
+    assert p2.n_cameras == 49 and p2.n_points == 7776
+    assert 31_000 < p2.n_observations < 32_600              # "about 31,800"
+
+
+def test_power_series_rejects_non_device_systems():
+    from paper_2204_12834_b200 import power_series
+
+    class Mini:
+        pass
+    with pytest.raises(TypeError):
+        power_series.power_series_solve(Mini())
+    with pytest.raises(ValueError, match="max_order"):
+        power_series.power_series_solve(Mini(), max_order=-1)
+
+
+def test_host_stop_criterion():
+    from paper_2204_12834_b200.power_series import stop_criterion
+    assert stop_criterion(np.array([1.0, 0.0]), np.array([1.0, 0.004]), 1, 0.01)
+    assert not stop_criterion(np.array([1.0, 0.0]), np.array([1.0, 0.004]), 3, 0.01)
+
+
+def test_lm_config_validation():
+    from paper_2204_12834_b200 import LmConfig
+    with pytest.raises(ValueError, match="unknown solver"):
+        LmConfig(solver="sgd")

@@ -1,0 +1,259 @@
+"""GPU parity: libpoba (through the C-ABI) against the reference's golden outputs.
+
+Contract (BASELINE.json north_star): ordering bit-exact; increments within
+1e-9 relative (fp64); per-LM-iteration cost within 1e-8 relative.  Golden
+values come from running the reference itself (tests/golden/make_golden.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden_problem, load_golden
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = ["rand3x5", "noisy4x60", "rig49", "c1", "c2"]
+INC_TOL = 1e-9     # increments, relative (north star)
+COST_TOL = 1e-8    # per-LM cost, relative (north star)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    d = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (d if d else 1.0)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2204_12834_b200 as pkg
+    return pkg
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_ordering_bit_exact(P, name):
+    p, z = golden_problem(name)
+    lin = P.linearize(p)
+    st = lin.store
+    assert np.array_equal(st.order, z["order"])
+    assert np.array_equal(st.cam_sorted, z["cam_sorted"])
+    assert np.array_equal(st.pt_sorted, z["pt_sorted"])
+    g = st.groups
+    assert [x.k for x in g] == z["group_k"].tolist()
+    assert [x.obs_start for x in g] == z["group_start"].tolist()
+    assert [x.n for x in g] == z["group_n"].tolist()
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_linearization(P, name):
+    p, z = golden_problem(name)
+    lin = P.linearize(p)
+    for key in ("U0", "V0", "b_p", "b_l", "D_p", "D_l"):
+        assert rel(getattr(lin, key), z[key]) < 1e-11, key
+    assert lin.n_invalid == int(z["n_invalid"])
+    if "storage" in z:
+        st = lin.store.storage_obs
+        assert np.abs(st - z["storage"]).max() <= 1e-11 * np.abs(z["storage"]).max()
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_damped_system_and_series(P, name):
+    p, z = golden_problem(name)
+    lin = P.linearize(p)
+    j = 0
+    while f"lam{j}" in z:
+        s = lin.damp(float(z[f"lam{j}"]))
+        assert rel(s.b_tilde(), z[f"sys{j}_b_tilde"]) < INC_TOL
+        assert rel(s.V_inv, z[f"sys{j}_V_inv"]) < 1e-9
+        # U^-1 entries inherit kappa(U) ~ 1e8; compare as an operator on U
+        Ut = np.einsum("pij,pjk->pik", s.U, z[f"sys{j}_U_inv"])
+        assert np.abs(Ut - np.eye(9)[None]).max() < 1e-5
+        i = 0
+        while f"sys{j}_solve{i}_eps" in z:
+            pre = f"sys{j}_solve{i}_"
+            r = P.power_series_solve(s, float(z[pre + "eps"]), int(z[pre + "m"]))
+            assert r.order_used == int(z[pre + "order"]), (name, j, i)
+            assert r.converged == bool(z[pre + "converged"])
+            assert rel(r.delta_p, z[pre + "delta_p"]) < INC_TOL, (name, j, i, rel(r.delta_p, z[pre + "delta_p"]))
+            dl = P.back_substitute(s, r.delta_p)
+            assert rel(dl, z[pre + "delta_l"]) < INC_TOL
+            i += 1
+        j += 1
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_cost(P, name):
+    p, z = golden_problem(name)
+    c, bad = P.residual_cost(p, P.BaState.from_problem(p))
+    assert abs(c - z["cost0"][0]) <= 1e-12 * z["cost0"][0]
+    assert bad == int(z["cost0"][1])
+
+
+@pytest.mark.parametrize("name,tag,kw", [
+    ("rand3x5", "lm_poba", {}),
+    ("noisy4x60", "lm_poba", {}),
+    ("rig49", "lm_poba", dict(max_outer_iterations=50)),
+    ("c1", "lm_c1", dict(max_outer_iterations=10, max_order=32)),
+    ("c2", "lm_c2", dict(max_outer_iterations=20, max_order=32, epsilon=1e-6)),
+])
+def test_lm_trace(P, name, tag, kw):
+    p, z = golden_problem(name)
+    tr = P.run(p, P.LmConfig(**kw))
+    costs = np.array([i.cost for i in tr.iterations])
+    want = z[tag + "_cost"]
+    assert len(costs) == len(want)
+    assert np.all(np.abs(costs - want) <= COST_TOL * want)
+    assert [i.accepted for i in tr.iterations] == z[tag + "_accepted"].tolist()
+    assert [i.order_m for i in tr.iterations] == z[tag + "_order"].tolist()
+    assert [i.lam for i in tr.iterations] == z[tag + "_lam"].tolist()
+    assert [i.peak_bytes for i in tr.iterations] == z[tag + "_peak_bytes"].tolist()
+    assert tr.converged == bool(z[tag + "_converged"])
+
+
+def test_rig49_end_to_end_golden(P):
+    """Reference criterion 6 golden (pkg/test_output.txt:19): final cost 7584.4992."""
+    p, _ = golden_problem("rig49")
+    tr = P.run(p, P.LmConfig(max_outer_iterations=50))
+    assert round(tr.final_cost, 4) == 7584.4992
+
+
+def test_explicit_systems(P):
+    z = load_golden("explicit")
+    for j in range(4):
+        pre = f"e{j}_"
+        lin = P.assemble_from_observations(z[pre + "cam_idx"], z[pre + "pt_idx"], z[pre + "jp"], z[pre + "jl"],
+                                           z[pre + "res"], int(z[pre + "n_cam"]), int(z[pre + "n_pt"]))
+        assert np.array_equal(lin.store.cam_sorted, z[pre + "cam_sorted"])
+        assert np.array_equal(lin.store.pt_sorted, z[pre + "pt_sorted"])
+        for key in ("U0", "V0", "b_p", "b_l", "D_p", "D_l"):
+            assert rel(getattr(lin, key), z[pre + key]) < 1e-12, key
+        s = lin.damp(float(z[pre + "lam"]))
+        i = 0
+        while f"{pre}sys_solve{i}_eps" in z:
+            q = f"{pre}sys_solve{i}_"
+            r = P.power_series_solve(s, float(z[q + "eps"]), int(z[q + "m"]))
+            assert r.order_used == int(z[q + "order"]) and r.converged == bool(z[q + "converged"])
+            assert rel(r.delta_p, z[q + "delta_p"]) < INC_TOL
+            assert rel(P.back_substitute(s, r.delta_p), z[q + "delta_l"]) < INC_TOL
+            i += 1
+
+
+def test_decoupled_system_stops_at_order_one(P):
+    # reference tests/test_power_series.py:82-94
+    z = load_golden("explicit")
+    lin = P.assemble_from_observations(z["dec_cam_idx"], z["dec_pt_idx"], z["dec_jp"], z["dec_jl"],
+                                       z["dec_res"], 2, 3)
+    s = lin.damp(1e-2)
+    r = P.power_series_solve(s, epsilon=1e-12)
+    assert r.converged and r.order_used == 1
+    assert np.array_equal(r.delta_p, s.apply_u_inv(-s.b_tilde()))
+    assert rel(r.delta_p, z["dec_delta_p"]) < 1e-13
+
+
+def test_operators_match_oracle(P):
+    from oracle import poba_oracle as O
+    p, _ = golden_problem("noisy4x60")
+    s = P.assemble(p, lam=1e-2)
+    lin_o = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points)
+    so = O.OracleSystem(lin_o, 1e-2)
+    rng = np.random.default_rng(0)
+    u = rng.normal(size=s.n_pose_params)
+    v = rng.normal(size=s.n_point_params)
+    assert rel(s.apply_w(v), so.apply_w(v)) < 1e-12
+    assert rel(s.apply_wt(u), so.apply_wt(u)) < 1e-12
+    assert rel(s.apply_v_inv(v), so.apply_v_inv(v)) < 1e-12
+    assert rel(s.apply_u(u), so.apply_u(u)) < 1e-12
+    assert rel(s.apply_schur(u), so.apply_schur(u)) < 1e-10
+    # adjointness (reference tests/test_blocks.py:84-91)
+    left, right = u @ s.apply_w(v), s.apply_wt(u) @ v
+    assert abs(left - right) <= 1e-10 * max(abs(left), 1.0)
+
+
+def test_pass_counters(P):
+    # reference tests/test_power_series.py:153-162
+    z = load_golden("explicit")
+    lin = P.assemble_from_observations(z["e3_cam_idx"], z["e3_pt_idx"], z["e3_jp"], z["e3_jl"], z["e3_res"],
+                                       int(z["e3_n_cam"]), int(z["e3_n_pt"]))
+    s = lin.damp(1e-2)
+    s.b_tilde()
+    s.counters.reset()
+    r = P.power_series_solve(s, epsilon=1e-300, max_order=6)
+    c = s.counters
+    assert r.order_used == 6 and (c.w, c.wt, c.v_inv, c.u_inv) == (6, 6, 6, 7)
+
+
+def test_run_to_run_bitwise(P):
+    p, _ = golden_problem("c2")
+    s = P.assemble(p, lam=1e-4)
+    a = P.power_series_solve(s, 1e-300, 16)
+    b = P.power_series_solve(s, 1e-300, 16)
+    assert np.array_equal(a.delta_p, b.delta_p)
+    assert np.array_equal(P.back_substitute(s, a.delta_p), P.back_substitute(s, b.delta_p))
+
+
+def test_permutation_invariance(P):
+    # reference tests/test_blocks.py:197-223
+    p, _ = golden_problem("noisy4x60")
+    q = p.copy()
+    perm = np.random.default_rng(13).permutation(p.n_observations)
+    q.cam_indices, q.pt_indices, q.pixels = q.cam_indices[perm], q.pt_indices[perm], q.pixels[perm]
+    a, b = P.linearize(p), P.linearize(q)
+    assert np.array_equal(a.store.storage_obs, b.store.storage_obs)
+    assert np.array_equal(a.U0, b.U0) and np.array_equal(a.b_p, b.b_p)
+    ra = P.power_series_solve(a.damp(1.0), max_order=10)
+    rb = P.power_series_solve(b.damp(1.0), max_order=10)
+    assert np.array_equal(ra.delta_p, rb.delta_p)
+
+
+def test_error_contract(P):
+    p, _ = golden_problem("rand3x5")
+    lin = P.linearize(p)
+    with pytest.raises(ValueError, match="non-negative"):
+        lin.damp(-1e-3)
+    with pytest.raises(ValueError, match="damping"):
+        lin.damp(0.1, damping="levenberg")
+    with pytest.raises(ValueError, match="precision"):
+        P.linearize(p, precision=16)
+    with pytest.raises(ValueError, match="max_order"):
+        P.power_series_solve(lin.damp(1e-2), max_order=-1)
+    rng = np.random.default_rng(8)
+    jp = rng.normal(size=(5, 2, 9))
+    bad = P.assemble_from_observations([0] * 5, list(range(5)), jp, np.zeros((5, 2, 3)),
+                                       rng.normal(size=(5, 2)), 1, 5)
+    with pytest.raises(ValueError, match="point blocks are not positive definite"):
+        bad.damp(0.0)
+    bad.damp(1e-2)
+    with pytest.raises(ValueError, match="camera"):
+        P.assemble_from_observations([0], [0], np.zeros((1, 2, 9)), np.zeros((1, 2, 3)), np.zeros((1, 2)), 2, 1)
+    with pytest.raises(ValueError, match="point"):
+        P.assemble_from_observations([0], [0], np.zeros((1, 2, 9)), np.zeros((1, 2, 3)), np.zeros((1, 2)), 1, 2)
+
+
+def test_identity_damping_and_clamp(P):
+    # reference tests/test_blocks.py:240-265
+    p, _ = golden_problem("rand3x5")
+    lin = P.linearize(p)
+    s = lin.damp(0.5, damping="identity")
+    di = np.arange(9)
+    assert np.array_equal(s.U[:, di, di], lin.U0[:, di, di] + 0.5)
+    jp = np.zeros((2, 2, 9))
+    jp[:, :, 0] = 1e7
+    jp[:, 0, 1:8] = 1.0
+    jl = np.tile(np.eye(3)[:2][None], (2, 1, 1))
+    lin2 = P.assemble_from_observations([0, 0], [0, 1], jp, jl, np.ones((2, 2)), 1, 2)
+    assert lin2.D_p[0, 0] == 1e6 and lin2.D_p[0, 8] == 1e-6
+
+
+def test_zero_rhs_and_zero_update(P):
+    from paper_2204_12834_b200 import configs
+    # exact synthetic data: zero residuals -> zero gradient -> zero rhs (reference tests/test_lm.py:25-33)
+    p, _ = golden_problem("rand3x5")
+    lin = P.assemble_from_observations(p.cam_indices, p.pt_indices,
+                                       np.random.default_rng(1).normal(size=(p.n_observations, 2, 9)),
+                                       np.random.default_rng(2).normal(size=(p.n_observations, 2, 3)),
+                                       np.zeros((p.n_observations, 2)), p.n_cameras, p.n_points)
+    s = lin.damp(1e-2)
+    r = P.power_series_solve(s)
+    assert r.converged and r.order_used == 0 and not r.delta_p.any()
+    assert not P.back_substitute(s, r.delta_p).any()
+    del configs
