@@ -148,7 +148,7 @@ class Device:
     def info(self) -> dict:
         v = np.zeros(16, dtype=np.int64)
         _check(self._lib.poba_problem_info(self._h, _i64(v)))
-        keys = ("n_groups", "n_tiles", "n_chunks", "n_partials", "obs_lo", "obs_hi", "lm_lo", "lm_hi",
+        keys = ("n_groups", "n_tiles", "n_chunks", "n_partials", "n_obs_local", "n_slots", "lm_lo", "lm_hi",
                 "max_slots", "n_long", "device_bytes", "k_max", "n_cam", "n_pt", "n_obs", "rank")
         return dict(zip(keys, (int(x) for x in v)))
 
@@ -237,8 +237,7 @@ class Device:
                   READ_B_P: (9 * self.n_cam,), READ_B_L: (3 * self.n_pt,), READ_D_P: (self.n_cam, 9),
                   READ_D_L: (self.n_pt, 3), READ_B_TILDE: (9 * self.n_cam,)}
         if what == READ_STORAGE:
-            info = self.info()
-            shape = (info["obs_hi"] - info["obs_lo"], 2, 13)
+            shape = (self.n_obs, 2, 13)
         else:
             shape = shapes[what]
         out = np.zeros(shape)

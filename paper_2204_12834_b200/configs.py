@@ -10,9 +10,10 @@ camera (negative camera-frame z, reference ``synthetic.py:17-31``).
 
 Interpretation choices (recorded in DESIGN.md):
   * "k1/k2 ~ N(0, 1e-3)" is read as standard deviation 1e-3.
-  * "0.01 rad rotation" perturbation is a right-multiplied random rotation with
-    per-axis standard deviation 0.01 (the reference ``perturb`` never touches
-    rotations, ``bal_io.py:297-312``; the configs ask for it).
+  * "0.01 rad rotation / 0.05 translation": each camera is turned by a
+    right-multiplied random rotation (per-axis standard deviation 0.01) about its
+    own centre, and its centre moved by N(0, 0.05^2 I) (the reference ``perturb``
+    never touches rotations, ``bal_io.py:297-312``; the configs ask for it).
   * Landmark indices are emitted in a spatially coherent order (sorted along
     the scene), and observations in BAL file order (camera, then point).
 """
@@ -25,7 +26,9 @@ from scipy.spatial.transform import Rotation
 
 from .problem import Problem
 
-MIN_DEPTH = 0.25  # generator-side margin, far above the model's 1e-12 validity floor
+# generator-side depth margin: every observed point is at least this far in front of
+# its camera, so the 0.01 rad / 0.05 perturbation cannot push it near the image plane
+MIN_DEPTH = 1.0
 
 
 @dataclass(frozen=True)
@@ -149,10 +152,18 @@ def _finish(name, cams_true, X_true, cam_idx, pt_idx, rng, *, outlier_frac=0.0,
     if outlier_frac > 0:
         out = rng.random(len(cam_idx)) < outlier_frac
         px[out] += rng.uniform(-outlier_px, outlier_px, (int(out.sum()), 2))
+    # initial state: orientation perturbed by a right-multiplied rotation about the
+    # camera's own centre and the centre moved by N(0, t_sigma) (with the BAL
+    # parameterization P = R X + t, perturbing R at fixed t would swing the
+    # centre about the world origin by |C| * angle)
     cams = cams_true.copy()
     delta = rng.normal(0.0, rot_sigma, (len(cams), 3))
-    cams[:, 0:3] = (Rotation.from_rotvec(cams[:, 0:3]) * Rotation.from_rotvec(delta)).as_rotvec()
-    cams[:, 3:6] += rng.normal(0.0, t_sigma, (len(cams), 3))
+    r0 = Rotation.from_rotvec(cams[:, 0:3])
+    centre = -np.einsum("nji,nj->ni", r0.as_matrix(), cams[:, 3:6])
+    r1 = r0 * Rotation.from_rotvec(delta)
+    centre = centre + rng.normal(0.0, t_sigma, (len(cams), 3))
+    cams[:, 0:3] = r1.as_rotvec()
+    cams[:, 3:6] = -np.einsum("nij,nj->ni", r1.as_matrix(), centre)
     pts = X_true + rng.normal(0.0, pt_sigma, X_true.shape)
     return Problem(cams, pts, cam_idx, pt_idx, px, name=name)
 
@@ -417,7 +428,7 @@ def make_city(n_cameras=13_700, n_points=4_500_000, seed=0, extent=200.0, street
         dz = Xb[:, None, 2].astype(np.float32) - np.float32(1.5)
         r2 = dx * dx + dy * dy
         along_fwd = dx * hxy32[cand, 0] + dy * hxy32[cand, 1]
-        vis = (inside & (cnt > 0) & (r2 <= np.float32(max_range ** 2)) & (r2 >= np.float32(1.0))
+        vis = (inside & (cnt > 0) & (r2 <= np.float32(max_range ** 2)) & (along_fwd >= np.float32(2.0))
                & (along_fwd > np.float32(cos_h) * np.sqrt(r2))
                & (np.abs(dz) < np.float32(tan_vm) * along_fwd))
         # compact the first 32 visible candidates per point before de-duplicating

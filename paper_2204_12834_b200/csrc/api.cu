@@ -11,7 +11,6 @@
 
 struct poba_ctx {
   poba::Ctx c;
-  std::vector<int> lm_pt_host;  // local landmark -> point id (host copy)
 };
 
 namespace poba {
@@ -86,6 +85,19 @@ void unpack9(const double* p45, double* out81) {
 void unpack3(const double* p6, double* out9) {
   const int idx[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
   for (int q = 0; q < 9; ++q) out9[q] = p6[idx[q]];
+}
+
+// landmark arrays: this rank owns points [lm_lo, lm_hi); host arrays are full (n_pt rows)
+int lm_upload(Ctx& c, const double* host_full, int width, double* d_local) {
+  if (c.n_lm_l == 0) return POBA_OK;
+  PCK(cudaMemcpyAsync(d_local, host_full + c.lm_lo * width, c.n_lm_l * width * 8, cudaMemcpyHostToDevice, c.stream));
+  return POBA_OK;
+}
+int lm_download(Ctx& c, const double* d_local, int width, double* host_full) {
+  if (c.n_lm_l == 0) return POBA_OK;
+  PCK(cudaMemcpyAsync(host_full + c.lm_lo * width, d_local, c.n_lm_l * width * 8, cudaMemcpyDeviceToHost, c.stream));
+  PCK(cudaStreamSynchronize(c.stream));
+  return POBA_OK;
 }
 
 int copy_down(Ctx& c, const DBuf& src, size_t bytes, std::vector<double>& out) {
@@ -188,8 +200,6 @@ int poba_set_problem(poba_ctx* ctx, int64_t n_cam, int64_t n_pt, int64_t n_obs, 
   c.n_obs = n_obs;
   c.have_problem = false;
   PTRY(poba::build_structure(c, cam_idx, pt_idx, pixels));
-  ctx->lm_pt_host.resize(c.n_lm_l);
-  PCK(cudaMemcpy(ctx->lm_pt_host.data(), c.lm_pt.p, c.n_lm_l * 4, cudaMemcpyDeviceToHost));
   return POBA_OK;
 }
 
@@ -198,15 +208,16 @@ int poba_problem_info(poba_ctx* ctx, int64_t* info) {
   NEED(info, "null output");
   const Ctx& c = ctx->c;
   size_t bytes = 0;
-  for (const DBuf* b : {&c.order, &c.cam_file, &c.pt_file, &c.cam_l, &c.pix_l, &c.file_l, &c.lm_pt, &c.lm_off,
-                        &c.pt_to_lm, &c.tiles, &c.chunks, &c.perm, &c.seg_start, &c.seg_slot, &c.part_cam_off,
-                        &c.part_idx, &c.cperm, &c.cc_start, &c.cc_cam_off, &c.J, &c.Rz, &c.cams, &c.cams_prep,
-                        &c.U0, &c.bp, &c.Dp, &c.Uinv, &c.Ud, &c.bt, &c.tvec, &c.xvec, &c.rvec, &c.cc_part,
-                        &c.partials, &c.points, &c.V0, &c.bl, &c.Dl, &c.Vinv, &c.Vd, &c.dl, &c.ltmp})
+  for (const DBuf* b : {&c.cam_file, &c.pt_file, &c.kpt, &c.order, &c.tiles, &c.chunks, &c.work, &c.cam_s, &c.file_s,
+                        &c.pix_s, &c.lidx_s, &c.perm_s, &c.lm_slot0, &c.lm_k, &c.seg_start, &c.seg_slot,
+                        &c.part_cam_off, &c.part_idx, &c.long_lm, &c.cperm, &c.cam_start, &c.cc_cam_off, &c.J,
+                        &c.Rz, &c.cams, &c.cams_prep, &c.cams_trial, &c.trial_prep, &c.U0, &c.bp, &c.Dp, &c.Uinv,
+                        &c.Ud, &c.bt, &c.tvec, &c.xvec, &c.rvec, &c.cc_part, &c.partials, &c.points, &c.V0, &c.bl,
+                        &c.Dl, &c.Vinv, &c.Vd, &c.dl, &c.ltmp, &c.ctmp, &c.ctmp2})
     bytes += b->bytes;
-  const int64_t v[16] = {(int64_t)c.grp_k.size(), c.n_tiles, c.n_chunks, c.n_partials, c.obs_lo, c.obs_hi,
-                         c.lm_lo, c.lm_hi, c.max_slots, c.n_long, (int64_t)bytes, c.k_max, c.n_cam, c.n_pt,
-                         c.n_obs, c.rank};
+  const int64_t v[16] = {c.have_order ? (int64_t)c.grp_k.size() : -1, c.n_tiles, c.n_chunks, c.n_partials,
+                         c.n_obs_l, c.n_slots, c.lm_lo, c.lm_hi, c.max_slots, c.n_long, (int64_t)bytes, c.k_max,
+                         c.n_cam, c.n_pt, c.n_obs, c.rank};
   std::memcpy(info, v, sizeof(v));
   return POBA_OK;
 }
@@ -215,6 +226,7 @@ int poba_get_ordering(poba_ctx* ctx, int64_t* order, int64_t* cam_sorted, int64_
   CTX_CHECK(ctx);
   Ctx& c = ctx->c;
   NEED(c.have_problem, "no problem set");
+  PTRY(poba::build_canonical_order(c));
   const int64_t n = c.n_obs;
   std::vector<int> o(n), cf, pf;
   PCK(cudaMemcpy(o.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
@@ -236,8 +248,9 @@ int poba_get_ordering(poba_ctx* ctx, int64_t* order, int64_t* cam_sorted, int64_
 
 int poba_get_groups(poba_ctx* ctx, int64_t cap, int64_t* n_groups, int64_t* k, int64_t* start, int64_t* n) {
   CTX_CHECK(ctx);
-  const Ctx& c = ctx->c;
+  Ctx& c = ctx->c;
   NEED(c.have_problem, "no problem set");
+  PTRY(poba::build_canonical_order(c));
   *n_groups = (int64_t)c.grp_k.size();
   for (int64_t g = 0; g < std::min<int64_t>(cap, *n_groups); ++g) {
     if (k) k[g] = c.grp_k[g];
@@ -252,7 +265,7 @@ int poba_set_points(poba_ctx* ctx, const double* points) {
   Ctx& c = ctx->c;
   NEED(c.have_problem, "no problem set");
   NEED(points, "null points");
-  PTRY(poba::points_gather_from_host(c, points, c.points.as<double>()));
+  PTRY(poba::lm_upload(c, points, 3, c.points.as<double>()));
   PCK(cudaStreamSynchronize(c.stream));
   c.have_points = true;
   return POBA_OK;
@@ -262,7 +275,7 @@ int poba_get_points(poba_ctx* ctx, double* points) {
   CTX_CHECK(ctx);
   Ctx& c = ctx->c;
   NEED(c.have_points, "no device points");
-  return poba::points_scatter_to_host(c, c.points.as<double>(), points);
+  return poba::lm_download(c, c.points.as<double>(), 3, points);
 }
 
 int poba_accept_points(poba_ctx* ctx) {
@@ -350,7 +363,7 @@ int poba_back_substitute(poba_ctx* ctx, const double* delta_p, double* delta_l, 
   int nz = 0;
   PTRY(poba::back_substitute_device(c, d_dp, &nz));
   if (nonzero) *nonzero = nz;
-  if (delta_l) PTRY(poba::points_scatter_to_host(c, c.dl.as<double>(), delta_l));
+  if (delta_l) PTRY(poba::lm_download(c, c.dl.as<double>(), 3, delta_l));
   return POBA_OK;
 }
 
@@ -370,7 +383,7 @@ int poba_cost(poba_ctx* ctx, const double* cam_params, const double* points, int
     DBuf saved;
     PTRY(saved.alloc(std::max<int64_t>(c.n_lm_l, 1) * 24));
     PCK(cudaMemcpyAsync(saved.p, c.points.p, c.n_lm_l * 24, cudaMemcpyDeviceToDevice, c.stream));
-    PTRY(poba::points_gather_from_host(c, points, c.points.as<double>()));
+    PTRY(poba::lm_upload(c, points, 3, c.points.as<double>()));
     int st = poba::cost_device(c, trial != 0, &v, &bad);
     cudaMemcpyAsync(c.points.p, saved.p, c.n_lm_l * 24, cudaMemcpyDeviceToDevice, c.stream);
     cudaStreamSynchronize(c.stream);
@@ -395,12 +408,12 @@ int poba_apply(poba_ctx* ctx, int op, const double* in, double* out) {
   DBuf din, dout;
   PTRY(din.alloc((in_lm ? std::max<int64_t>(c.n_lm_l, 1) * 3 : c.n_cam * 9) * 8));
   PTRY(dout.alloc((out_lm ? std::max<int64_t>(c.n_lm_l, 1) * 3 : c.n_cam * 9) * 8));
-  if (in_lm) PTRY(poba::points_gather_from_host(c, in, din.as<double>()));
+  if (in_lm) PTRY(poba::lm_upload(c, in, 3, din.as<double>()));
   else PCK(cudaMemcpyAsync(din.p, in, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
   PTRY(poba::apply_op_device(c, op, din.as<double>(), dout.as<double>()));
   if (op == POBA_OP_W && c.nranks > 1) PTRY(poba::allreduce_sum(c, dout.as<double>(), c.n_cam * 9));
   if (out_lm) {
-    PTRY(poba::points_scatter_to_host(c, dout.as<double>(), out));
+    PTRY(poba::lm_download(c, dout.as<double>(), 3, out));
   } else {
     PCK(cudaMemcpyAsync(out, dout.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToHost, c.stream));
     PCK(cudaStreamSynchronize(c.stream));
@@ -416,8 +429,7 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
   std::vector<double> h;
   const int64_t nc = c.n_cam, nl = c.n_lm_l;
   auto scatter_lm = [&](const std::vector<double>& src, int width) {
-    for (int64_t j = 0; j < nl; ++j)
-      std::memcpy(dst + (int64_t)ctx->lm_pt_host[j] * width, src.data() + j * width, width * 8);
+    std::memcpy(dst + c.lm_lo * width, src.data(), nl * width * 8);
   };
   auto lm_sym = [&](const DBuf& b) -> int {
     PTRY(poba::copy_down(c, b, nl * 6 * 8, h));
@@ -465,16 +477,27 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
       return POBA_OK;
     }
     case POBA_READ_STORAGE: {
-      const int64_t n = c.n_obs_l, pad = c.obs_pad;
-      std::vector<double> J((size_t)poba::kJPlanes * pad * 2), R(pad * 2);
+      // (n_obs, 2, 13) rows in the reference's canonical order; rows of
+      // observations owned by other ranks are left untouched
+      PTRY(poba::build_canonical_order(c));
+      const int64_t ns = c.n_slots, n = c.n_obs;
+      std::vector<double> J((size_t)poba::kJPlanes * ns * 2), R(ns * 2);
+      std::vector<int> file(ns), order(n), slot_of_file(n, -1);
       PCK(cudaMemcpy(J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
       PCK(cudaMemcpy(R.data(), c.Rz.p, R.size() * 8, cudaMemcpyDeviceToHost));
-      for (int64_t o = 0; o < n; ++o)
+      PCK(cudaMemcpy(file.data(), c.file_s.p, ns * 4, cudaMemcpyDeviceToHost));
+      PCK(cudaMemcpy(order.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
+      for (int64_t q = 0; q < ns; ++q)
+        if (file[q] >= 0) slot_of_file[file[q]] = (int)q;
+      for (int64_t i = 0; i < n; ++i) {
+        const int64_t q = slot_of_file[order[i]];
+        if (q < 0) continue;
         for (int a = 0; a < 2; ++a) {
-          double* row = dst + (o * 2 + a) * 13;
-          for (int j = 0; j < 12; ++j) row[j] = J[((size_t)j * pad + o) * 2 + a];
-          row[12] = R[o * 2 + a];
+          double* row = dst + (i * 2 + a) * 13;
+          for (int j = 0; j < 12; ++j) row[j] = J[((size_t)j * ns + q) * 2 + a];
+          row[12] = R[q * 2 + a];
         }
+      }
       return POBA_OK;
     }
     default:

@@ -125,50 +125,55 @@ __device__ __forceinline__ void evaluate_obs(const double* __restrict__ cp, doub
   m.jp0[8] = fs * s * p0; m.jp1[8] = fs * s * p1;
 }
 
-// Store + per-observation V0/b_l contributions + per-landmark sums (in
-// canonical order; matches np.add.at's sequential fold, blocks.py:394,396).
+// Store + per-observation V0/b_l contributions + per-landmark sums, each
+// landmark's observations in camera order (np.add.at's sequential fold of
+// blocks.py:394,396 runs over the same observations in the same order).
 template <bool kExplicit>
 __global__ void __launch_bounds__(kTile)
-k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const int* __restrict__ file_l,
-           const double2* __restrict__ pix_l, const double* __restrict__ prep,
+k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const int* __restrict__ file_s,
+           const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s, const double* __restrict__ prep,
            const double* __restrict__ points, const double* __restrict__ ejp, const double* __restrict__ ejl,
-           const double* __restrict__ eres, double2* __restrict__ J, double2* __restrict__ Rz, int64_t pad,
+           const double* __restrict__ eres, double2* __restrict__ J, double2* __restrict__ Rz, int64_t ns,
            double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
            unsigned long long* __restrict__ n_invalid) {
   __shared__ double contrib[kTile * 9];
+  __shared__ int lstart[kTile + 1];
   __shared__ int bad_count;
   const Tile t = tiles[blockIdx.x];
+  const int64_t s0 = (int64_t)blockIdx.x * kTile;
   const int i = threadIdx.x;
+  const bool is_long = t.flags & kTileLong;
   if (i == 0) bad_count = 0;
+  if (!is_long) tile_landmark_starts(lidx_s + s0, t.n, t.nlm, lstart);
   __syncthreads();
   if (i < t.n) {
-    const int o = t.obs0 + i;
+    const int64_t o = s0 + i;
     ObsModel m;
     if (kExplicit) {
-      const int f = file_l[o];
+      const int64_t f = file_s[o];
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
-        m.jp0[j] = ejp[(int64_t)f * 18 + j];
-        m.jp1[j] = ejp[(int64_t)f * 18 + 9 + j];
+        m.jp0[j] = ejp[f * 18 + j];
+        m.jp1[j] = ejp[f * 18 + 9 + j];
       }
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        m.jl0[j] = ejl[(int64_t)f * 6 + j];
-        m.jl1[j] = ejl[(int64_t)f * 6 + 3 + j];
+        m.jl0[j] = ejl[f * 6 + j];
+        m.jl1[j] = ejl[f * 6 + 3 + j];
       }
-      m.r0 = eres[(int64_t)f * 2];
-      m.r1 = eres[(int64_t)f * 2 + 1];
+      m.r0 = eres[f * 2];
+      m.r1 = eres[f * 2 + 1];
       m.valid = true;
     } else {
-      const int lm = t.lm0 + (t.k > kTile ? 0 : i / t.k);
+      const int lm = t.lm0 + (is_long ? 0 : lidx_s[o]);
       const double* X = points + (int64_t)lm * 3;
-      evaluate_obs<true>(prep + (int64_t)cam_l[o] * 16, X[0], X[1], X[2], pix_l[o], m);
+      evaluate_obs<true>(prep + (int64_t)cam_s[o] * 16, X[0], X[1], X[2], pix_s[o], m);
       if (!m.valid) atomicAdd(&bad_count, 1);
     }
 #pragma unroll
-    for (int j = 0; j < 9; ++j) J[j * pad + o] = make_double2(m.jp0[j], m.jp1[j]);
+    for (int j = 0; j < 9; ++j) J[j * ns + o] = make_double2(m.jp0[j], m.jp1[j]);
 #pragma unroll
-    for (int b = 0; b < 3; ++b) J[(9 + b) * pad + o] = make_double2(m.jl0[b], m.jl1[b]);
+    for (int b = 0; b < 3; ++b) J[(9 + b) * ns + o] = make_double2(m.jl0[b], m.jl1[b]);
     Rz[o] = make_double2(m.r0, m.r1);
     double* cc = contrib + i * 9;
     cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
@@ -183,12 +188,11 @@ k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const 
   }
   __syncthreads();
   if (i == 0 && bad_count) atomicAdd(n_invalid, (unsigned long long)bad_count);
-  if (t.k > kTile) return;  // long landmarks are reduced by k_lin_long
-  // (landmark, component) per thread
+  if (is_long) return;  // long landmarks are reduced by k_lin_long
   for (int q = i; q < t.nlm * 9; q += kTile) {
     const int j = q / 9, comp = q - j * 9;
     double acc = 0.0;
-    for (int r = 0; r < t.k; ++r) acc += contrib[(j * t.k + r) * 9 + comp];
+    for (int r = lstart[j]; r < lstart[j + 1]; ++r) acc += contrib[r * 9 + comp];
     const int lm = t.lm0 + j;
     if (comp < 6) V0[(int64_t)lm * 6 + comp] = acc; else bl[(int64_t)lm * 3 + comp - 6] = acc;
     if (comp == 0 || comp == 3 || comp == 5) {
@@ -199,11 +203,12 @@ k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const 
 }
 
 // V0/b_l of landmarks longer than a tile, straight from the stored rows
-__global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restrict__ lm_off,
-                           const double2* __restrict__ J, const double2* __restrict__ Rz, int64_t pad,
-                           double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl) {
+__global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0,
+                           const int* __restrict__ lm_k, const double2* __restrict__ J,
+                           const double2* __restrict__ Rz, int64_t pad, double* __restrict__ V0,
+                           double* __restrict__ bl, double* __restrict__ Dl) {
   const int lm = long_lm[blockIdx.x];
-  const int o0 = lm_off[lm], o1 = lm_off[lm + 1];
+  const int o0 = lm_slot0[lm], o1 = o0 + lm_k[lm];
   const int comp = threadIdx.x;  // 9 threads
   if (comp >= 9) return;
   double acc = 0.0;
@@ -314,19 +319,20 @@ __global__ void k_cam_dp(const double* __restrict__ U0, int64_t n_cam, double* _
 
 // 0.5 sum ||r||^2 per tile (fixed tree), invalid counts
 __global__ void __launch_bounds__(kTile)
-k_cost_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const double2* __restrict__ pix_l,
-            const double* __restrict__ prep, const double* __restrict__ points,
+k_cost_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const double2* __restrict__ pix_s,
+            const uint8_t* __restrict__ lidx_s, const double* __restrict__ prep, const double* __restrict__ points,
             const double* __restrict__ dl, double* __restrict__ tile_sum, unsigned long long* __restrict__ n_invalid) {
   __shared__ double red[kTile];
   __shared__ int bad_count;
   const Tile t = tiles[blockIdx.x];
+  const int64_t s0 = (int64_t)blockIdx.x * kTile;
   const int i = threadIdx.x;
   if (i == 0) bad_count = 0;
   __syncthreads();
   double v = 0.0;
   if (i < t.n) {
-    const int o = t.obs0 + i;
-    const int lm = t.lm0 + (t.k > kTile ? 0 : i / t.k);
+    const int64_t o = s0 + i;
+    const int lm = t.lm0 + ((t.flags & kTileLong) ? 0 : lidx_s[o]);
     double X0 = points[(int64_t)lm * 3], X1 = points[(int64_t)lm * 3 + 1], X2 = points[(int64_t)lm * 3 + 2];
     if (dl) {
       X0 += dl[(int64_t)lm * 3];
@@ -334,14 +340,14 @@ k_cost_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const
       X2 += dl[(int64_t)lm * 3 + 2];
     }
     ObsModel m;
-    evaluate_obs<false>(prep + (int64_t)cam_l[o] * 16, X0, X1, X2, pix_l[o], m);
+    evaluate_obs<false>(prep + (int64_t)cam_s[o] * 16, X0, X1, X2, pix_s[o], m);
     if (!m.valid) atomicAdd(&bad_count, 1);
     v = m.r0 * m.r0 + m.r1 * m.r1;
   }
   red[i] = v;
   __syncthreads();
-  for (int s = kTile / 2; s > 0; s >>= 1) {
-    if (i < s) red[i] += red[i + s];
+  for (int st = kTile / 2; st > 0; st >>= 1) {
+    if (i < st) red[i] += red[i + st];
     __syncthreads();
   }
   if (i == 0) {
@@ -365,22 +371,6 @@ __global__ void k_sum_fixed(const double* __restrict__ v, int64_t n, double* __r
   if (i == 0) out[0] = red[0];
 }
 
-__global__ void k_points_gather(const double* __restrict__ full, const int* __restrict__ lm_pt, int64_t n_lm,
-                                double* __restrict__ local) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n_lm * 3) return;
-  const int64_t j = q / 3;
-  local[q] = full[(int64_t)lm_pt[j] * 3 + (q - j * 3)];
-}
-
-__global__ void k_points_scatter(const double* __restrict__ local, const int* __restrict__ lm_pt, int64_t n_lm,
-                                 double* __restrict__ full) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n_lm * 3) return;
-  const int64_t j = q / 3;
-  full[(int64_t)lm_pt[j] * 3 + (q - j * 3)] = local[q];
-}
-
 }  // namespace
 
 int cameras_prep(Ctx& c, const double* d_cams, double* d_prep) {
@@ -390,31 +380,9 @@ int cameras_prep(Ctx& c, const double* d_cams, double* d_prep) {
   return POBA_OK;
 }
 
-int points_gather_from_host(Ctx& c, const double* h_pts, double* d_local) {
-  PTRY(c.scratch_a.alloc(c.n_pt * 3 * 8));
-  PCK(cudaMemcpyAsync(c.scratch_a.p, h_pts, c.n_pt * 3 * 8, cudaMemcpyHostToDevice, c.stream));
-  k_points_gather<<<grid_for(c.n_lm_l * 3, 256), 256, 0, c.stream>>>(c.scratch_a.as<double>(), c.lm_pt.as<int>(),
-                                                                    c.n_lm_l, d_local);
-  c.launches++;
-  PCK(cudaGetLastError());
-  return POBA_OK;
-}
-
-int points_scatter_to_host(Ctx& c, const double* d_local, double* h_full) {
-  // host array is (n_pt, 3); only this shard's landmarks are written
-  PTRY(c.scratch_a.alloc(c.n_pt * 3 * 8));
-  PCK(cudaMemcpyAsync(c.scratch_a.p, h_full, c.n_pt * 3 * 8, cudaMemcpyHostToDevice, c.stream));
-  k_points_scatter<<<grid_for(c.n_lm_l * 3, 256), 256, 0, c.stream>>>(d_local, c.lm_pt.as<int>(), c.n_lm_l,
-                                                                     c.scratch_a.as<double>());
-  c.launches++;
-  PCK(cudaMemcpyAsync(h_full, c.scratch_a.p, c.n_pt * 3 * 8, cudaMemcpyDeviceToHost, c.stream));
-  PCK(cudaStreamSynchronize(c.stream));
-  return POBA_OK;
-}
-
 int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, const double* h_res) {
   cudaStream_t s = c.stream;
-  const int64_t pad = c.obs_pad;
+  const int64_t ns = c.n_slots;
   DBuf ejp, ejl, eres;
   if (expl) {
     PTRY(ejp.alloc(c.n_obs * 18 * 8));
@@ -429,30 +397,30 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 32);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
   if (expl)
-    k_lin_tile<true><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.file_l.as<int>(),
-                                                 c.pix_l.as<double2>(), nullptr, nullptr, ejp.as<double>(),
-                                                 ejl.as<double>(), eres.as<double>(), c.J.as<double2>(),
-                                                 c.Rz.as<double2>(), pad, c.V0.as<double>(), c.bl.as<double>(),
-                                                 c.Dl.as<double>(), d_bad);
+    k_lin_tile<true><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.file_s.as<int>(),
+                                                 c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(), nullptr, nullptr,
+                                                 ejp.as<double>(), ejl.as<double>(), eres.as<double>(),
+                                                 c.J.as<double2>(), c.Rz.as<double2>(), ns, c.V0.as<double>(),
+                                                 c.bl.as<double>(), c.Dl.as<double>(), d_bad);
   else
-    k_lin_tile<false><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.file_l.as<int>(),
-                                                  c.pix_l.as<double2>(), c.cams_prep.as<double>(),
-                                                  c.points.as<double>(), nullptr, nullptr, nullptr,
-                                                  c.J.as<double2>(), c.Rz.as<double2>(), pad, c.V0.as<double>(),
-                                                  c.bl.as<double>(), c.Dl.as<double>(), d_bad);
+    k_lin_tile<false><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.file_s.as<int>(),
+                                                  c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(),
+                                                  c.cams_prep.as<double>(), c.points.as<double>(), nullptr,
+                                                  nullptr, nullptr, c.J.as<double2>(), c.Rz.as<double2>(), ns,
+                                                  c.V0.as<double>(), c.bl.as<double>(), c.Dl.as<double>(), d_bad);
   c.launches++;
   PCK(cudaGetLastError());
   if (c.n_long) {
-    k_lin_long<<<c.n_long, 32, 0, s>>>(c.long_lm.as<int>(), c.lm_off.as<int>(), c.J.as<double2>(),
-                                       c.Rz.as<double2>(), pad, c.V0.as<double>(), c.bl.as<double>(),
-                                       c.Dl.as<double>());
+    k_lin_long<<<c.n_long, 32, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
+                                       c.J.as<double2>(), c.Rz.as<double2>(), ns, c.V0.as<double>(),
+                                       c.bl.as<double>(), c.Dl.as<double>());
     c.launches++;
   }
   // camera side: U0 / b_p via camera-major chunks, then a fixed-order merge
   if (c.n_cchunks) {
     k_cam_chunk_reduce<<<grid_for((int64_t)c.n_cchunks * 32, 256), 256, 0, s>>>(
-        c.cc_cam_off.as<int>(), c.cc_start.as<int>(), c.cperm.as<int>(), c.J.as<double2>(), c.Rz.as<double2>(),
-        pad, (int)c.n_cam, c.n_cchunks, c.cc_part.as<double>());
+        c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(), c.J.as<double2>(), c.Rz.as<double2>(),
+        ns, (int)c.n_cam, c.n_cchunks, c.cc_part.as<double>());
     c.launches++;
   }
   k_cam_merge54<<<grid_for(c.n_cam * 32, 256), 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_part.as<double>(),
@@ -488,8 +456,8 @@ int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid) {
   PTRY(c.scratch_c.alloc((c.n_tiles + 8) * 8));
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 40);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
-  k_cost_tile<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.pix_l.as<double2>(),
-                                          c.trial_prep.as<double>(), c.points.as<double>(),
+  k_cost_tile<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.pix_s.as<double2>(),
+                                          c.lidx_s.as<uint8_t>(), c.trial_prep.as<double>(), c.points.as<double>(),
                                           trial ? c.dl.as<double>() : nullptr, c.scratch_c.as<double>(), d_bad);
   k_sum_fixed<<<1, 1024, 0, s>>>(c.scratch_c.as<double>(), c.n_tiles, c.red.as<double>());
   c.launches += 2;

@@ -12,11 +12,18 @@
 
 namespace poba {
 
-// ---- fixed geometry of the landmark-tile kernels --------------------------------
-constexpr int kTile = 256;        // observations per tile == threads per CTA
-constexpr int kSlotCap = 1536;    // max distinct cameras per chunk (smem accumulators)
+// ---- fixed geometry ------------------------------------------------------------
+// The device store is landmark-major in "slot space": tile t owns slots
+// [t*kTile, t*kTile + n_t); a tile packs whole landmarks (index order, each
+// landmark's observations sorted by camera) until kTile observations; a
+// landmark with k > kTile spans consecutive full sub-tiles.  Padding slots are
+// never read by the kernels (bulk copies move exactly n_t rows per plane).
+constexpr int kTile = 256;        // observation slots per tile == threads per CTA
+constexpr int kSlotCap = 16384;   // max distinct cameras per chunk (uint16 slot ids; bounds the L2-resident partials)
 constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
 constexpr int kJPlanes = 12;      // double2 planes: 9 x (Jp[0][j],Jp[1][j]) + 3 x (Jl[0][b],Jl[1][b])
+constexpr int kStages = 2;        // bulk-copy pipeline depth of the term kernel
+constexpr int kMaxLmPerTile = 64; // landmarks per tile (bounds the staged V^-1 slice)
 
 // Error plumbing ---------------------------------------------------------------
 void set_error(const std::string& msg);
@@ -87,21 +94,30 @@ struct SeriesState {
   int converged;
   int error;         // 0, POBA_ENONFINITE or POBA_EVANISH
   int error_order;
-  int any_nonzero;   // back-substitution: dx_p or dx_l non-zero
+  int any_nonzero;   // -1: zero right-hand side shortcut
   unsigned ticket;   // last-block-done counter
   unsigned ticket2;
 };
 
-// Per-tile descriptor (landmark-aligned, all landmarks of one tile share k).
+// Per-tile descriptor.
 struct Tile {
-  int obs0;    // first local observation
+  int obs0;    // first local observation (prefix count over tiles; slots are tile*kTile)
   int n;       // observations in tile
-  int k;       // track length of its landmarks (k > kTile: one sub-range of a long landmark)
   int lm0;     // first local landmark
-  int nlm;     // landmarks in tile (1 for long sub-tiles)
-  int seg0;    // first segment of the tile in the segment arrays
-  int nseg;    // number of (camera) segments
+  int nlm;     // landmarks in tile (1 for a sub-tile of a long landmark)
+  int seg0;    // first camera segment of the tile
+  int nseg;    // number of camera segments
   int chunk;   // owning chunk
+  int flags;   // bit0: sub-tile of a landmark with k > kTile
+};
+constexpr int kTileLong = 1;
+constexpr int kTileChunkFirst = 2;
+constexpr int kTileChunkLast = 4;
+
+// Compact per-tile descriptor streamed into the term kernel's stage (32 B).
+struct TileK {
+  int n, lm0, nlm, nseg;
+  int flags, part0, nslot, chunk;
 };
 
 struct Chunk {
@@ -124,43 +140,47 @@ struct Ctx {
        have_delta_l = false, have_points = false, have_pixels = false;
   int k_max = 0;
 
-  // global ordering (kept for export; K0)
-  DBuf order;        // int64 [n_obs] canonical -> file index
+  // global ordering (export only; K0), built lazily
   DBuf cam_file;     // int32 [n_obs] file-order camera index
   DBuf pt_file;      // int32 [n_obs] file-order point index
-  std::vector<int64_t> grp_k, grp_start, grp_n;  // k-groups (host)
+  DBuf kpt;          // int32 [n_pt] track length
+  DBuf order;        // int32 [n_obs] canonical -> file index (lazy)
+  bool have_order = false;
+  std::vector<int64_t> grp_k, grp_start, grp_n;  // k-groups (host, lazy)
 
-  // local shard
-  int64_t obs_lo = 0, obs_hi = 0, lm_lo = 0, lm_hi = 0;
-  int64_t n_obs_l = 0, n_lm_l = 0, obs_pad = 0;
-  DBuf cam_l;        // int32 [n_obs_l] camera of each local observation (canonical order)
-  DBuf pix_l;        // double2 [n_obs_l] pixels, canonical order
-  DBuf file_l;       // int32 [n_obs_l] file index of each local observation
-  DBuf lm_pt;        // int32 [n_lm_l] point id of each local landmark
-  DBuf lm_off;       // int32 [n_lm_l+1] local obs offset
-  DBuf pt_to_lm;     // int32 [n_pt] local landmark of a point, -1 if not local
-
-  // tiles / chunks / camera-slot map
-  int n_tiles = 0, n_chunks = 0, n_partials = 0, max_slots = 0, n_long = 0, n_segs = 0;
+  // local shard: points [lm_lo, lm_hi), its observations, tiles
+  int64_t lm_lo = 0, lm_hi = 0, n_lm_l = 0, n_obs_l = 0;
+  int64_t n_slots = 0;  // n_tiles * kTile
+  int n_tiles = 0, n_chunks = 0, n_partials = 0, max_slots = 0, n_long = 0, n_segs = 0, n_work = 0;
   DBuf tiles;        // Tile [n_tiles]
+  DBuf tilek;        // TileK [n_tiles]
   DBuf chunks;       // Chunk [n_chunks]
-  DBuf perm;         // uint8 [n_obs_l] tile-local position sorted by camera
-  DBuf seg_start;    // uint16 [n_segs]
-  DBuf seg_slot;     // uint16 [n_segs]
+  DBuf work;         // int2 [n_work] contiguous tile ranges, one per CTA of the term kernel
+  DBuf cam_s;        // int32 [n_slots] camera of each slot
+  DBuf file_s;       // int32 [n_slots] file index of each slot (-1 padding)
+  DBuf pix_s;        // double2 [n_slots] pixels
+  DBuf lidx_s;       // uint8 [n_slots] landmark index within its tile
+  DBuf perm_s;       // uint8 [n_slots] tile-local position sorted by camera
+  DBuf lm_slot0;     // int32 [n_lm_l] first slot of each local landmark
+  DBuf lm_k;         // int32 [n_lm_l]
+  DBuf seg_start;    // uint16 [n_slots] per tile: start position of segment s at tile*kTile + s
+  DBuf seg_slot;     // uint16 [n_slots] per tile: chunk slot of segment s
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
-  DBuf long_lm;      // int32 [n_long] local landmark ids with k > kTile
-  DBuf long_zb;      // double [n_long*3] per long landmark z (V^-1 y)
-  std::vector<int> long_host;  // host copy of long landmarks
-  // camera-major reduction chunks over cperm
+  DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
+  std::vector<int> long_host;
+  std::vector<Chunk> chunks_host;
+  std::vector<int> tile_n_host;
+  int work_occ = 0;  // CTAs/SM the work ranges were planned for
+  // camera-major reduction chunks
   int n_cchunks = 0;
-  DBuf cperm;        // int32 [n_obs_l] local obs sorted by (camera, obs)
-  DBuf cc_start;     // int32 [n_cchunks]
+  DBuf cperm;        // int32 [n_obs_l] slots sorted by (camera, slot)
+  DBuf cam_start;    // int32 [n_cam+1] camera -> first position in cperm
   DBuf cc_cam_off;   // int32 [n_cam+1] camera -> cchunk range
 
-  // store (K1)
-  DBuf J;            // double2 [kJPlanes][obs_pad]
-  DBuf Rz;           // double2 [obs_pad] residuals
+  // store (K1), slot space
+  DBuf J;            // double2 [kJPlanes][n_slots]
+  DBuf Rz;           // double2 [n_slots] residuals
 
   // camera arrays
   DBuf cams;         // double [n_cam*9] current linearization cameras
@@ -184,7 +204,7 @@ struct Ctx {
   DBuf ratios;       // double [max_order+1]
   int ratios_cap = 0;
 
-  // landmark arrays (local, canonical landmark order)
+  // landmark arrays (local, point order)
   DBuf points;       // double [n_lm_l*3]
   DBuf V0;           // double [n_lm_l*6] packed
   DBuf bl;           // double [n_lm_l*3]
@@ -192,10 +212,10 @@ struct Ctx {
   DBuf Vinv;         // double [n_lm_l*6]
   DBuf Vd;           // double [n_lm_l*6] damped V
   DBuf dl;           // double [n_lm_l*3] last delta_l
-  DBuf ltmp;         // double [n_lm_l*3] scratch
+  DBuf ltmp;         // double [n_lm_l*3] scratch / z of long landmarks
   DBuf ctmp;         // double [n_cam*9] scratch
   DBuf ctmp2;        // double [n_cam*9]
-  DBuf flag;         // int [4]
+  DBuf flag;         // int [16]
   DBuf red;          // double scratch for reductions
   DBuf cub_tmp;      // CUB temp storage
 
@@ -204,12 +224,12 @@ struct Ctx {
   int64_t n_invalid = 0;
   int last_order = 0;
 
-  // host staging
-  DBuf scratch_a, scratch_b, scratch_c, scratch_d;
+  DBuf scratch_a, scratch_b, scratch_c;
 };
 
-// ---- host-side orchestration entry points (defined per translation unit) ------
+// ---- host-side orchestration entry points ---------------------------------------
 int build_structure(Ctx& c, const int64_t* cam_idx, const int64_t* pt_idx, const double* pixels);
+int build_canonical_order(Ctx& c);
 int linearize_device(Ctx& c, bool explicit_jac, const double* jp, const double* jl, const double* res);
 int damp_device(Ctx& c, double lam, int identity);
 int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_used, int* converged);
@@ -222,9 +242,20 @@ int allreduce_sum(Ctx& c, double* d_buf, size_t n);
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches);
 int b_tilde_device(Ctx& c);
 int points_accept_device(Ctx& c);
-int points_scatter_to_host(Ctx& c, const double* d_lm3, double* host_pt3);
-int points_gather_from_host(Ctx& c, const double* host_pt3, double* d_lm3);
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+// ---- device helpers shared by the tile kernels -----------------------------------
+#ifdef __CUDACC__
+// landmark starts inside a tile from the per-slot landmark index (lstart has nlm+1 entries)
+__device__ __forceinline__ void tile_landmark_starts(const uint8_t* __restrict__ lidx_tile, int n, int nlm,
+                                                     int* lstart) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int l = lidx_tile[i];
+    if (i == 0 || lidx_tile[i - 1] != l) lstart[l] = i;
+  }
+  if (threadIdx.x == 0) lstart[nlm] = n;
+}
+#endif
 
 }  // namespace poba

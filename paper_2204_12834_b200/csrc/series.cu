@@ -17,7 +17,9 @@
 // order and written once per (chunk, camera).  A second, small kernel merges
 // the chunk partials per camera (fixed order), applies U^-1, accumulates the
 // partial sum x and evaluates the stop test on the device.
+#include <algorithm>
 #include <limits>
+#include <vector>
 
 #include "poba_internal.h"
 
@@ -152,147 +154,258 @@ __global__ void k_damp_v(const double* __restrict__ V0, const double* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// the fused term kernel (one CTA per chunk of tiles)
+// the fused term kernel: bulk-copy (TMA) pipeline over tiles, one CTA per SM
 // ---------------------------------------------------------------------------
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 struct TermArgs {
-  const Tile* tiles;
-  const Chunk* chunks;
-  const int* cam_l;
-  const uint8_t* perm;
+  const TileK* tk;         // per-tile kernel descriptors
+  const int2* work;        // per-CTA contiguous tile range (whole chunks)
+  const int* cam_s;
+  const uint8_t* perm_s;
+  const uint8_t* lidx_s;
   const uint16_t* seg_start;
   const uint16_t* seg_slot;
   const double2* J;
-  int64_t pad;
-  const double* tin;    // camera vector (kModeTerm)
-  const double* lvec;   // b_l (kModeBt) or landmark input (kModeW)
+  int64_t ns;              // plane stride = slots
+  const double* tin;       // camera vector (kModeTerm)
+  const double* lvec;      // b_l (kModeBt) or landmark input (kModeW)
   const double* Vinv;
-  const double* zlong;  // landmark-indexed z of long landmarks (kModeTerm)
+  const double* zlong;     // landmark-indexed z of long landmarks (kModeTerm)
   double* partials;
   const SeriesState* st;
-  int max_slots;
   int check_stop;
 };
 
+// shared-memory carve-up of k_term (bytes).  One stage holds everything a tile
+// needs, moved by bulk copies: the 12 Jacobian planes, the camera permutation,
+// the landmark index, the camera segments, the descriptor and the V^-1 slice.
+// After phase 1 the Jacobians live in registers, so the plane area doubles as
+// scratch for w (planes 9..11) and g (planes 0..8); the stage is released for
+// the next bulk copy at the end of the tile.  The per-chunk camera-slot
+// accumulators live in the chunk's own (CTA-exclusive, L2-resident) partial
+// buffer, so two CTAs fit per SM.
+constexpr int kStPlanes = kJPlanes * kTile * 16;            // 49152
+constexpr int kStPerm = kStPlanes;                          // +256
+constexpr int kStLidx = kStPerm + kTile;                    // +256
+constexpr int kStSegStart = kStLidx + kTile;                // +512
+constexpr int kStSegSlot = kStSegStart + kTile * 2;         // +512
+constexpr int kStDesc = kStSegSlot + kTile * 2;             // +32
+constexpr int kStVinv = kStDesc + 32;                       // +64*48
+constexpr int kStageBytes = (kStVinv + kMaxLmPerTile * 48 + 127) / 128 * 128;
+constexpr int kOffBars = kStages * kStageBytes;
+constexpr int kOffZ = kOffBars + 64;
+constexpr int kOffL = kOffZ + kMaxLmPerTile * 3 * 8;
+constexpr int kTermSmem = kOffL + (kTile + 4) * 4;
+static_assert(2 * (kTermSmem + 1024) <= 228 * 1024, "term kernel must fit two CTAs per SM");
+
 template <int MODE>
 __global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
-  extern __shared__ double sm[];
-  double* acc = sm;
-  double* gbuf = acc + a.max_slots * 9;
-  double* wbuf = gbuf + kTile * 9;
-  double* zbuf = wbuf + kTile * 3;
-  uint8_t* pbuf = reinterpret_cast<uint8_t*>(zbuf + kTile * 3);
-  uint16_t* sbuf = reinterpret_cast<uint16_t*>(pbuf + kTile);  // [start | slot] x kTile
+  extern __shared__ __align__(128) uint8_t smraw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + kOffBars);
+  double* zbuf = reinterpret_cast<double*>(smraw + kOffZ);
+  int* lstart = reinterpret_cast<int*>(smraw + kOffL);
   const int tid = threadIdx.x;
   if (a.check_stop && a.st->stopped) return;
-  const Chunk ch = a.chunks[blockIdx.x];
-  for (int q = tid; q < ch.nslot * 9; q += kTile) acc[q] = 0.0;
+  const int2 wr = a.work[blockIdx.x];
+  const int nq = wr.y - wr.x;
+  if (nq <= 0) return;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
 
-  // prologue: operands of the first tile
-  Tile t = a.tiles[ch.tile0];
-  double2 jr[kJPlanes];
-  double tc[9];
-  uint8_t pr = 0;
-  uint16_t s_start = 0, s_slot = 0;
-  auto fetch = [&](const Tile& tt) {
-    if (tid < tt.n) {
-      const int o = tt.obs0 + tid;
-#pragma unroll
-      for (int p = 0; p < kJPlanes; ++p) jr[p] = __ldcs(&a.J[p * a.pad + o]);  // streamed once per term
-      pr = a.perm[o];
-      if (MODE == kModeTerm && tt.k <= kTile) {
-        const double* tv = a.tin + (int64_t)a.cam_l[o] * 9;
-#pragma unroll
-        for (int j = 0; j < 9; ++j) tc[j] = tv[j];
-      }
-    }
-    if (tid < tt.nseg) {
-      s_start = a.seg_start[tt.seg0 + tid];
-      s_slot = a.seg_slot[tt.seg0 + tid];
-    }
+  // producer (thread 0): descriptor of the tile to copy comes one issue ahead
+  auto issue = [&](int q, int4 d) {  // d = (n, lm0, nlm, nseg) of tile wr.x + q
+    const int ti = wr.x + q;
+    uint8_t* stg = smraw + (q % kStages) * kStageBytes;
+    uint64_t* bar = &bars[q % kStages];
+    const uint32_t vbytes = (MODE != kModeW) ? (uint32_t)(d.z * 48) : 0u;
+    fence_proxy_async();
+    mbar_expect_tx(bar, (uint32_t)(kJPlanes * d.x * 16 + 2 * kTile + 4 * kTile + 32) + vbytes);
+    const int64_t s0 = (int64_t)ti * kTile;
+#pragma unroll 1
+    for (int p = 0; p < kJPlanes; ++p) bulk_g2s(stg + p * kTile * 16, a.J + p * a.ns + s0, (uint32_t)(d.x * 16), bar);
+    bulk_g2s(stg + kStPerm, a.perm_s + s0, kTile, bar);
+    bulk_g2s(stg + kStLidx, a.lidx_s + s0, kTile, bar);
+    bulk_g2s(stg + kStSegStart, a.seg_start + s0, 2 * kTile, bar);
+    bulk_g2s(stg + kStSegSlot, a.seg_slot + s0, 2 * kTile, bar);
+    bulk_g2s(stg + kStDesc, a.tk + ti, 32, bar);
+    if (vbytes) bulk_g2s(stg + kStVinv, a.Vinv + (int64_t)d.y * 6, vbytes, bar);
   };
-  fetch(t);
+  int4 dnext = make_int4(0, 0, 0, 0);  // descriptor of the next tile to issue (thread 0)
+  if (tid == 0) {
+    for (int q = 0; q < kStages && q < nq; ++q) issue(q, *reinterpret_cast<const int4*>(a.tk + wr.x + q));
+    if (kStages < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + kStages);
+  }
 
-  for (int ti = ch.tile0; ti < ch.tile1; ++ti) {
+  // camera-vector gathers run one tile ahead, camera indices two tiles ahead
+  // (padding slots carry camera 0, so these loads need no descriptor)
+  double tc[9], tn[9];
+  int cn = 0;
+  if (MODE == kModeTerm) {
+    const double* tv = a.tin + (int64_t)a.cam_s[(int64_t)wr.x * kTile + tid] * 9;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) tc[j] = tv[j];
+    if (nq > 1) cn = a.cam_s[(int64_t)(wr.x + 1) * kTile + tid];
+  }
+
+  for (int q = 0; q < nq; ++q) {
+    const int ti = wr.x + q;
+    if (MODE == kModeTerm) {
+      if (q + 1 < nq) {
+        const double* tv = a.tin + (int64_t)cn * 9;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) tn[j] = tv[j];
+      }
+      if (q + 2 < nq) cn = a.cam_s[(int64_t)(ti + 2) * kTile + tid];
+    }
+    uint8_t* stg = smraw + (q % kStages) * kStageBytes;
+    mbar_wait(&bars[q % kStages], (uint32_t)((q / kStages) & 1));
+    const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
     const bool valid = tid < t.n;
-    const bool is_long = t.k > kTile;
-    // phase 1: w_o = J_l^T (J_p t_c)
+    const bool is_long = t.flags & kTileLong;
+    double* acc = a.partials + (int64_t)t.part0 * 9;  // this chunk's slots, owned by this CTA
+    if (t.flags & kTileChunkFirst)
+      for (int k = tid; k < t.nslot * 9; k += kTile) acc[k] = 0.0;
+    double2* pl = reinterpret_cast<double2*>(stg);
+    // phase 1: operands out of the stage; w_o = J_l^T (J_p t_c) into the plane-9 area
+    double2 jr[kJPlanes];
+    int li = 0;
     if (valid) {
-      if (MODE == kModeTerm && !is_long) {
-        double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-        for (int j = 0; j < 9; ++j) {
-          u0 = fma(jr[j].x, tc[j], u0);
-          u1 = fma(jr[j].y, tc[j], u1);
-        }
+      for (int p = 0; p < kJPlanes; ++p) jr[p] = pl[p * kTile + tid];
+      li = stg[kStLidx + tid];
+      if (!is_long && (tid == 0 || stg[kStLidx + tid - 1] != li)) lstart[li] = tid;
+    }
+    if (tid == 0) lstart[t.nlm] = t.n;
+    __syncthreads();  // A: planes are in registers; the plane area is scratch from here on
+    double* wbuf = reinterpret_cast<double*>(stg + 9 * kTile * 16);  // 3 doubles per observation
+    double* gbuf = reinterpret_cast<double*>(stg);                     // 9 doubles per observation
+    if (MODE == kModeTerm && valid && !is_long) {
+      double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) wbuf[tid * 3 + b] = fma(jr[9 + b].x, u0, jr[9 + b].y * u1);
+      for (int j = 0; j < 9; ++j) {
+        u0 = fma(jr[j].x, tc[j], u0);
+        u1 = fma(jr[j].y, tc[j], u1);
       }
+#pragma unroll
+      for (int b = 0; b < 3; ++b) wbuf[tid * 3 + b] = fma(jr[9 + b].x, u0, jr[9 + b].y * u1);
     }
-    __syncthreads();
-    // (pbuf/sbuf are rewritten only after the sync above: the previous tile's
-    // phase 4 reads them)
-    if (valid) pbuf[tid] = pr;
-    if (tid < t.nseg) {
-      sbuf[tid] = s_start;
-      sbuf[kTile + tid] = s_slot;
-    }
-    // phase 2: per landmark z_l
-    if (tid < t.nlm) {
-      const int lm = t.lm0 + tid;
-      double y[3], z[3];
-      if (MODE == kModeW) {
-        z[0] = a.lvec[lm * 3]; z[1] = a.lvec[lm * 3 + 1]; z[2] = a.lvec[lm * 3 + 2];
-      } else if (MODE == kModeTerm && is_long) {
-        z[0] = a.zlong[lm * 3]; z[1] = a.zlong[lm * 3 + 1]; z[2] = a.zlong[lm * 3 + 2];
-      } else {
-        if (MODE == kModeBt) {
-          y[0] = a.lvec[lm * 3]; y[1] = a.lvec[lm * 3 + 1]; y[2] = a.lvec[lm * 3 + 2];
+    if (MODE == kModeTerm) __syncthreads();  // A2
+    // phase 2: per landmark z_l, four lanes per landmark (lane c sums y_c)
+    {
+      const int lmi = tid >> 2, c = tid & 3;
+      double yc = 0.0;
+      const bool act = lmi < t.nlm;
+      const int lm = t.lm0 + lmi;
+      if (act && c < 3) {
+        if (MODE == kModeW) {
+          yc = a.lvec[lm * 3 + c];
+        } else if (MODE == kModeTerm && is_long) {
+          yc = a.zlong[lm * 3 + c];
+        } else if (MODE == kModeBt) {
+          yc = a.lvec[lm * 3 + c];
         } else {
-          y[0] = y[1] = y[2] = 0.0;
-          const double* w = wbuf + tid * t.k * 3;
-          for (int r = 0; r < t.k; ++r) {
-            y[0] += w[r * 3];
-            y[1] += w[r * 3 + 1];
-            y[2] += w[r * 3 + 2];
-          }
+          for (int r = lstart[lmi]; r < lstart[lmi + 1]; ++r) yc += wbuf[r * 3 + c];
         }
-        sym3_mv(a.Vinv + (int64_t)lm * 6, y, z);
       }
-      zbuf[tid * 3] = z[0];
-      zbuf[tid * 3 + 1] = z[1];
-      zbuf[tid * 3 + 2] = z[2];
+      const int base = (tid & 31) & ~3;
+      const double y0 = __shfl_sync(0xffffffffu, yc, base);
+      const double y1 = __shfl_sync(0xffffffffu, yc, base + 1);
+      const double y2 = __shfl_sync(0xffffffffu, yc, base + 2);
+      if (act && c < 3) {
+        double z;
+        if (MODE == kModeW || (MODE == kModeTerm && is_long)) {
+          z = yc;  // already z
+        } else {
+          const double* V = reinterpret_cast<const double*>(stg + kStVinv) + lmi * 6;
+          const int r0 = c == 0 ? 0 : (c == 1 ? 1 : 2), r1 = c == 0 ? 1 : (c == 1 ? 3 : 4),
+                    r2 = c == 0 ? 2 : (c == 1 ? 4 : 5);
+          z = V[r0] * y0 + V[r1] * y1 + V[r2] * y2;
+        }
+        zbuf[lmi * 3 + c] = z;
+      }
     }
-    __syncthreads();
-    // phase 3: g_o = J_p^T (J_l z_l)
+    __syncthreads();  // B
+    // phase 3: g_o = J_p^T (J_l z_l) into the plane-0..8 area
     if (valid) {
-      const int j = is_long ? 0 : tid / t.k;
-      const double z0 = zbuf[j * 3], z1 = zbuf[j * 3 + 1], z2 = zbuf[j * 3 + 2];
+      const double z0 = zbuf[li * 3], z1 = zbuf[li * 3 + 1], z2 = zbuf[li * 3 + 2];
       const double v0 = fma(jr[9].x, z0, fma(jr[10].x, z1, jr[11].x * z2));
       const double v1 = fma(jr[9].y, z0, fma(jr[10].y, z1, jr[11].y * z2));
 #pragma unroll
-      for (int q = 0; q < 9; ++q) gbuf[tid * 9 + q] = fma(jr[q].x, v0, jr[q].y * v1);
+      for (int p = 0; p < 9; ++p) gbuf[tid * 9 + p] = fma(jr[p].x, v0, jr[p].y * v1);
     }
-    // prefetch the next tile while this one is reduced
-    const int nseg = t.nseg, tn = t.n;
-    if (ti + 1 < ch.tile1) {
-      t = a.tiles[ti + 1];
-      fetch(t);
+    __syncthreads();  // C
+    // phase 4: camera segments -> slot accumulators (fixed order), loads batched
+    {
+      const uint16_t* ss = reinterpret_cast<const uint16_t*>(stg + kStSegStart);
+      const uint16_t* sl = reinterpret_cast<const uint16_t*>(stg + kStSegSlot);
+      const uint8_t* pm = stg + kStPerm;
+      const int items = t.nseg * 9;
+      double sum[9];
+      int dst[9];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) {
+        const int k = tid + u * kTile;
+        sum[u] = 0.0;
+        dst[u] = -1;
+        if (k < items) {
+          const int sg = k / 9, comp = k - sg * 9;
+          const int r0 = ss[sg], r1 = (sg + 1 < t.nseg) ? ss[sg + 1] : t.n;
+          for (int r = r0; r < r1; ++r) sum[u] += gbuf[pm[r] * 9 + comp];
+          dst[u] = sl[sg] * 9 + comp;
+        }
+      }
+      double old[9];
+#pragma unroll
+      for (int u = 0; u < 9; ++u) old[u] = dst[u] >= 0 ? acc[dst[u]] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 9; ++u)
+        if (dst[u] >= 0) acc[dst[u]] = old[u] + sum[u];
     }
-    __syncthreads();
-    // phase 4: camera segments -> slot accumulators, fixed order
-    for (int q = tid; q < nseg * 9; q += kTile) {
-      const int s = q / 9, comp = q - s * 9;
-      const int r0 = sbuf[s], r1 = (s + 1 < nseg) ? sbuf[s + 1] : tn;
-      double sum = 0.0;
-      for (int r = r0; r < r1; ++r) sum += gbuf[pbuf[r] * 9 + comp];
-      acc[sbuf[kTile + s] * 9 + comp] += sum;
+    __syncthreads();  // D: stage free, accumulator updates visible to the next tile
+    if (tid == 0 && q + kStages < nq) {
+      issue(q + kStages, dnext);
+      if (q + kStages + 1 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + ti + kStages + 1);
     }
-    // the next phase-1 sync orders this phase before gbuf/sbuf are rewritten
+    if (MODE == kModeTerm) {
+#pragma unroll
+      for (int j = 0; j < 9; ++j) tc[j] = tn[j];
+    }
   }
-  __syncthreads();
-  double* dst = a.partials + (int64_t)ch.part0 * 9;
-  for (int q = tid; q < ch.nslot * 9; q += kTile) dst[q] = acc[q];
 }
 
 // ---------------------------------------------------------------------------
@@ -473,26 +586,29 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
 
 template <int OUT>
 __global__ void __launch_bounds__(kTile)
-k_wt_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const double2* __restrict__ J,
-          int64_t pad, const double* __restrict__ tin, const double* __restrict__ bl,
+k_wt_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const uint8_t* __restrict__ lidx_s,
+          const double2* __restrict__ J, int64_t ns, const double* __restrict__ tin, const double* __restrict__ bl,
           const double* __restrict__ Vinv, double* __restrict__ out, int* __restrict__ nonzero_flag) {
   __shared__ double wbuf[kTile * 3];
+  __shared__ int lstart[kTile + 1];
   const Tile t = tiles[blockIdx.x];
-  if (t.k > kTile) return;  // handled by k_wt_long
+  if (t.flags & kTileLong) return;  // handled by k_wt_long
+  const int64_t s0 = (int64_t)blockIdx.x * kTile;
   const int tid = threadIdx.x;
+  tile_landmark_starts(lidx_s + s0, t.n, t.nlm, lstart);
   if (tid < t.n) {
-    const int o = t.obs0 + tid;
-    const double* tv = tin + (int64_t)cam_l[o] * 9;
+    const int64_t o = s0 + tid;
+    const double* tv = tin + (int64_t)cam_s[o] * 9;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = J[j * pad + o];
+      const double2 v = J[j * ns + o];
       u0 = fma(v.x, tv[j], u0);
       u1 = fma(v.y, tv[j], u1);
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const double2 v = J[(9 + b) * pad + o];
+      const double2 v = J[(9 + b) * ns + o];
       wbuf[tid * 3 + b] = fma(v.x, u0, v.y * u1);
     }
   }
@@ -500,11 +616,10 @@ k_wt_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const d
   if (tid < t.nlm) {
     const int lm = t.lm0 + tid;
     double y[3] = {0.0, 0.0, 0.0}, z[3];
-    const double* w = wbuf + tid * t.k * 3;
-    for (int r = 0; r < t.k; ++r) {
-      y[0] += w[r * 3];
-      y[1] += w[r * 3 + 1];
-      y[2] += w[r * 3 + 2];
+    for (int r = lstart[tid]; r < lstart[tid + 1]; ++r) {
+      y[0] += wbuf[r * 3];
+      y[1] += wbuf[r * 3 + 1];
+      y[2] += wbuf[r * 3 + 2];
     }
     if (OUT == kOutWt) {
       z[0] = y[0]; z[1] = y[1]; z[2] = y[2];
@@ -524,26 +639,26 @@ k_wt_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, const d
 
 template <int OUT>
 __global__ void __launch_bounds__(kTile)
-k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_off, const int* __restrict__ cam_l,
-          const double2* __restrict__ J, int64_t pad, const double* __restrict__ tin,
+k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, const int* __restrict__ lm_k,
+          const int* __restrict__ cam_s, const double2* __restrict__ J, int64_t ns, const double* __restrict__ tin,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag, const SeriesState* __restrict__ st, int check_stop) {
   __shared__ double red[kTile][3];
   if (check_stop && st->stopped) return;
   const int lm = long_lm[blockIdx.x];
-  const int o0 = lm_off[lm], o1 = lm_off[lm + 1];
+  const int o0 = lm_slot0[lm], o1 = o0 + lm_k[lm];
   const int tid = threadIdx.x;
   double y0 = 0.0, y1 = 0.0, y2 = 0.0;
   for (int o = o0 + tid; o < o1; o += kTile) {
-    const double* tv = tin + (int64_t)cam_l[o] * 9;
+    const double* tv = tin + (int64_t)cam_s[o] * 9;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = J[j * pad + o];
+      const double2 v = J[j * ns + o];
       u0 = fma(v.x, tv[j], u0);
       u1 = fma(v.y, tv[j], u1);
     }
-    const double2 a = J[9 * pad + o], b = J[10 * pad + o], c = J[11 * pad + o];
+    const double2 a = J[9 * ns + o], b = J[10 * ns + o], c = J[11 * ns + o];
     y0 += fma(a.x, u0, a.y * u1);
     y1 += fma(b.x, u0, b.y * u1);
     y2 += fma(c.x, u0, c.y * u1);
@@ -574,6 +689,7 @@ k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_off, const
     out[lm * 3 + 2] = z[2];
   }
 }
+
 
 // elementwise block-diagonal products
 __global__ void k_cam_mv(const double* __restrict__ M45, const double* __restrict__ v, int64_t n_cam,
@@ -611,40 +727,69 @@ __global__ void k_add_inplace(double* __restrict__ a, const double* __restrict__
 }
 
 size_t term_smem(const Ctx& c) {
-  return (size_t)c.max_slots * 9 * 8 + kTile * 9 * 8 + kTile * 3 * 8 * 2 + kTile + kTile * 4;
+  (void)c;
+  return (size_t)kTermSmem;
 }
 
 int configure_term(Ctx& c) {
-  (void)c;
   static thread_local int done_dev = -1;
   int dev = 0;
   PCK(cudaGetDevice(&dev));
   if (done_dev != dev) {
-    PCK(cudaFuncSetAttribute(k_term<kModeTerm>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    PCK(cudaFuncSetAttribute(k_term<kModeBt>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    PCK(cudaFuncSetAttribute(k_term<kModeW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const int lim = (int)kTermSmem;
+    PCK(cudaFuncSetAttribute(k_term<kModeTerm>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    PCK(cudaFuncSetAttribute(k_term<kModeBt>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    PCK(cudaFuncSetAttribute(k_term<kModeW>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
     done_dev = dev;
+  }
+  if (c.work_occ == 0) {
+    // one CTA per SM (or more if the accumulators are small): group whole chunks
+    // into contiguous tile ranges of about equal observation count
+    int occ = 0;
+    PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_term<kModeTerm>, kTile, term_smem(c)));
+    occ = std::max(occ, 1);
+    const int n_work = std::max(1, std::min(c.n_chunks, c.n_sm * occ));
+    std::vector<int64_t> cobs(c.n_chunks + 1, 0);
+    for (int q = 0; q < c.n_chunks; ++q) {
+      int64_t o = 0;
+      for (int t = c.chunks_host[q].tile0; t < c.chunks_host[q].tile1; ++t) o += c.tile_n_host[t];
+      cobs[q + 1] = cobs[q] + o;
+    }
+    std::vector<int2> wr;
+    int prev = 0;
+    for (int w = 1; w <= n_work && prev < c.n_chunks; ++w) {
+      const int64_t want = cobs[c.n_chunks] * w / n_work;
+      int e = (int)(std::lower_bound(cobs.begin(), cobs.end(), want) - cobs.begin());
+      e = std::min(std::max(e, prev + 1), c.n_chunks);
+      if (w == n_work) e = c.n_chunks;
+      wr.push_back(make_int2(c.chunks_host[prev].tile0, c.chunks_host[e - 1].tile1));
+      prev = e;
+    }
+    PTRY(c.work.alloc(wr.size() * sizeof(int2)));
+    PCK(cudaMemcpy(c.work.p, wr.data(), wr.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    c.n_work = (int)wr.size();
+    c.work_occ = occ;
   }
   return POBA_OK;
 }
 
 TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_stop) {
   TermArgs a;
-  a.tiles = c.tiles.as<Tile>();
-  a.chunks = c.chunks.as<Chunk>();
-  a.cam_l = c.cam_l.as<int>();
-  a.perm = c.perm.as<uint8_t>();
+  a.tk = c.tilek.as<TileK>();
+  a.work = c.work.as<int2>();
+  a.cam_s = c.cam_s.as<int>();
+  a.perm_s = c.perm_s.as<uint8_t>();
+  a.lidx_s = c.lidx_s.as<uint8_t>();
   a.seg_start = c.seg_start.as<uint16_t>();
   a.seg_slot = c.seg_slot.as<uint16_t>();
   a.J = c.J.as<double2>();
-  a.pad = c.obs_pad;
+  a.ns = c.n_slots;
   a.tin = tin;
   a.lvec = lvec;
   a.Vinv = c.Vinv.as<double>();
   a.zlong = c.ltmp.as<double>();
   a.partials = c.partials.as<double>();
   a.st = c.state.as<SeriesState>();
-  a.max_slots = c.max_slots;
   a.check_stop = check_stop ? 1 : 0;
   return a;
 }
@@ -678,15 +823,16 @@ int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool ch
   if (mode == kModeTerm) {
     if (c.n_long) {
       k_wt_long<kOutZ><<<c.n_long, kTile, 0, c.stream>>>(
-          c.long_lm.as<int>(), c.lm_off.as<int>(), c.cam_l.as<int>(), c.J.as<double2>(), c.obs_pad, tin, nullptr,
-          c.Vinv.as<double>(), c.ltmp.as<double>(), nullptr, c.state.as<SeriesState>(), check_stop ? 1 : 0);
+          c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.as<double2>(),
+          c.n_slots, tin, nullptr, c.Vinv.as<double>(), c.ltmp.as<double>(), nullptr, c.state.as<SeriesState>(),
+          check_stop ? 1 : 0);
       c.launches++;
     }
-    k_term<kModeTerm><<<c.n_chunks, kTile, smem, c.stream>>>(a);
+    k_term<kModeTerm><<<c.n_work, kTile, smem, c.stream>>>(a);
   } else if (mode == kModeBt) {
-    k_term<kModeBt><<<c.n_chunks, kTile, smem, c.stream>>>(a);
+    k_term<kModeBt><<<c.n_work, kTile, smem, c.stream>>>(a);
   } else {
-    k_term<kModeW><<<c.n_chunks, kTile, smem, c.stream>>>(a);
+    k_term<kModeW><<<c.n_work, kTile, smem, c.stream>>>(a);
   }
   c.launches++;
   PCK(cudaGetLastError());
@@ -851,13 +997,14 @@ int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero) {
   cudaStream_t s = c.stream;
   int* fl = c.flag.as<int>() + 1;
   PCK(cudaMemsetAsync(fl, 0, 4, s));
-  k_wt_tile<kOutBack><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.J.as<double2>(), c.obs_pad,
-                                                  d_dp, c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl);
+  k_wt_tile<kOutBack><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(),
+                                                  c.J.as<double2>(), c.n_slots, d_dp, c.bl.as<double>(),
+                                                  c.Vinv.as<double>(), c.dl.as<double>(), fl);
   c.launches++;
   if (c.n_long) {
-    k_wt_long<kOutBack><<<c.n_long, kTile, 0, s>>>(c.long_lm.as<int>(), c.lm_off.as<int>(), c.cam_l.as<int>(),
-                                                   c.J.as<double2>(), c.obs_pad, d_dp, c.bl.as<double>(),
-                                                   c.Vinv.as<double>(), c.dl.as<double>(), fl,
+    k_wt_long<kOutBack><<<c.n_long, kTile, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
+                                                   c.cam_s.as<int>(), c.J.as<double2>(), c.n_slots, d_dp,
+                                                   c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl,
                                                    c.state.as<SeriesState>(), 0);
     c.launches++;
   }
@@ -888,13 +1035,14 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
       PCK(cudaMemcpyAsync(d_out, c.rvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, s));
       break;
     case POBA_OP_WT:
-      k_wt_tile<kOutWt><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), c.J.as<double2>(),
-                                                    c.obs_pad, d_in, nullptr, nullptr, d_out, nullptr);
+      k_wt_tile<kOutWt><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(),
+                                                    c.J.as<double2>(), c.n_slots, d_in, nullptr, nullptr, d_out,
+                                                    nullptr);
       c.launches++;
       if (c.n_long) {
-        k_wt_long<kOutWt><<<c.n_long, kTile, 0, s>>>(c.long_lm.as<int>(), c.lm_off.as<int>(), c.cam_l.as<int>(),
-                                                     c.J.as<double2>(), c.obs_pad, d_in, nullptr, nullptr, d_out,
-                                                     nullptr, c.state.as<SeriesState>(), 0);
+        k_wt_long<kOutWt><<<c.n_long, kTile, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
+                                                     c.cam_s.as<int>(), c.J.as<double2>(), c.n_slots, d_in, nullptr,
+                                                     nullptr, d_out, nullptr, c.state.as<SeriesState>(), 0);
         c.launches++;
       }
       break;

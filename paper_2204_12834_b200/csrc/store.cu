@@ -1,19 +1,24 @@
 // K0 -- observation store structure.
 //
-// Replaces the reference's canonical ordering and grouping
-// (/root/reference/pkg/src/powerba/blocks.py:362-372 _sorted_observation_order,
-//  blocks.py:405-417 _build_groups, blocks.py:83-87 per-landmark offsets):
-//   * canonical order = stable radix sort of the packed key (k[pt], pt, cam),
-//     identical to np.lexsort((cam, pt, k[pt])) -- ties (duplicate pairs, only
-//     possible through assemble_from_observations) keep file order, as lexsort;
-//   * landmark-aligned tiles of <= 256 observations (one k per tile, so a tile
-//     is a slice of one k-group view (n, k, 2, 13));
-//   * chunks = contiguous tile ranges, one per persistent CTA of the series
-//     kernel, with a chunk-local camera "slot" map: the series kernel reduces
-//     per-observation camera contributions into shared-memory slot
-//     accumulators in a fixed order (deterministic, no fp64 atomics);
-//   * the camera-major permutation used by the U0/b_p reduction;
-//   * (sharded) this rank's contiguous landmark range.
+// Two orders exist for the observations:
+//   * the reference's CANONICAL order, (k of landmark, landmark, camera), which
+//     np.lexsort((cam, pt, k[pt])) produces in blocks._sorted_observation_order
+//     (/root/reference/pkg/src/powerba/blocks.py:362-372) and which defines
+//     the k-groups of blocks._build_groups (blocks.py:405-417).  libpoba
+//     reproduces it bit-exactly with a stable device radix sort of the packed
+//     key (k, pt, cam) and exports it (order / cam_sorted / pt_sorted / groups);
+//   * the STORE order the kernels stream: landmarks in index order, each
+//     landmark's observations sorted by camera (the within-block order of the
+//     reference), packed into landmark-aligned tiles of <= 256 slots.  Dropping
+//     the k-grouping keeps spatially adjacent landmarks (and therefore the
+//     cameras that see them) in the same tiles and chunks, which is what makes
+//     the shared-memory camera reduction of the series kernel effective.  The
+//     store order changes only fp64 summation order, never which terms are
+//     summed.
+// On top of the tiles it builds chunks (contiguous tile ranges whose distinct
+// cameras fit the shared-memory slot accumulators), the per-tile camera
+// segments and permutation (fixed-order reduction, no fp64 atomics), the
+// camera -> partial CSR, and the camera-major permutation used by U0/b_p.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -25,10 +30,11 @@ namespace poba {
 
 namespace {
 
-__global__ void k_convert_idx(const int64_t* __restrict__ cam64, const int64_t* __restrict__ pt64,
-                              int64_t n, int64_t n_cam, int64_t n_pt, int* __restrict__ cam32,
-                              int* __restrict__ pt32, int* __restrict__ kpt, int* __restrict__ kcam,
-                              int* __restrict__ flag) {
+constexpr uint64_t kSentinel = ~0ull;
+
+__global__ void k_convert_idx(const int64_t* __restrict__ cam64, const int64_t* __restrict__ pt64, int64_t n,
+                              int64_t n_cam, int64_t n_pt, int* __restrict__ cam32, int* __restrict__ pt32,
+                              int* __restrict__ kpt, int* __restrict__ kcam, int* __restrict__ flag) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t c = cam64[i], p = pt64[i];
@@ -60,13 +66,22 @@ __global__ void k_minmax(const int* __restrict__ a, int64_t n, int* __restrict__
   }
 }
 
-__global__ void k_obs_keys(const int* __restrict__ cam, const int* __restrict__ pt,
-                           const int* __restrict__ kpt, int64_t n, int bc, int bp,
-                           uint64_t* __restrict__ key, int* __restrict__ val) {
+// canonical key (k, pt, cam) + file index
+__global__ void k_canon_keys(const int* __restrict__ cam, const int* __restrict__ pt, const int* __restrict__ kpt,
+                             int64_t n, int bc, int bp, uint64_t* __restrict__ key, int* __restrict__ val) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   int p = pt[i];
   key[i] = ((uint64_t)kpt[p] << (bp + bc)) | ((uint64_t)p << bc) | (uint64_t)cam[i];
+  val[i] = (int)i;
+}
+
+// store key (pt, cam) + file index
+__global__ void k_store_keys(const int* __restrict__ cam, const int* __restrict__ pt, int64_t n, int bc,
+                             uint64_t* __restrict__ key, int* __restrict__ val) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  key[i] = ((uint64_t)pt[i] << bc) | (uint64_t)cam[i];
   val[i] = (int)i;
 }
 
@@ -76,38 +91,38 @@ __global__ void k_lm_keys(const int* __restrict__ kpt, int64_t n_pt, int bp, uin
   key[p] = ((uint64_t)kpt[p] << bp) | (uint64_t)p;
 }
 
-__global__ void k_lm_split(const uint64_t* __restrict__ key, int64_t n_pt, int bp,
-                           int* __restrict__ lm_pt, int* __restrict__ lm_k) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= n_pt) return;
-  uint64_t k = key[j];
-  lm_pt[j] = (int)(k & ((1ull << bp) - 1));
-  lm_k[j] = (int)(k >> bp);
+// place the local observations into their slots
+__global__ void k_fill_slots(const uint64_t* __restrict__ key, const int* __restrict__ val, int64_t q0,
+                             int64_t nq, int bc, int64_t lm_lo, const int* __restrict__ lm_first_l,
+                             const int* __restrict__ lm_slot0, const uint8_t* __restrict__ lm_tidx,
+                             const double2* __restrict__ pix, int* __restrict__ cam_s, int* __restrict__ file_s,
+                             double2* __restrict__ pix_s, uint8_t* __restrict__ lidx_s) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const uint64_t k = key[q0 + q];
+  const int f = val[q0 + q];
+  const int l = (int)((int64_t)(k >> bc) - lm_lo);
+  const int c = (int)(k & ((1ull << bc) - 1));
+  const int r = (int)q - lm_first_l[l];
+  const int s = lm_slot0[l] + r;
+  cam_s[s] = c;
+  file_s[s] = f;
+  if (pix) pix_s[s] = pix[f];
+  lidx_s[s] = lm_tidx[l];
 }
 
-// local observation arrays for the shard [obs_lo, obs_lo + n)
-__global__ void k_local_obs(const int* __restrict__ order, const int* __restrict__ cam_file,
-                            const double2* __restrict__ pix_file, int64_t obs_lo, int64_t n,
-                            int* __restrict__ cam_l, int* __restrict__ file_l, double2* __restrict__ pix_l) {
+__global__ void k_fill_i32(int* __restrict__ a, int64_t n, int v) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int f = order[obs_lo + i];
-  file_l[i] = f;
-  cam_l[i] = cam_file[f];
-  if (pix_file) pix_l[i] = pix_file[f];
+  if (i < n) a[i] = v;
 }
 
-__global__ void k_pt_to_lm(const int* __restrict__ lm_pt, int64_t n_lm, int* __restrict__ pt_to_lm) {
-  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j < n_lm) pt_to_lm[lm_pt[j]] = (int)j;
-}
-
-// key (chunk, cam) per local observation, via the tile table
-__global__ void k_chunk_cam_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, int bc,
+// key (chunk, cam) per slot; padding slots -> sentinel
+__global__ void k_chunk_cam_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, int bc,
                                  uint64_t* __restrict__ key) {
   const Tile t = tiles[blockIdx.x];
-  for (int i = threadIdx.x; i < t.n; i += blockDim.x)
-    key[t.obs0 + i] = ((uint64_t)t.chunk << bc) | (uint64_t)cam_l[t.obs0 + i];
+  const int64_t s0 = (int64_t)blockIdx.x * kTile;
+  for (int i = threadIdx.x; i < kTile; i += blockDim.x)
+    key[s0 + i] = i < t.n ? (((uint64_t)t.chunk << bc) | (uint64_t)cam_s[s0 + i]) : kSentinel;
 }
 
 __global__ void k_unique_flags(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ flag) {
@@ -115,14 +130,12 @@ __global__ void k_unique_flags(const uint64_t* __restrict__ key, int64_t n, int*
   if (i < n) flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
 }
 
-// compact unique keys; pos = exclusive scan of flags
 __global__ void k_unique_compact(const uint64_t* __restrict__ key, const int* __restrict__ flag,
                                  const int* __restrict__ pos, int64_t n, uint64_t* __restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n && flag[i]) out[pos[i]] = key[i];
 }
 
-// first unique entry of each chunk
 __global__ void k_chunk_first(const uint64_t* __restrict__ ukey, int n_u, int bc, int* __restrict__ first) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_u) return;
@@ -130,9 +143,8 @@ __global__ void k_chunk_first(const uint64_t* __restrict__ ukey, int n_u, int bc
   if (i == 0 || (int)(ukey[i - 1] >> bc) != ch) first[ch] = i;
 }
 
-// (cam, chunk) keys of the unique pairs, value = partial index
-__global__ void k_part_keys(const uint64_t* __restrict__ ukey, int n_u, int bc, int bch,
-                            uint64_t* __restrict__ key, int* __restrict__ val, int* __restrict__ cam_cnt) {
+__global__ void k_part_keys(const uint64_t* __restrict__ ukey, int n_u, int bc, int bch, uint64_t* __restrict__ key,
+                            int* __restrict__ val, int* __restrict__ cam_cnt) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_u) return;
   uint64_t u = ukey[i];
@@ -143,13 +155,14 @@ __global__ void k_part_keys(const uint64_t* __restrict__ ukey, int n_u, int bc, 
   atomicAdd(&cam_cnt[cam], 1);
 }
 
-// key (tile, cam, tile-local position) per local observation
-__global__ void k_tile_cam_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_l, int bc,
+// key (tile, cam, tile position) per slot; padding -> sentinel
+__global__ void k_tile_cam_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, int bc,
                                 uint64_t* __restrict__ key) {
-  const int ti = blockIdx.x;
-  const Tile t = tiles[ti];
-  for (int i = threadIdx.x; i < t.n; i += blockDim.x)
-    key[t.obs0 + i] = ((uint64_t)ti << (bc + 8)) | ((uint64_t)cam_l[t.obs0 + i] << 8) | (uint64_t)i;
+  const Tile t = tiles[blockIdx.x];
+  const int64_t s0 = (int64_t)blockIdx.x * kTile;
+  for (int i = threadIdx.x; i < kTile; i += blockDim.x)
+    key[s0 + i] = i < t.n ? (((uint64_t)blockIdx.x << (bc + 8)) | ((uint64_t)cam_s[s0 + i] << 8) | (uint64_t)i)
+                          : kSentinel;
 }
 
 __global__ void k_seg_flags(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ flag) {
@@ -158,47 +171,51 @@ __global__ void k_seg_flags(const uint64_t* __restrict__ key, int64_t n, int* __
   flag[q] = (q == 0 || (key[q] >> 8) != (key[q - 1] >> 8)) ? 1 : 0;
 }
 
-__device__ __forceinline__ int lower_bound_cam(const uint64_t* __restrict__ ukey, int lo, int hi,
-                                               uint64_t target) {
+__device__ __forceinline__ int lower_bound_u64(const uint64_t* __restrict__ a, int lo, int hi, uint64_t target) {
   while (lo < hi) {
     int mid = (lo + hi) >> 1;
-    if (ukey[mid] < target) lo = mid + 1; else hi = mid;
+    if (a[mid] < target) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 
+// per tile: permutation (position sorted by camera) and camera segments
 __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restrict__ flag,
                            const int* __restrict__ segpos, Tile* __restrict__ tiles,
                            const Chunk* __restrict__ chunks, const uint64_t* __restrict__ ukey, int bc,
-                           uint8_t* __restrict__ perm, uint16_t* __restrict__ seg_start,
+                           uint8_t* __restrict__ perm_s, uint16_t* __restrict__ seg_start,
                            uint16_t* __restrict__ seg_slot) {
   const int ti = blockIdx.x;
-  Tile t = tiles[ti];
+  const Tile t = tiles[ti];
   const Chunk ch = chunks[t.chunk];
+  const int64_t s0 = (int64_t)ti * kTile;
   for (int r = threadIdx.x; r < t.n; r += blockDim.x) {
-    int64_t q = t.obs0 + r;
-    uint64_t k = key[q];
-    perm[q] = (uint8_t)(k & 0xff);
+    const int64_t q = t.obs0 + r;
+    const uint64_t k = key[q];
+    perm_s[s0 + r] = (uint8_t)(k & 0xff);
     if (flag[q]) {
-      int cam = (int)((k >> 8) & ((1ull << bc) - 1));
-      uint64_t target = ((uint64_t)t.chunk << bc) | (uint64_t)cam;
-      int u = lower_bound_cam(ukey, ch.part0, ch.part0 + ch.nslot, target);
-      int s = segpos[q];
-      seg_start[s] = (uint16_t)r;
-      seg_slot[s] = (uint16_t)(u - ch.part0);
+      const int cam = (int)((k >> 8) & ((1ull << bc) - 1));
+      const uint64_t target = ((uint64_t)t.chunk << bc) | (uint64_t)cam;
+      const int u = lower_bound_u64(ukey, ch.part0, ch.part0 + ch.nslot, target);
+      const int64_t sl = s0 + (segpos[q] - segpos[t.obs0]);  // segment index within the tile
+      seg_start[sl] = (uint16_t)r;
+      seg_slot[sl] = (uint16_t)(u - ch.part0);
     }
   }
   if (threadIdx.x == 0) {
-    int s0 = segpos[t.obs0];
-    int s1 = segpos[t.obs0 + t.n - 1] + flag[t.obs0 + t.n - 1];
-    tiles[ti].seg0 = s0;
-    tiles[ti].nseg = s1 - s0;
+    const int s_first = segpos[t.obs0];
+    const int s_end = segpos[t.obs0 + t.n - 1] + flag[t.obs0 + t.n - 1];
+    tiles[ti].seg0 = s_first;
+    tiles[ti].nseg = s_end - s_first;
   }
 }
 
-__global__ void k_cam_obs_keys(const int* __restrict__ cam_l, int64_t n, uint64_t* __restrict__ key) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) key[i] = ((uint64_t)cam_l[i] << 32) | (uint64_t)i;
+__global__ void k_cam_slot_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
+                                uint64_t* __restrict__ key) {
+  const Tile t = tiles[blockIdx.x];
+  const int64_t s0 = (int64_t)blockIdx.x * kTile;
+  for (int i = threadIdx.x; i < kTile; i += blockDim.x)
+    key[s0 + i] = i < t.n ? (((uint64_t)cam_s[s0 + i] << 32) | (uint64_t)(s0 + i)) : kSentinel;
 }
 
 __global__ void k_low32(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ out) {
@@ -206,9 +223,9 @@ __global__ void k_low32(const uint64_t* __restrict__ key, int64_t n, int* __rest
   if (i < n) out[i] = (int)(key[i] & 0xffffffffu);
 }
 
-__global__ void k_cam_degree(const int* __restrict__ cam_l, int64_t n, int* __restrict__ deg) {
+__global__ void k_cam_degree(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ deg) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(&deg[cam_l[i]], 1);
+  if (i < n) atomicAdd(&deg[(int)(key[i] >> 32)], 1);
 }
 
 __global__ void k_cc_counts(const int* __restrict__ deg, int64_t n_cam, int* __restrict__ cnt) {
@@ -225,7 +242,6 @@ int bitlen(uint64_t v) {
   return b;
 }
 
-// CUB helpers with a growing temp buffer
 template <class F>
 int cub_call(Ctx& c, F&& f) {
   size_t need = 0;
@@ -236,16 +252,15 @@ int cub_call(Ctx& c, F&& f) {
   return POBA_OK;
 }
 
-int sort_keys(Ctx& c, uint64_t* keys_in, uint64_t* keys_out, int64_t n, int end_bit) {
+int sort_keys(Ctx& c, uint64_t* in, uint64_t* out, int64_t n, int end_bit) {
   return cub_call(c, [&](void* tmp, size_t& bytes) {
-    return cub::DeviceRadixSort::SortKeys(tmp, bytes, keys_in, keys_out, (int)n, 0, end_bit, c.stream);
+    return cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int)n, 0, end_bit, c.stream);
   });
 }
 
 int sort_pairs(Ctx& c, uint64_t* k_in, uint64_t* k_out, int* v_in, int* v_out, int64_t n, int end_bit) {
   return cub_call(c, [&](void* tmp, size_t& bytes) {
-    return cub::DeviceRadixSort::SortPairs(tmp, bytes, k_in, k_out, v_in, v_out, (int)n, 0, end_bit,
-                                           c.stream);
+    return cub::DeviceRadixSort::SortPairs(tmp, bytes, k_in, k_out, v_in, v_out, (int)n, 0, end_bit, c.stream);
   });
 }
 
@@ -257,32 +272,84 @@ int excl_sum(Ctx& c, int* in, int* out, int64_t n) {
 
 }  // namespace
 
+// Canonical (reference) order and k-groups, built on first export request.
+int build_canonical_order(Ctx& c) {
+  if (c.have_order) return POBA_OK;
+  const int64_t n = c.n_obs, n_pt = c.n_pt;
+  const int B = 256;
+  cudaStream_t s = c.stream;
+  const int bc = std::max(1, bitlen((uint64_t)(c.n_cam - 1)));
+  const int bp = std::max(1, bitlen((uint64_t)(n_pt - 1)));
+  const int bk = bitlen((uint64_t)c.k_max);
+  if (bk + bp + bc > 64) return fail(POBA_EINVAL, "ordering key exceeds 64 bits");
+  {
+    DBuf ka, kb, va, vb;
+    PTRY(ka.alloc(n * 8));
+    PTRY(kb.alloc(n * 8));
+    PTRY(va.alloc(n * 4));
+    PTRY(c.order.alloc(n * 4));
+    k_canon_keys<<<grid_for(n, B), B, 0, s>>>(c.cam_file.as<int>(), c.pt_file.as<int>(), c.kpt.as<int>(), n, bc, bp,
+                                             ka.as<uint64_t>(), va.as<int>());
+    c.launches++;
+    PTRY(sort_pairs(c, ka.as<uint64_t>(), kb.as<uint64_t>(), va.as<int>(), c.order.as<int>(), n, bk + bp + bc));
+  }
+  // k-groups from landmarks sorted by (k, pt)
+  std::vector<uint64_t> lk(n_pt);
+  {
+    DBuf ka, kb;
+    PTRY(ka.alloc(n_pt * 8));
+    PTRY(kb.alloc(n_pt * 8));
+    k_lm_keys<<<grid_for(n_pt, B), B, 0, s>>>(c.kpt.as<int>(), n_pt, bp, ka.as<uint64_t>());
+    c.launches++;
+    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), n_pt, bk + bp));
+    PCK(cudaMemcpyAsync(lk.data(), kb.p, n_pt * 8, cudaMemcpyDeviceToHost, s));
+    PCK(cudaStreamSynchronize(s));
+  }
+  c.grp_k.clear();
+  c.grp_start.clear();
+  c.grp_n.clear();
+  int64_t off = 0;
+  for (int64_t j = 0; j < n_pt;) {
+    const int64_t k = (int64_t)(lk[j] >> bp);
+    int64_t e = j;
+    while (e < n_pt && (int64_t)(lk[e] >> bp) == k) ++e;
+    c.grp_k.push_back(k);
+    c.grp_start.push_back(off);
+    c.grp_n.push_back(e - j);
+    off += k * (e - j);
+    j = e;
+  }
+  c.have_order = true;
+  return POBA_OK;
+}
+
 int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const double* h_pix) {
   const int64_t n = c.n_obs, n_cam = c.n_cam, n_pt = c.n_pt;
   const int B = 256;
   cudaStream_t s = c.stream;
   if (n >= (1ll << 31) - 1 || n_pt >= (1ll << 31) - 1 || n_cam >= (1ll << 24))
     return fail(POBA_EINVAL, "problem too large for 32-bit observation indexing");
+  c.have_order = false;
 
-  // --- upload + validate indices, histograms --------------------------------------
-  DBuf cam64, pt64, kpt, kcam, flag;
+  // --- upload + validate indices, histograms ---------------------------------------
+  DBuf cam64, pt64, kcam, flag;
   PTRY(cam64.alloc(n * 8));
   PTRY(pt64.alloc(n * 8));
   PCK(cudaMemcpyAsync(cam64.p, h_cam, n * 8, cudaMemcpyHostToDevice, s));
   PCK(cudaMemcpyAsync(pt64.p, h_pt, n * 8, cudaMemcpyHostToDevice, s));
   PTRY(c.cam_file.alloc(n * 4));
   PTRY(c.pt_file.alloc(n * 4));
-  PTRY(kpt.alloc(n_pt * 4));
+  PTRY(c.kpt.alloc(n_pt * 4));
   PTRY(kcam.alloc(n_cam * 4));
   PTRY(flag.alloc(16));
-  PCK(cudaMemsetAsync(kpt.p, 0, n_pt * 4, s));
+  PCK(cudaMemsetAsync(c.kpt.p, 0, n_pt * 4, s));
   PCK(cudaMemsetAsync(kcam.p, 0, n_cam * 4, s));
   int hflag[4] = {0, INT32_MAX, INT32_MIN, 0};
   PCK(cudaMemcpyAsync(flag.p, hflag, 16, cudaMemcpyHostToDevice, s));
   k_convert_idx<<<grid_for(n, B), B, 0, s>>>(cam64.as<int64_t>(), pt64.as<int64_t>(), n, n_cam, n_pt,
-                                            c.cam_file.as<int>(), c.pt_file.as<int>(), kpt.as<int>(),
+                                            c.cam_file.as<int>(), c.pt_file.as<int>(), c.kpt.as<int>(),
                                             kcam.as<int>(), flag.as<int>());
-  k_minmax<<<std::min<unsigned>(grid_for(n_pt, B), 1024), B, 0, s>>>(kpt.as<int>(), n_pt, flag.as<int>() + 1);
+  k_minmax<<<std::min<unsigned>(grid_for(n_pt, B), 1024), B, 0, s>>>(c.kpt.as<int>(), n_pt, flag.as<int>() + 1);
   c.launches += 2;
   PCK(cudaMemcpyAsync(hflag, flag.p, 16, cudaMemcpyDeviceToHost, s));
   PCK(cudaStreamSynchronize(s));
@@ -300,98 +367,64 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PCK(cudaStreamSynchronize(s));
     if (mm[0] == 0) return fail(POBA_EINVAL, "every camera must have at least one observation");
   }
-
-  // --- canonical order: stable sort of (k, pt, cam) --------------------------------
   const int bc = std::max(1, bitlen((uint64_t)(n_cam - 1)));
   const int bp = std::max(1, bitlen((uint64_t)(n_pt - 1)));
-  const int bk = bitlen((uint64_t)c.k_max);
-  if (bk + bp + bc > 64) return fail(POBA_EINVAL, "ordering key exceeds 64 bits");
-  {
-    DBuf ka, kb, va, vb;
-    PTRY(ka.alloc(n * 8));
-    PTRY(kb.alloc(n * 8));
-    PTRY(va.alloc(n * 4));
-    PTRY(vb.alloc(n * 4));
-    k_obs_keys<<<grid_for(n, B), B, 0, s>>>(c.cam_file.as<int>(), c.pt_file.as<int>(), kpt.as<int>(), n,
-                                           bc, bp, ka.as<uint64_t>(), va.as<int>());
-    c.launches++;
-    PTRY(sort_pairs(c, ka.as<uint64_t>(), kb.as<uint64_t>(), va.as<int>(), vb.as<int>(), n, bk + bp + bc));
-    PTRY(c.order.alloc(n * 4));
-    PCK(cudaMemcpyAsync(c.order.p, vb.p, n * 4, cudaMemcpyDeviceToDevice, s));
-  }
+  if (bp + bc > 64) return fail(POBA_EINVAL, "store key exceeds 64 bits");
 
-  // --- canonical landmark order: sort points by (k, pt) -----------------------------
-  std::vector<int> h_lm_pt(n_pt), h_lm_k(n_pt);
-  DBuf g_lm_pt, g_lm_k;
-  PTRY(g_lm_pt.alloc(n_pt * 4));
-  PTRY(g_lm_k.alloc(n_pt * 4));
-  {
-    DBuf ka, kb;
-    PTRY(ka.alloc(n_pt * 8));
-    PTRY(kb.alloc(n_pt * 8));
-    k_lm_keys<<<grid_for(n_pt, B), B, 0, s>>>(kpt.as<int>(), n_pt, bp, ka.as<uint64_t>());
-    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), n_pt, bk + bp));
-    k_lm_split<<<grid_for(n_pt, B), B, 0, s>>>(kb.as<uint64_t>(), n_pt, bp, g_lm_pt.as<int>(), g_lm_k.as<int>());
-    c.launches += 2;
-    PCK(cudaMemcpyAsync(h_lm_pt.data(), g_lm_pt.p, n_pt * 4, cudaMemcpyDeviceToHost, s));
-    PCK(cudaMemcpyAsync(h_lm_k.data(), g_lm_k.p, n_pt * 4, cudaMemcpyDeviceToHost, s));
-    PCK(cudaStreamSynchronize(s));
-  }
-  std::vector<int64_t> h_lm_off(n_pt + 1);
-  h_lm_off[0] = 0;
-  for (int64_t j = 0; j < n_pt; ++j) h_lm_off[j + 1] = h_lm_off[j] + h_lm_k[j];
-
-  // --- k-groups (blocks.py:405-417) ---------------------------------------------------
-  c.grp_k.clear();
-  c.grp_start.clear();
-  c.grp_n.clear();
-  std::vector<int64_t> grp_lm0;
-  for (int64_t j = 0; j < n_pt;) {
-    int64_t e = j;
-    while (e < n_pt && h_lm_k[e] == h_lm_k[j]) ++e;
-    c.grp_k.push_back(h_lm_k[j]);
-    c.grp_start.push_back(h_lm_off[j]);
-    c.grp_n.push_back(e - j);
-    grp_lm0.push_back(j);
-    j = e;
-  }
-
-  // --- tiles (global) -----------------------------------------------------------------
+  // --- tiles (host greedy packing of landmarks in index order) -------------------------
+  std::vector<int> hk(n_pt);
+  PCK(cudaMemcpy(hk.data(), c.kpt.p, n_pt * 4, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> lm_first(n_pt + 1);
+  lm_first[0] = 0;
+  for (int64_t j = 0; j < n_pt; ++j) lm_first[j + 1] = lm_first[j] + hk[j];
   std::vector<Tile> gt;
-  std::vector<char> cut_ok;  // may a shard boundary sit before this tile?
-  gt.reserve(n / kTile + c.grp_k.size() + 16);
-  for (size_t g = 0; g < c.grp_k.size(); ++g) {
-    const int k = (int)c.grp_k[g];
-    const int64_t lm0 = grp_lm0[g], ng = c.grp_n[g];
-    if (k <= kTile) {
-      const int per = kTile / k;
-      for (int64_t a = 0; a < ng; a += per) {
-        Tile t{};
-        t.lm0 = (int)(lm0 + a);
-        t.nlm = (int)std::min<int64_t>(per, ng - a);
-        t.k = k;
-        t.obs0 = (int)h_lm_off[lm0 + a];
-        t.n = t.nlm * k;
-        gt.push_back(t);
+  std::vector<char> cut_ok;
+  std::vector<int> lm_tile(n_pt), lm_off_in_tile(n_pt);
+  gt.reserve(n / kTile * 11 / 10 + 16);
+  {
+    Tile cur{};
+    bool open = false;
+    auto close = [&]() {
+      if (open) {
+        gt.push_back(cur);
         cut_ok.push_back(1);
+        open = false;
       }
-    } else {
-      for (int64_t a = 0; a < ng; ++a) {
+    };
+    for (int64_t j = 0; j < n_pt; ++j) {
+      const int k = hk[j];
+      if (k > kTile) {
+        close();
+        lm_tile[j] = (int)gt.size();
+        lm_off_in_tile[j] = 0;
         for (int sub = 0; sub < k; sub += kTile) {
           Tile t{};
-          t.lm0 = (int)(lm0 + a);
-          t.nlm = 1;
-          t.k = k;
-          t.obs0 = (int)(h_lm_off[lm0 + a] + sub);
+          t.obs0 = (int)(lm_first[j] + sub);
           t.n = std::min(kTile, k - sub);
+          t.lm0 = (int)j;
+          t.nlm = 1;
+          t.flags = kTileLong;
           gt.push_back(t);
           cut_ok.push_back(sub == 0);
         }
+        continue;
       }
+      if (open && (cur.n + k > kTile || cur.nlm >= kMaxLmPerTile)) close();
+      if (!open) {
+        cur = Tile{};
+        cur.obs0 = (int)lm_first[j];
+        cur.lm0 = (int)j;
+        open = true;
+      }
+      lm_tile[j] = (int)gt.size();
+      lm_off_in_tile[j] = cur.n;
+      cur.n += k;
+      cur.nlm += 1;
     }
+    close();
   }
 
-  // --- shard: contiguous tile range balanced by observations ---------------------------
+  // --- shard: contiguous tile range balanced by observations ------------------------------
   size_t t_lo = 0, t_hi = gt.size();
   if (c.nranks > 1) {
     auto cut_at = [&](int r) -> size_t {
@@ -399,7 +432,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
       if (r >= c.nranks) return gt.size();
       const int64_t target = (n * r) / c.nranks;
       size_t lo = 0, hi = gt.size();
-      while (lo < hi) {  // first tile with obs0 >= target
+      while (lo < hi) {
         size_t mid = (lo + hi) / 2;
         if (gt[mid].obs0 < target) lo = mid + 1; else hi = mid;
       }
@@ -410,99 +443,115 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     t_hi = cut_at(c.rank + 1);
   }
   if (t_hi <= t_lo) return fail(POBA_EINVAL, "shard received no landmarks (too many ranks)");
-  c.obs_lo = gt[t_lo].obs0;
-  c.obs_hi = (t_hi < gt.size()) ? gt[t_hi].obs0 : n;
   c.lm_lo = gt[t_lo].lm0;
   c.lm_hi = (t_hi < gt.size()) ? gt[t_hi].lm0 : n_pt;
-  c.n_obs_l = c.obs_hi - c.obs_lo;
   c.n_lm_l = c.lm_hi - c.lm_lo;
-  c.obs_pad = (c.n_obs_l + 63) / 64 * 64;
+  const int64_t obs_lo = lm_first[c.lm_lo];
+  c.n_obs_l = lm_first[c.lm_hi] - obs_lo;
   std::vector<Tile> tiles(gt.begin() + t_lo, gt.begin() + t_hi);
-  std::vector<int> long_host;
+  c.long_host.clear();
   for (auto& t : tiles) {
-    t.obs0 -= (int)c.obs_lo;
+    t.obs0 -= (int)obs_lo;
     t.lm0 -= (int)c.lm_lo;
-    if (t.k > kTile && (long_host.empty() || long_host.back() != t.lm0)) long_host.push_back(t.lm0);
+    if ((t.flags & kTileLong) && (c.long_host.empty() || c.long_host.back() != t.lm0)) c.long_host.push_back(t.lm0);
   }
   c.n_tiles = (int)tiles.size();
-  c.long_host = long_host;
-  c.n_long = (int)long_host.size();
+  c.n_long = (int)c.long_host.size();
+  c.n_slots = (int64_t)c.n_tiles * kTile;
+  const int64_t ns = c.n_slots, nl = c.n_obs_l, nlm = c.n_lm_l;
 
-  // --- local observation / landmark arrays ------------------------------------------------
-  const int64_t nl = c.n_obs_l;
-  PTRY(c.cam_l.alloc(nl * 4));
-  PTRY(c.file_l.alloc(nl * 4));
-  PTRY(c.pix_l.alloc(nl * 16));
+  // --- per-landmark slot map ------------------------------------------------------------------
+  std::vector<int> h_slot0(nlm), h_first(nlm + 1), h_k(nlm);
+  std::vector<uint8_t> h_tidx(nlm);
+  for (int64_t j = 0; j < nlm; ++j) {
+    const int64_t g = c.lm_lo + j;
+    h_slot0[j] = (lm_tile[g] - (int)t_lo) * kTile + lm_off_in_tile[g];
+    h_first[j] = (int)(lm_first[g] - obs_lo);
+    h_k[j] = hk[g];
+    const Tile& t = tiles[lm_tile[g] - t_lo];
+    h_tidx[j] = (t.flags & kTileLong) ? 0 : (uint8_t)(j - t.lm0);
+  }
+  h_first[nlm] = (int)nl;
+  PTRY(c.lm_slot0.alloc(std::max<int64_t>(nlm, 1) * 4));
+  PTRY(c.lm_k.alloc(std::max<int64_t>(nlm, 1) * 4));
+  PCK(cudaMemcpyAsync(c.lm_slot0.p, h_slot0.data(), nlm * 4, cudaMemcpyHostToDevice, s));
+  PCK(cudaMemcpyAsync(c.lm_k.p, h_k.data(), nlm * 4, cudaMemcpyHostToDevice, s));
+  if (c.n_long) {
+    PTRY(c.long_lm.alloc(c.n_long * 4));
+    PCK(cudaMemcpyAsync(c.long_lm.p, c.long_host.data(), c.n_long * 4, cudaMemcpyHostToDevice, s));
+  }
+
+  // --- store order: stable sort of (pt, cam), then place local observations in slots -------------
+  PTRY(c.cam_s.alloc(ns * 4));
+  PTRY(c.file_s.alloc(ns * 4));
+  PTRY(c.pix_s.alloc(ns * 16));
+  PTRY(c.lidx_s.alloc(ns));
+  PTRY(c.perm_s.alloc(ns));
+  PCK(cudaMemsetAsync(c.cam_s.p, 0, ns * 4, s));
+  k_fill_i32<<<grid_for(ns, B), B, 0, s>>>(c.file_s.as<int>(), ns, -1);
+  PCK(cudaMemsetAsync(c.pix_s.p, 0, ns * 16, s));
+  PCK(cudaMemsetAsync(c.lidx_s.p, 0, ns, s));
+  PCK(cudaMemsetAsync(c.perm_s.p, 0, ns, s));
+  c.launches++;
   {
-    DBuf pix_file;
+    DBuf ka, kb, va, vb, pixf, dfirst, dtidx;
+    PTRY(ka.alloc(n * 8));
+    PTRY(kb.alloc(n * 8));
+    PTRY(va.alloc(n * 4));
+    PTRY(vb.alloc(n * 4));
+    k_store_keys<<<grid_for(n, B), B, 0, s>>>(c.cam_file.as<int>(), c.pt_file.as<int>(), n, bc, ka.as<uint64_t>(),
+                                             va.as<int>());
+    c.launches++;
+    PTRY(sort_pairs(c, ka.as<uint64_t>(), kb.as<uint64_t>(), va.as<int>(), vb.as<int>(), n, bp + bc));
     if (h_pix) {
-      PTRY(pix_file.alloc(n * 16));
-      PCK(cudaMemcpyAsync(pix_file.p, h_pix, n * 16, cudaMemcpyHostToDevice, s));
+      PTRY(pixf.alloc(n * 16));
+      PCK(cudaMemcpyAsync(pixf.p, h_pix, n * 16, cudaMemcpyHostToDevice, s));
     }
-    k_local_obs<<<grid_for(nl, B), B, 0, s>>>(c.order.as<int>(), c.cam_file.as<int>(),
-                                             h_pix ? pix_file.as<double2>() : nullptr, c.obs_lo, nl,
-                                             c.cam_l.as<int>(), c.file_l.as<int>(), c.pix_l.as<double2>());
+    PTRY(dfirst.alloc((nlm + 1) * 4));
+    PTRY(dtidx.alloc(std::max<int64_t>(nlm, 1)));
+    PCK(cudaMemcpyAsync(dfirst.p, h_first.data(), (nlm + 1) * 4, cudaMemcpyHostToDevice, s));
+    PCK(cudaMemcpyAsync(dtidx.p, h_tidx.data(), nlm, cudaMemcpyHostToDevice, s));
+    k_fill_slots<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), vb.as<int>(), obs_lo, nl, bc, c.lm_lo,
+                                              dfirst.as<int>(), c.lm_slot0.as<int>(), dtidx.as<uint8_t>(),
+                                              h_pix ? pixf.as<double2>() : nullptr, c.cam_s.as<int>(),
+                                              c.file_s.as<int>(), c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>());
     c.launches++;
     PCK(cudaStreamSynchronize(s));
   }
   c.have_pixels = h_pix != nullptr;
-  PTRY(c.lm_pt.alloc(c.n_lm_l * 4));
-  PTRY(c.lm_off.alloc((c.n_lm_l + 1) * 4));
-  PCK(cudaMemcpyAsync(c.lm_pt.p, h_lm_pt.data() + c.lm_lo, c.n_lm_l * 4, cudaMemcpyHostToDevice, s));
-  {
-    std::vector<int> off(c.n_lm_l + 1);
-    for (int64_t j = 0; j <= c.n_lm_l; ++j) off[j] = (int)(h_lm_off[c.lm_lo + j] - c.obs_lo);
-    PCK(cudaMemcpyAsync(c.lm_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, s));
-    PCK(cudaStreamSynchronize(s));
-  }
-  PTRY(c.pt_to_lm.alloc(n_pt * 4));
-  PCK(cudaMemsetAsync(c.pt_to_lm.p, 0xff, n_pt * 4, s));
-  k_pt_to_lm<<<grid_for(c.n_lm_l, B), B, 0, s>>>(c.lm_pt.as<int>(), c.n_lm_l, c.pt_to_lm.as<int>());
-  c.launches++;
-  if (c.n_long) {
-    PTRY(c.long_lm.alloc(c.n_long * 4));
-    PTRY(c.long_zb.alloc(c.n_long * 3 * 8));
-    PCK(cudaMemcpyAsync(c.long_lm.p, long_host.data(), c.n_long * 4, cudaMemcpyHostToDevice, s));
-  }
 
-  // --- chunks + camera slots ------------------------------------------------------------------
-  // one chunk per resident CTA of the series kernel (2 per SM); a chunk whose
-  // distinct cameras exceed kSlotCap is split until it fits.
+  // --- chunks + camera slots -------------------------------------------------------------------------
   std::vector<Chunk> chunks;
   {
     const int target = std::max(1, std::min(c.n_tiles, 2 * c.n_sm));
     std::vector<int64_t> cum(c.n_tiles + 1, 0);
     for (int i = 0; i < c.n_tiles; ++i) cum[i + 1] = cum[i] + tiles[i].n;
     int prev = 0;
-    for (int q = 1; q <= target; ++q) {
+    for (int q = 1; q <= target && prev < c.n_tiles; ++q) {
       int64_t want = (nl * q) / target;
       int e = (int)(std::lower_bound(cum.begin(), cum.end(), want) - cum.begin());
       e = std::min(std::max(e, prev + 1), c.n_tiles);
       if (q == target) e = c.n_tiles;
-      if (e > prev) chunks.push_back(Chunk{prev, e, 0, 0});
+      chunks.push_back(Chunk{prev, e, 0, 0});
       prev = e;
-      if (prev >= c.n_tiles) break;
     }
   }
-  const int bch_tiles = std::max(1, bitlen((uint64_t)c.n_tiles));
-  DBuf d_tiles_buf;
   DBuf ka, kb, ukey, fl, pos;
-  PTRY(ka.alloc(nl * 8));
-  PTRY(kb.alloc(nl * 8));
+  PTRY(ka.alloc(ns * 8));
+  PTRY(kb.alloc(ns * 8));
   PTRY(ukey.alloc(nl * 8));
   PTRY(fl.alloc((nl + 1) * 4));
   PTRY(pos.alloc((nl + 1) * 4));
   int n_u = 0;
-  std::vector<int> first;
   for (int iter = 0;; ++iter) {
     for (size_t q = 0; q < chunks.size(); ++q)
       for (int t = chunks[q].tile0; t < chunks[q].tile1; ++t) tiles[t].chunk = (int)q;
     PTRY(c.tiles.alloc(tiles.size() * sizeof(Tile)));
     PCK(cudaMemcpyAsync(c.tiles.p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice, s));
     const int bchunk = std::max(1, bitlen((uint64_t)chunks.size()));
-    if (bchunk + bc > 64) return fail(POBA_EINVAL, "chunk key exceeds 64 bits");
-    k_chunk_cam_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), bc, ka.as<uint64_t>());
-    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), nl, bchunk + bc));
+    if (bchunk + bc > 63) return fail(POBA_EINVAL, "chunk key exceeds 64 bits");
+    k_chunk_cam_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
+    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     k_unique_flags<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, fl.as<int>());
     PCK(cudaMemsetAsync(fl.as<int>() + nl, 0, 4, s));
     PTRY(excl_sum(c, fl.as<int>(), pos.as<int>(), nl + 1));
@@ -515,7 +564,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PTRY(dfirst.alloc(chunks.size() * 4));
     k_chunk_first<<<grid_for(n_u, B), B, 0, s>>>(ukey.as<uint64_t>(), n_u, bc, dfirst.as<int>());
     c.launches++;
-    first.assign(chunks.size() + 1, 0);
+    std::vector<int> first(chunks.size() + 1, 0);
     PCK(cudaMemcpyAsync(first.data(), dfirst.p, chunks.size() * 4, cudaMemcpyDeviceToHost, s));
     PCK(cudaStreamSynchronize(s));
     first[chunks.size()] = n_u;
@@ -525,7 +574,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
       chunks[q].part0 = first[q];
       chunks[q].nslot = first[q + 1] - first[q];
       if (chunks[q].nslot > kSlotCap && chunks[q].tile1 - chunks[q].tile0 > 1) {
-        int mid = (chunks[q].tile0 + chunks[q].tile1) / 2;
+        const int mid = (chunks[q].tile0 + chunks[q].tile1) / 2;
         next.push_back(Chunk{chunks[q].tile0, mid, 0, 0});
         next.push_back(Chunk{mid, chunks[q].tile1, 0, 0});
         split = true;
@@ -535,7 +584,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     }
     if (!split) break;
     chunks.swap(next);
-    if (iter > 40) return fail(POBA_EINVAL, "cannot split chunks under the camera-slot cap");
+    if (iter > 60) return fail(POBA_EINVAL, "cannot split chunks under the camera-slot cap");
   }
   c.n_chunks = (int)chunks.size();
   c.n_partials = n_u;
@@ -544,6 +593,10 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   if (c.max_slots > kSlotCap) return fail(POBA_EINVAL, "a single tile touches more cameras than the slot cap");
   PTRY(c.chunks.alloc(chunks.size() * sizeof(Chunk)));
   PCK(cudaMemcpyAsync(c.chunks.p, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice, s));
+  c.chunks_host = chunks;
+  c.tile_n_host.resize(c.n_tiles);
+  for (int i = 0; i < c.n_tiles; ++i) c.tile_n_host[i] = tiles[i].n;
+  c.work_occ = 0;  // work ranges planned at first launch
 
   // camera -> partials (chunk order)
   {
@@ -567,9 +620,10 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
 
   // per-tile camera segments + tile-local permutation
   {
-    if (bch_tiles + bc + 8 > 64) return fail(POBA_EINVAL, "tile key exceeds 64 bits");
-    k_tile_cam_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_l.as<int>(), bc, ka.as<uint64_t>());
-    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), nl, bch_tiles + bc + 8));
+    const int bt = std::max(1, bitlen((uint64_t)c.n_tiles));
+    if (bt + bc + 8 > 63) return fail(POBA_EINVAL, "tile key exceeds 64 bits");
+    k_tile_cam_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
+    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     k_seg_flags<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, fl.as<int>());
     PCK(cudaMemsetAsync(fl.as<int>() + nl, 0, 4, s));
     PTRY(excl_sum(c, fl.as<int>(), pos.as<int>(), nl + 1));
@@ -578,31 +632,53 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PCK(cudaMemcpyAsync(&nseg, pos.as<int>() + nl, 4, cudaMemcpyDeviceToHost, s));
     PCK(cudaStreamSynchronize(s));
     c.n_segs = nseg;
-    PTRY(c.perm.alloc(nl));
-    PTRY(c.seg_start.alloc(std::max(nseg, 1) * 2));
-    PTRY(c.seg_slot.alloc(std::max(nseg, 1) * 2));
+    PTRY(c.seg_start.alloc(ns * 2));
+    PTRY(c.seg_slot.alloc(ns * 2));
+    PCK(cudaMemsetAsync(c.seg_start.p, 0, ns * 2, s));
+    PCK(cudaMemsetAsync(c.seg_slot.p, 0, ns * 2, s));
     k_segments<<<c.n_tiles, B, 0, s>>>(kb.as<uint64_t>(), fl.as<int>(), pos.as<int>(), c.tiles.as<Tile>(),
-                                       c.chunks.as<Chunk>(), ukey.as<uint64_t>(), bc, c.perm.as<uint8_t>(),
+                                       c.chunks.as<Chunk>(), ukey.as<uint64_t>(), bc, c.perm_s.as<uint8_t>(),
                                        c.seg_start.as<uint16_t>(), c.seg_slot.as<uint16_t>());
     c.launches++;
   }
 
-  // camera-major permutation and chunks for the U0 / b_p reduction
+  // compact kernel descriptors (chunk bounds folded into the flags)
   {
-    k_cam_obs_keys<<<grid_for(nl, B), B, 0, s>>>(c.cam_l.as<int>(), nl, ka.as<uint64_t>());
-    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), nl, 32 + bc));
+    std::vector<Tile> tt(c.n_tiles);
+    PCK(cudaMemcpy(tt.data(), c.tiles.p, c.n_tiles * sizeof(Tile), cudaMemcpyDeviceToHost));
+    std::vector<TileK> tk(c.n_tiles);
+    for (int i = 0; i < c.n_tiles; ++i) {
+      const Chunk& ch = chunks[tt[i].chunk];
+      TileK& k = tk[i];
+      k.n = tt[i].n;
+      k.lm0 = tt[i].lm0;
+      k.nlm = tt[i].nlm;
+      k.nseg = tt[i].nseg;
+      k.flags = tt[i].flags | (i == ch.tile0 ? kTileChunkFirst : 0) | (i + 1 == ch.tile1 ? kTileChunkLast : 0);
+      k.part0 = ch.part0;
+      k.nslot = ch.nslot;
+      k.chunk = tt[i].chunk;
+    }
+    PTRY(c.tilek.alloc(c.n_tiles * sizeof(TileK)));
+    PCK(cudaMemcpy(c.tilek.p, tk.data(), c.n_tiles * sizeof(TileK), cudaMemcpyHostToDevice));
+  }
+
+  // camera-major permutation of slots for the U0 / b_p reduction
+  {
+    k_cam_slot_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), ka.as<uint64_t>());
+    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     PTRY(c.cperm.alloc(nl * 4));
     k_low32<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, c.cperm.as<int>());
     DBuf deg, ccnt;
     PTRY(deg.alloc((n_cam + 1) * 4));
     PTRY(ccnt.alloc((n_cam + 1) * 4));
     PCK(cudaMemsetAsync(deg.p, 0, (n_cam + 1) * 4, s));
-    k_cam_degree<<<grid_for(nl, B), B, 0, s>>>(c.cam_l.as<int>(), nl, deg.as<int>());
+    k_cam_degree<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, deg.as<int>());
     k_cc_counts<<<grid_for(n_cam, B), B, 0, s>>>(deg.as<int>(), n_cam, ccnt.as<int>());
     PCK(cudaMemsetAsync(ccnt.as<int>() + n_cam, 0, 4, s));
     c.launches += 4;
-    PTRY(c.cc_start.alloc((n_cam + 1) * 4));  // camera -> first observation in cperm
-    PTRY(excl_sum(c, deg.as<int>(), c.cc_start.as<int>(), n_cam + 1));
+    PTRY(c.cam_start.alloc((n_cam + 1) * 4));
+    PTRY(excl_sum(c, deg.as<int>(), c.cam_start.as<int>(), n_cam + 1));
     PTRY(c.cc_cam_off.alloc((n_cam + 1) * 4));
     PTRY(excl_sum(c, ccnt.as<int>(), c.cc_cam_off.as<int>(), n_cam + 1));
     int ncc = 0;
@@ -611,22 +687,22 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     c.n_cchunks = ncc;
   }
 
-  // --- per-context work buffers ---------------------------------------------------------------
-  PTRY(c.J.alloc((size_t)kJPlanes * c.obs_pad * 16));
-  PTRY(c.Rz.alloc((size_t)c.obs_pad * 16));
-  PCK(cudaMemsetAsync(c.J.p, 0, (size_t)kJPlanes * c.obs_pad * 16, s));
-  PCK(cudaMemsetAsync(c.Rz.p, 0, (size_t)c.obs_pad * 16, s));
-  const int64_t nc = n_cam, nlm = c.n_lm_l;
+  // --- work buffers --------------------------------------------------------------------------------------
+  PTRY(c.J.alloc((size_t)kJPlanes * ns * 16));
+  PTRY(c.Rz.alloc((size_t)ns * 16));
+  PCK(cudaMemsetAsync(c.J.p, 0, (size_t)kJPlanes * ns * 16, s));
+  PCK(cudaMemsetAsync(c.Rz.p, 0, (size_t)ns * 16, s));
+  const int64_t nc = n_cam, nlm1 = std::max<int64_t>(nlm, 1);
   for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.bt, &c.tvec, &c.xvec, &c.rvec, &c.ctmp, &c.ctmp2})
     PTRY(b->alloc(nc * 9 * 8));
   for (DBuf* b : {&c.cams_prep, &c.trial_prep}) PTRY(b->alloc(nc * 16 * 8));
   for (DBuf* b : {&c.U0, &c.Uinv, &c.Ud}) PTRY(b->alloc(nc * 45 * 8));
-  for (DBuf* b : {&c.points, &c.bl, &c.Dl, &c.dl, &c.ltmp}) PTRY(b->alloc(std::max<int64_t>(nlm, 1) * 3 * 8));
-  for (DBuf* b : {&c.V0, &c.Vinv, &c.Vd}) PTRY(b->alloc(std::max<int64_t>(nlm, 1) * 6 * 8));
+  for (DBuf* b : {&c.points, &c.bl, &c.Dl, &c.dl, &c.ltmp}) PTRY(b->alloc(nlm1 * 3 * 8));
+  for (DBuf* b : {&c.V0, &c.Vinv, &c.Vd}) PTRY(b->alloc(nlm1 * 6 * 8));
   PTRY(c.cc_part.alloc(std::max(c.n_cchunks, 1) * 54 * 8));
   PTRY(c.partials.alloc(std::max(c.n_partials, 1) * 9 * 8));
   PTRY(c.state.alloc(sizeof(SeriesState)));
-  PTRY(c.blk_part.alloc(4096 * 4 * 8));
+  PTRY(c.blk_part.alloc((grid_for(n_cam, 8) + 8) * 4 * 8));
   PTRY(c.flag.alloc(64));
   PTRY(c.red.alloc(64 * 8));
   PCK(cudaMemsetAsync(c.state.p, 0, sizeof(SeriesState), s));
