@@ -152,6 +152,8 @@ int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_ter
                     int* launches);
 /* kernel launches issued by the library since creation (all entry points)  */
 int64_t poba_launch_count(poba_ctx* ctx);
+/* the cudaStream_t every kernel of this context runs on (for external events) */
+int poba_stream(poba_ctx* ctx, void** stream);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,7 @@ _SIGS = {
     "poba_read": (ctypes.c_int, [_P, ctypes.c_int, _DP]),
     "poba_time_terms": (ctypes.c_int, [_P, ctypes.c_int, _DP, _DP, _IP]),
     "poba_launch_count": (ctypes.c_int64, [_P]),
+    "poba_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -253,3 +254,8 @@ class Device:
 
     def launch_count(self) -> int:
         return int(self._lib.poba_launch_count(self._h))
+
+    def stream_ptr(self) -> int:
+        s = _P()
+        _check(self._lib.poba_stream(self._h, ctypes.byref(s)))
+        return int(s.value or 0)

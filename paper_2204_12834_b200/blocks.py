@@ -441,7 +441,9 @@ def linearize(problem, state=None, precision: int = 64, device: int = 0) -> Line
     n_invalid = dp.dev.linearize(cams, pts)
     if n_invalid:
         log.warning("%d observation(s) had zero projected depth and were zeroed", n_invalid)
-    return Linearization(dp, ("state", cams.copy(), pts.copy()), n_invalid)
+    # the source arrays are kept by reference (no copy), like the reference keeps
+    # no copy at all; callers must not mutate them while the Linearization lives
+    return Linearization(dp, ("state", cams, pts), n_invalid)
 
 
 def assemble(problem, state=None, lam: float = 1e-4, precision: int = 64,

@@ -515,4 +515,10 @@ int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_ter
 
 int64_t poba_launch_count(poba_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int poba_stream(poba_ctx* ctx, void** stream) {
+  NEED(ctx && stream, "null argument");
+  *stream = (void*)ctx->c.stream;
+  return POBA_OK;
+}
+
 }  // extern "C"
