@@ -186,6 +186,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// streamed-once data: evict-first in L2 so the chunk accumulators stay resident
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -256,8 +270,10 @@ __global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
     fence_proxy_async();
     mbar_expect_tx(bar, (uint32_t)(kJPlanes * d.x * 16 + 2 * kTile + 4 * kTile + 32) + vbytes);
     const int64_t s0 = (int64_t)ti * kTile;
+    const uint64_t pol = policy_evict_first();
 #pragma unroll 1
-    for (int p = 0; p < kJPlanes; ++p) bulk_g2s(stg + p * kTile * 16, a.J + p * a.ns + s0, (uint32_t)(d.x * 16), bar);
+    for (int p = 0; p < kJPlanes; ++p)
+      bulk_g2s_stream(stg + p * kTile * 16, a.J + p * a.ns + s0, (uint32_t)(d.x * 16), bar, pol);
     bulk_g2s(stg + kStPerm, a.perm_s + s0, kTile, bar);
     bulk_g2s(stg + kStLidx, a.lidx_s + s0, kTile, bar);
     bulk_g2s(stg + kStSegStart, a.seg_start + s0, 2 * kTile, bar);
@@ -271,9 +287,10 @@ __global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
     if (kStages < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + kStages);
   }
 
-  // camera-vector gathers run one tile ahead, camera indices two tiles ahead
-  // (padding slots carry camera 0, so these loads need no descriptor)
-  double tc[9], tn[9];
+  // camera-vector gathers run one tile ahead (issued once the current tile's
+  // vector is consumed), camera indices two tiles ahead; padding slots carry
+  // camera 0, so these loads need no descriptor
+  double tc[9];
   int cn = 0;
   if (MODE == kModeTerm) {
     const double* tv = a.tin + (int64_t)a.cam_s[(int64_t)wr.x * kTile + tid] * 9;
@@ -284,14 +301,6 @@ __global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
 
   for (int q = 0; q < nq; ++q) {
     const int ti = wr.x + q;
-    if (MODE == kModeTerm) {
-      if (q + 1 < nq) {
-        const double* tv = a.tin + (int64_t)cn * 9;
-#pragma unroll
-        for (int j = 0; j < 9; ++j) tn[j] = tv[j];
-      }
-      if (q + 2 < nq) cn = a.cam_s[(int64_t)(ti + 2) * kTile + tid];
-    }
     uint8_t* stg = smraw + (q % kStages) * kStageBytes;
     mbar_wait(&bars[q % kStages], (uint32_t)((q / kStages) & 1));
     const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
@@ -324,7 +333,15 @@ __global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
 #pragma unroll
       for (int b = 0; b < 3; ++b) wbuf[tid * 3 + b] = fma(jr[9 + b].x, u0, jr[9 + b].y * u1);
     }
-    if (MODE == kModeTerm) __syncthreads();  // A2
+    if (MODE == kModeTerm) {
+      if (q + 1 < nq) {  // tc is consumed: start the next tile's gather
+        const double* tv = a.tin + (int64_t)cn * 9;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) tc[j] = tv[j];
+      }
+      if (q + 2 < nq) cn = a.cam_s[(int64_t)(ti + 2) * kTile + tid];
+      __syncthreads();  // A2
+    }
     // phase 2: per landmark z_l, four lanes per landmark (lane c sums y_c)
     {
       const int lmi = tid >> 2, c = tid & 3;
@@ -375,35 +392,35 @@ __global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
       const uint16_t* sl = reinterpret_cast<const uint16_t*>(stg + kStSegSlot);
       const uint8_t* pm = stg + kStPerm;
       const int items = t.nseg * 9;
-      double sum[9];
       int dst[9];
+      double old[9];
 #pragma unroll
       for (int u = 0; u < 9; ++u) {
         const int k = tid + u * kTile;
-        sum[u] = 0.0;
         dst[u] = -1;
         if (k < items) {
-          const int sg = k / 9, comp = k - sg * 9;
-          const int r0 = ss[sg], r1 = (sg + 1 < t.nseg) ? ss[sg + 1] : t.n;
-          for (int r = r0; r < r1; ++r) sum[u] += gbuf[pm[r] * 9 + comp];
-          dst[u] = sl[sg] * 9 + comp;
+          const int sg = k / 9;
+          dst[u] = sl[sg] * 9 + (k - sg * 9);
         }
       }
-      double old[9];
 #pragma unroll
       for (int u = 0; u < 9; ++u) old[u] = dst[u] >= 0 ? acc[dst[u]] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 9; ++u)
-        if (dst[u] >= 0) acc[dst[u]] = old[u] + sum[u];
+      for (int u = 0; u < 9; ++u) {
+        const int k = tid + u * kTile;
+        if (k < items) {
+          const int sg = k / 9, comp = k - sg * 9;
+          const int r0 = ss[sg], r1 = (sg + 1 < t.nseg) ? ss[sg + 1] : t.n;
+          double sum = 0.0;
+          for (int r = r0; r < r1; ++r) sum += gbuf[pm[r] * 9 + comp];
+          acc[dst[u]] = old[u] + sum;
+        }
+      }
     }
     __syncthreads();  // D: stage free, accumulator updates visible to the next tile
     if (tid == 0 && q + kStages < nq) {
       issue(q + kStages, dnext);
       if (q + kStages + 1 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + ti + kStages + 1);
-    }
-    if (MODE == kModeTerm) {
-#pragma unroll
-      for (int j = 0; j < 9; ++j) tc[j] = tn[j];
     }
   }
 }
