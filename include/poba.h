@@ -154,6 +154,8 @@ int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_ter
 int64_t poba_launch_count(poba_ctx* ctx);
 /* the cudaStream_t every kernel of this context runs on (for external events) */
 int poba_stream(poba_ctx* ctx, void** stream);
+/* instrumentation counters of POBA_PHASE_TIMING builds (8 x uint64, reset on read) */
+int poba_debug_counters(poba_ctx* ctx, uint64_t* out);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,7 @@ _SIGS = {
     "poba_time_terms": (ctypes.c_int, [_P, ctypes.c_int, _DP, _DP, _IP]),
     "poba_launch_count": (ctypes.c_int64, [_P]),
     "poba_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "poba_debug_counters": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -254,6 +255,11 @@ class Device:
 
     def launch_count(self) -> int:
         return int(self._lib.poba_launch_count(self._h))
+
+    def debug_counters(self):
+        out = (ctypes.c_uint64 * 8)()
+        _check(self._lib.poba_debug_counters(self._h, out))
+        return list(out)
 
     def stream_ptr(self) -> int:
         s = _P()

@@ -481,7 +481,7 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
       // observations owned by other ranks are left untouched
       PTRY(poba::build_canonical_order(c));
       const int64_t ns = c.n_slots, n = c.n_obs;
-      std::vector<double> J((size_t)poba::kJPlanes * ns * 2), R(ns * 2);
+      std::vector<double> J((size_t)poba::kRow * ns * 2), R(ns * 2);
       std::vector<int> file(ns), order(n), slot_of_file(n, -1);
       PCK(cudaMemcpy(J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
       PCK(cudaMemcpy(R.data(), c.Rz.p, R.size() * 8, cudaMemcpyDeviceToHost));
@@ -494,7 +494,7 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
         if (q < 0) continue;
         for (int a = 0; a < 2; ++a) {
           double* row = dst + (i * 2 + a) * 13;
-          for (int j = 0; j < 12; ++j) row[j] = J[((size_t)j * ns + q) * 2 + a];
+          for (int j = 0; j < 12; ++j) row[j] = J[((size_t)q * poba::kRow + j) * 2 + a];
           row[12] = R[q * 2 + a];
         }
       }
@@ -514,6 +514,18 @@ int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_ter
 }
 
 int64_t poba_launch_count(poba_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+// instrumentation (POBA_PHASE_TIMING builds): read and reset 8 counters
+int poba_debug_counters(poba_ctx* ctx, uint64_t* out) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  PTRY(c.dbg.alloc(64));
+  if (out) {
+    PCK(cudaMemcpy(out, c.dbg.p, 64, cudaMemcpyDeviceToHost));
+  }
+  PCK(cudaMemset(c.dbg.p, 0, 64));
+  return POBA_OK;
+}
 
 int poba_stream(poba_ctx* ctx, void** stream) {
   NEED(ctx && stream, "null argument");

@@ -125,29 +125,30 @@ __device__ __forceinline__ void evaluate_obs(const double* __restrict__ cp, doub
   m.jp0[8] = fs * s * p0; m.jp1[8] = fs * s * p1;
 }
 
-// Store + per-observation V0/b_l contributions + per-landmark sums, each
-// landmark's observations in camera order (np.add.at's sequential fold of
-// blocks.py:394,396 runs over the same observations in the same order).
+// Store rows + per-observation V0/b_l contributions + per-landmark sums; one
+// warp per warp-tile, each landmark's observations in camera order (np.add.at's
+// sequential fold of blocks.py:394,396 runs over the same observations in the
+// same order).
 template <bool kExplicit>
-__global__ void __launch_bounds__(kTile)
-k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const int* __restrict__ file_s,
-           const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s, const double* __restrict__ prep,
-           const double* __restrict__ points, const double* __restrict__ ejp, const double* __restrict__ ejl,
-           const double* __restrict__ eres, double2* __restrict__ J, double2* __restrict__ Rz, int64_t ns,
-           double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
+__global__ void __launch_bounds__(kBlockTiles * kTile)
+k_lin_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
+           const int* __restrict__ file_s, const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s,
+           const double* __restrict__ prep, const double* __restrict__ points, const double* __restrict__ ejp,
+           const double* __restrict__ ejl, const double* __restrict__ eres, double2* __restrict__ J,
+           double2* __restrict__ Rz, double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
            unsigned long long* __restrict__ n_invalid) {
-  __shared__ double contrib[kTile * 9];
-  __shared__ int lstart[kTile + 1];
-  __shared__ int bad_count;
-  const Tile t = tiles[blockIdx.x];
-  const int64_t s0 = (int64_t)blockIdx.x * kTile;
-  const int i = threadIdx.x;
+  __shared__ double contrib_all[kBlockTiles][kTile * 9];
+  __shared__ int lstart_all[kBlockTiles][kTile + 1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ti = blockIdx.x * kBlockTiles + w;
+  if (ti >= n_tiles) return;  // warps are independent: no block-wide barrier below
+  double* contrib = contrib_all[w];
+  int* lstart = lstart_all[w];
+  const Tile t = tiles[ti];
+  const int64_t o = (int64_t)ti * kTile + lane;
   const bool is_long = t.flags & kTileLong;
-  if (i == 0) bad_count = 0;
-  if (!is_long) tile_landmark_starts(lidx_s + s0, t.n, t.nlm, lstart);
-  __syncthreads();
-  if (i < t.n) {
-    const int64_t o = s0 + i;
+  bool bad = false;
+  if (lane < t.n) {
     ObsModel m;
     if (kExplicit) {
       const int64_t f = file_s[o];
@@ -168,14 +169,15 @@ k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const 
       const int lm = t.lm0 + (is_long ? 0 : lidx_s[o]);
       const double* X = points + (int64_t)lm * 3;
       evaluate_obs<true>(prep + (int64_t)cam_s[o] * 16, X[0], X[1], X[2], pix_s[o], m);
-      if (!m.valid) atomicAdd(&bad_count, 1);
+      bad = !m.valid;
     }
+    double2* row = J + o * kRow;
 #pragma unroll
-    for (int j = 0; j < 9; ++j) J[j * ns + o] = make_double2(m.jp0[j], m.jp1[j]);
+    for (int j = 0; j < 9; ++j) row[j] = make_double2(m.jp0[j], m.jp1[j]);
 #pragma unroll
-    for (int b = 0; b < 3; ++b) J[(9 + b) * ns + o] = make_double2(m.jl0[b], m.jl1[b]);
+    for (int b = 0; b < 3; ++b) row[9 + b] = make_double2(m.jl0[b], m.jl1[b]);
     Rz[o] = make_double2(m.r0, m.r1);
-    double* cc = contrib + i * 9;
+    double* cc = contrib + lane * 9;
     cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
     cc[1] = m.jl0[0] * m.jl0[1] + m.jl1[0] * m.jl1[1];
     cc[2] = m.jl0[0] * m.jl0[2] + m.jl1[0] * m.jl1[2];
@@ -185,11 +187,17 @@ k_lin_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const 
     cc[6] = m.jl0[0] * m.r0 + m.jl1[0] * m.r1;
     cc[7] = m.jl0[1] * m.r0 + m.jl1[1] * m.r1;
     cc[8] = m.jl0[2] * m.r0 + m.jl1[2] * m.r1;
+    if (!is_long) {
+      const int li = lidx_s[o];
+      if (lane == 0 || lidx_s[o - 1] != li) lstart[li] = lane;
+    }
   }
-  __syncthreads();
-  if (i == 0 && bad_count) atomicAdd(n_invalid, (unsigned long long)bad_count);
+  if (lane == 0) lstart[t.nlm] = t.n;
+  const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
+  if (lane == 0 && nbad) atomicAdd(n_invalid, (unsigned long long)nbad);
+  __syncwarp();
   if (is_long) return;  // long landmarks are reduced by k_lin_long
-  for (int q = i; q < t.nlm * 9; q += kTile) {
+  for (int q = lane; q < t.nlm * 9; q += kTile) {
     const int j = q / 9, comp = q - j * 9;
     double acc = 0.0;
     for (int r = lstart[j]; r < lstart[j + 1]; ++r) acc += contrib[r * 9 + comp];
@@ -213,7 +221,8 @@ __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restric
   if (comp >= 9) return;
   double acc = 0.0;
   for (int o = o0; o < o1; ++o) {
-    const double2 a = J[(9 + 0) * pad + o], b = J[(9 + 1) * pad + o], c = J[(9 + 2) * pad + o];
+    const double2* row = J + (int64_t)o * kRow;
+    const double2 a = row[9], b = row[10], c = row[11];
     const double2 r = Rz[o];
     double v;
     switch (comp) {
@@ -264,9 +273,10 @@ k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ c
   for (int p = p0 + lane; p < p1; p += 32) {
     const int o = cperm[p];
     double a[9], b[9];
+    const double2* row = J + (int64_t)o * kRow;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = J[j * pad + o];
+      const double2 v = row[j];
       a[j] = v.x;
       b[j] = v.y;
     }
@@ -317,42 +327,46 @@ __global__ void k_cam_dp(const double* __restrict__ U0, int64_t n_cam, double* _
   Dp[q] = sqrt(fmin(fmax(v, kClampLo * kClampLo), kClampHi * kClampHi));
 }
 
-// 0.5 sum ||r||^2 per tile (fixed tree), invalid counts
-__global__ void __launch_bounds__(kTile)
-k_cost_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const double2* __restrict__ pix_s,
-            const uint8_t* __restrict__ lidx_s, const double* __restrict__ prep, const double* __restrict__ points,
-            const double* __restrict__ dl, double* __restrict__ tile_sum, unsigned long long* __restrict__ n_invalid) {
-  __shared__ double red[kTile];
-  __shared__ int bad_count;
-  const Tile t = tiles[blockIdx.x];
-  const int64_t s0 = (int64_t)blockIdx.x * kTile;
-  const int i = threadIdx.x;
-  if (i == 0) bad_count = 0;
-  __syncthreads();
+// 0.5 sum ||r||^2: per warp-tile butterfly, per block fixed-order sum, invalid counts
+__global__ void __launch_bounds__(kBlockTiles * kTile)
+k_cost_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
+            const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s, const double* __restrict__ prep,
+            const double* __restrict__ points, const double* __restrict__ dl, double* __restrict__ block_sum,
+            unsigned long long* __restrict__ n_invalid) {
+  __shared__ double wsum[kBlockTiles];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ti = blockIdx.x * kBlockTiles + w;
   double v = 0.0;
-  if (i < t.n) {
-    const int64_t o = s0 + i;
-    const int lm = t.lm0 + ((t.flags & kTileLong) ? 0 : lidx_s[o]);
-    double X0 = points[(int64_t)lm * 3], X1 = points[(int64_t)lm * 3 + 1], X2 = points[(int64_t)lm * 3 + 2];
-    if (dl) {
-      X0 += dl[(int64_t)lm * 3];
-      X1 += dl[(int64_t)lm * 3 + 1];
-      X2 += dl[(int64_t)lm * 3 + 2];
+  bool bad = false;
+  if (ti < n_tiles) {
+    const Tile t = tiles[ti];
+    if (lane < t.n) {
+      const int64_t o = (int64_t)ti * kTile + lane;
+      const int lm = t.lm0 + ((t.flags & kTileLong) ? 0 : lidx_s[o]);
+      double X0 = points[(int64_t)lm * 3], X1 = points[(int64_t)lm * 3 + 1], X2 = points[(int64_t)lm * 3 + 2];
+      if (dl) {
+        X0 += dl[(int64_t)lm * 3];
+        X1 += dl[(int64_t)lm * 3 + 1];
+        X2 += dl[(int64_t)lm * 3 + 2];
+      }
+      ObsModel m;
+      evaluate_obs<false>(prep + (int64_t)cam_s[o] * 16, X0, X1, X2, pix_s[o], m);
+      bad = !m.valid;
+      v = m.r0 * m.r0 + m.r1 * m.r1;
     }
-    ObsModel m;
-    evaluate_obs<false>(prep + (int64_t)cam_s[o] * 16, X0, X1, X2, pix_s[o], m);
-    if (!m.valid) atomicAdd(&bad_count, 1);
-    v = m.r0 * m.r0 + m.r1 * m.r1;
   }
-  red[i] = v;
+#pragma unroll
+  for (int s = 16; s; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
+  if (lane == 0) {
+    wsum[w] = v;
+    if (nbad) atomicAdd(n_invalid, (unsigned long long)nbad);
+  }
   __syncthreads();
-  for (int st = kTile / 2; st > 0; st >>= 1) {
-    if (i < st) red[i] += red[i + st];
-    __syncthreads();
-  }
-  if (i == 0) {
-    tile_sum[blockIdx.x] = red[0];
-    if (bad_count) atomicAdd(n_invalid, (unsigned long long)bad_count);
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int k = 0; k < kBlockTiles; ++k) b += wsum[k];
+    block_sum[blockIdx.x] = b;
   }
 }
 
@@ -396,18 +410,17 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   }
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 32);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
+  const unsigned nb = grid_for(c.n_tiles, kBlockTiles);
   if (expl)
-    k_lin_tile<true><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.file_s.as<int>(),
-                                                 c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(), nullptr, nullptr,
-                                                 ejp.as<double>(), ejl.as<double>(), eres.as<double>(),
-                                                 c.J.as<double2>(), c.Rz.as<double2>(), ns, c.V0.as<double>(),
-                                                 c.bl.as<double>(), c.Dl.as<double>(), d_bad);
+    k_lin_tile<true><<<nb, kBlockTiles * kTile, 0, s>>>(
+        c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
+        c.lidx_s.as<uint8_t>(), nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>(),
+        c.J.as<double2>(), c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(), c.Dl.as<double>(), d_bad);
   else
-    k_lin_tile<false><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.file_s.as<int>(),
-                                                  c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(),
-                                                  c.cams_prep.as<double>(), c.points.as<double>(), nullptr,
-                                                  nullptr, nullptr, c.J.as<double2>(), c.Rz.as<double2>(), ns,
-                                                  c.V0.as<double>(), c.bl.as<double>(), c.Dl.as<double>(), d_bad);
+    k_lin_tile<false><<<nb, kBlockTiles * kTile, 0, s>>>(
+        c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
+        c.lidx_s.as<uint8_t>(), c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr,
+        c.J.as<double2>(), c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(), c.Dl.as<double>(), d_bad);
   c.launches++;
   PCK(cudaGetLastError());
   if (c.n_long) {
@@ -453,13 +466,15 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
 
 int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid) {
   cudaStream_t s = c.stream;
-  PTRY(c.scratch_c.alloc((c.n_tiles + 8) * 8));
+  const unsigned nb = grid_for(c.n_tiles, kBlockTiles);
+  PTRY(c.scratch_c.alloc((nb + 8) * 8));
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 40);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
-  k_cost_tile<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.pix_s.as<double2>(),
-                                          c.lidx_s.as<uint8_t>(), c.trial_prep.as<double>(), c.points.as<double>(),
-                                          trial ? c.dl.as<double>() : nullptr, c.scratch_c.as<double>(), d_bad);
-  k_sum_fixed<<<1, 1024, 0, s>>>(c.scratch_c.as<double>(), c.n_tiles, c.red.as<double>());
+  k_cost_tile<<<nb, kBlockTiles * kTile, 0, s>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(),
+                                                 c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(),
+                                                 c.trial_prep.as<double>(), c.points.as<double>(),
+                                                 trial ? c.dl.as<double>() : nullptr, c.scratch_c.as<double>(), d_bad);
+  k_sum_fixed<<<1, 1024, 0, s>>>(c.scratch_c.as<double>(), nb, c.red.as<double>());
   c.launches += 2;
   PCK(cudaGetLastError());
   double sum = 0;

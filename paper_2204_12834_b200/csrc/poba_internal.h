@@ -13,17 +13,33 @@
 namespace poba {
 
 // ---- fixed geometry ------------------------------------------------------------
-// The device store is landmark-major in "slot space": tile t owns slots
-// [t*kTile, t*kTile + n_t); a tile packs whole landmarks (index order, each
-// landmark's observations sorted by camera) until kTile observations; a
-// landmark with k > kTile spans consecutive full sub-tiles.  Padding slots are
-// never read by the kernels (bulk copies move exactly n_t rows per plane).
-constexpr int kTile = 256;        // observation slots per tile == threads per CTA
-constexpr int kSlotCap = 16384;   // max distinct cameras per chunk (uint16 slot ids; bounds the L2-resident partials)
+// The device store is landmark-major in "slot space": warp-tile t owns slots
+// [t*kTile, t*kTile + n_t); a warp-tile packs whole landmarks (index order, each
+// landmark's observations sorted by camera) up to kTile observations and kTileLm
+// landmarks; a landmark with k > kTile spans consecutive full sub-tiles.  Each
+// slot is one 208-byte row of 13 double2: the 2x9 pose Jacobian (9 column
+// pairs), the 2x3 point Jacobian (3 column pairs) and a 16-byte metadata word
+// (camera, tile-local camera permutation, landmark index, camera segment) --
+// the reference's 2x13 block row with the residual column replaced by the
+// metadata (residuals live in their own array; the series never reads them).
+constexpr int kTile = 32;         // observation slots per warp-tile (one warp)
+constexpr int kTileLm = 32;       // landmarks per warp-tile (bounds the staged V^-1 slice)
+constexpr int kRow = 13;          // double2 per slot row
+constexpr int kRowBytes = kRow * 16;
+constexpr int kBlockTiles = 8;    // warp-tiles per CTA in the streaming kernels (256 threads)
+constexpr int kSlotCap = 65535;   // uint16 camera-slot ids per chunk
 constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
-constexpr int kJPlanes = 12;      // double2 planes: 9 x (Jp[0][j],Jp[1][j]) + 3 x (Jl[0][b],Jl[1][b])
-constexpr int kStages = 2;        // bulk-copy pipeline depth of the term kernel
-constexpr int kMaxLmPerTile = 64; // landmarks per tile (bounds the staged V^-1 slice)
+constexpr int kJPlanes = 12;      // Jacobian column pairs per row
+constexpr int kStages = 2;        // bulk-copy pipeline depth per warp of the term kernel
+constexpr int kTermWarps = 10;    // independent warps per CTA of the term kernel
+
+// metadata word (row entry 12, as int4)
+struct RowMeta {
+  int cam;
+  int packed;  // perm (bits 0-7) | landmark index in tile (8-15) | segment start (16-23)
+  int seg_slot;
+  int pad;
+};
 
 // Error plumbing ---------------------------------------------------------------
 void set_error(const std::string& msg);
@@ -155,7 +171,7 @@ struct Ctx {
   DBuf tiles;        // Tile [n_tiles]
   DBuf tilek;        // TileK [n_tiles]
   DBuf chunks;       // Chunk [n_chunks]
-  DBuf work;         // int2 [n_work] contiguous tile ranges, one per CTA of the term kernel
+  DBuf work;         // int4 [n_work] (tile0, tile1, part0, nslot): one chunk per warp of the term kernel
   DBuf cam_s;        // int32 [n_slots] camera of each slot
   DBuf file_s;       // int32 [n_slots] file index of each slot (-1 padding)
   DBuf pix_s;        // double2 [n_slots] pixels
@@ -163,15 +179,13 @@ struct Ctx {
   DBuf perm_s;       // uint8 [n_slots] tile-local position sorted by camera
   DBuf lm_slot0;     // int32 [n_lm_l] first slot of each local landmark
   DBuf lm_k;         // int32 [n_lm_l]
-  DBuf seg_start;    // uint16 [n_slots] per tile: start position of segment s at tile*kTile + s
+  DBuf seg_start;    // uint8 [n_slots] per tile: start position of segment s at tile*kTile + s
   DBuf seg_slot;     // uint16 [n_slots] per tile: chunk slot of segment s
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
   DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
   std::vector<int> long_host;
   std::vector<Chunk> chunks_host;
-  std::vector<int> tile_n_host;
-  int work_occ = 0;  // CTAs/SM the work ranges were planned for
   // camera-major reduction chunks
   int n_cchunks = 0;
   DBuf cperm;        // int32 [n_obs_l] slots sorted by (camera, slot)
@@ -179,7 +193,7 @@ struct Ctx {
   DBuf cc_cam_off;   // int32 [n_cam+1] camera -> cchunk range
 
   // store (K1), slot space
-  DBuf J;            // double2 [kJPlanes][n_slots]
+  DBuf J;            // double2 [n_slots][kRow] rows (J_p pairs, J_l pairs, metadata)
   DBuf Rz;           // double2 [n_slots] residuals
 
   // camera arrays
@@ -216,6 +230,7 @@ struct Ctx {
   DBuf ctmp;         // double [n_cam*9] scratch
   DBuf ctmp2;        // double [n_cam*9]
   DBuf flag;         // int [16]
+  DBuf dbg;          // instrumentation counters (POBA_PHASE_TIMING builds)
   DBuf red;          // double scratch for reductions
   DBuf cub_tmp;      // CUB temp storage
 

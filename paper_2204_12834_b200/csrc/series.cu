@@ -204,15 +204,12 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 struct TermArgs {
-  const TileK* tk;         // per-tile kernel descriptors
-  const int2* work;        // per-CTA contiguous tile range (whole chunks)
-  const int* cam_s;
-  const uint8_t* perm_s;
-  const uint8_t* lidx_s;
-  const uint16_t* seg_start;
-  const uint16_t* seg_slot;
-  const double2* J;
-  int64_t ns;              // plane stride = slots
+  unsigned long long* dbg;  // POBA_PHASE_TIMING: per-phase cycle totals (8 entries)
+  const TileK* tk;         // per warp-tile kernel descriptors
+  const int* cam_s;        // camera of each slot (prefetch of the camera-vector gather)
+  const int4* work;        // per warp: (tile0, tile1, part0, nslot) -- one chunk
+  int n_work;
+  const double2* J;        // slot rows
   const double* tin;       // camera vector (kModeTerm)
   const double* lvec;      // b_l (kModeBt) or landmark input (kModeW)
   const double* Vinv;
@@ -222,107 +219,120 @@ struct TermArgs {
   int check_stop;
 };
 
-// shared-memory carve-up of k_term (bytes).  One stage holds everything a tile
-// needs, moved by bulk copies: the 12 Jacobian planes, the camera permutation,
-// the landmark index, the camera segments, the descriptor and the V^-1 slice.
-// After phase 1 the Jacobians live in registers, so the plane area doubles as
-// scratch for w (planes 9..11) and g (planes 0..8); the stage is released for
-// the next bulk copy at the end of the tile.  The per-chunk camera-slot
-// accumulators live in the chunk's own (CTA-exclusive, L2-resident) partial
-// buffer, so two CTAs fit per SM.
-constexpr int kStPlanes = kJPlanes * kTile * 16;            // 49152
-constexpr int kStPerm = kStPlanes;                          // +256
-constexpr int kStLidx = kStPerm + kTile;                    // +256
-constexpr int kStSegStart = kStLidx + kTile;                // +512
-constexpr int kStSegSlot = kStSegStart + kTile * 2;         // +512
-constexpr int kStDesc = kStSegSlot + kTile * 2;             // +32
-constexpr int kStVinv = kStDesc + 32;                       // +64*48
-constexpr int kStageBytes = (kStVinv + kMaxLmPerTile * 48 + 127) / 128 * 128;
-constexpr int kOffBars = kStages * kStageBytes;
-constexpr int kOffZ = kOffBars + 64;
-constexpr int kOffL = kOffZ + kMaxLmPerTile * 3 * 8;
-constexpr int kTermSmem = kOffL + (kTile + 4) * 4;
-static_assert(2 * (kTermSmem + 1024) <= 228 * 1024, "term kernel must fit two CTAs per SM");
+// Per-warp shared memory (bytes): kStages stages of one warp-tile (32 rows of
+// 208 B, the 32-B descriptor and the V^-1 slice of its landmarks), plus
+// scratch for w, z, g and the segment/permutation tables.
+constexpr int kStDesc = kTile * kRowBytes;                 // 6656
+constexpr int kStVinv = kStDesc + 32;                      // 6688
+constexpr int kStageBytes = (kStVinv + kTileLm * 48 + 127) / 128 * 128;
+constexpr int kWOffBars = kStages * kStageBytes;
+constexpr int kWOffG = kWOffBars + 16 * kStages;           // g: 32 x 10 doubles (16-B aligned rows)
+constexpr int kWOffW = kWOffG + kTile * 10 * 8;
+constexpr int kWOffZ = kWOffW + kTile * 3 * 8;
+constexpr int kWOffL = kWOffZ + kTileLm * 3 * 8;           // landmark starts (33 ints)
+constexpr int kWOffP = kWOffL + (kTile + 4) * 4;           // permutation (32 B) + segment starts (36 B)
+constexpr int kWarpSmem = (kWOffP + 2 * kTile + 8 + 127) / 128 * 128;
+constexpr int kTermSmem = kTermWarps * kWarpSmem;
+static_assert(kTermSmem <= 227 * 1024, "term kernel shared memory over budget");
 
+// One warp streams one chunk of warp-tiles through its own bulk-copy pipeline;
+// warps never wait on each other (no block-wide barrier in the loop).  Within a
+// warp-tile the landmark sums are a segmented warp scan (landmarks are runs of
+// consecutive lanes), V^-1 is applied by each landmark's last lane and z is
+// broadcast back by shuffle; camera segments are summed through shared memory
+// in the fixed camera-sorted order and accumulated into the warp's chunk.
 template <int MODE>
-__global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
+__global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smraw + kOffBars);
-  double* zbuf = reinterpret_cast<double*>(smraw + kOffZ);
-  int* lstart = reinterpret_cast<int*>(smraw + kOffL);
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kTermWarps + wid;
+  if (gw >= a.n_work) return;
   if (a.check_stop && a.st->stopped) return;
-  const int2 wr = a.work[blockIdx.x];
+  uint8_t* wsm = smraw + wid * kWarpSmem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wsm + kWOffBars);
+  double* gbuf = reinterpret_cast<double*>(wsm + kWOffG);
+  uint8_t* pbuf = wsm + kWOffP;
+  const int4 wr = a.work[gw];
   const int nq = wr.y - wr.x;
-  if (nq <= 0) return;
-  if (tid == 0) {
+  double* acc = a.partials + (int64_t)wr.z * 9;  // this warp's chunk accumulators
+  for (int k = lane; k < wr.w * 9; k += 32) acc[k] = 0.0;
+  if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  __syncwarp();
 
-  // producer (thread 0): descriptor of the tile to copy comes one issue ahead
-  auto issue = [&](int q, int4 d) {  // d = (n, lm0, nlm, nseg) of tile wr.x + q
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int q, int4 d) {  // lane 0; d = (n, lm0, nlm, nseg) of tile wr.x + q
     const int ti = wr.x + q;
-    uint8_t* stg = smraw + (q % kStages) * kStageBytes;
+    uint8_t* stg = wsm + (q % kStages) * kStageBytes;
     uint64_t* bar = &bars[q % kStages];
     const uint32_t vbytes = (MODE != kModeW) ? (uint32_t)(d.z * 48) : 0u;
-    fence_proxy_async();
-    mbar_expect_tx(bar, (uint32_t)(kJPlanes * d.x * 16 + 2 * kTile + 4 * kTile + 32) + vbytes);
-    const int64_t s0 = (int64_t)ti * kTile;
-    const uint64_t pol = policy_evict_first();
-#pragma unroll 1
-    for (int p = 0; p < kJPlanes; ++p)
-      bulk_g2s_stream(stg + p * kTile * 16, a.J + p * a.ns + s0, (uint32_t)(d.x * 16), bar, pol);
-    bulk_g2s(stg + kStPerm, a.perm_s + s0, kTile, bar);
-    bulk_g2s(stg + kStLidx, a.lidx_s + s0, kTile, bar);
-    bulk_g2s(stg + kStSegStart, a.seg_start + s0, 2 * kTile, bar);
-    bulk_g2s(stg + kStSegSlot, a.seg_slot + s0, 2 * kTile, bar);
+    mbar_expect_tx(bar, (uint32_t)(d.x * kRowBytes + 32) + vbytes);
+    bulk_g2s_stream(stg, a.J + (int64_t)ti * kTile * kRow, (uint32_t)(d.x * kRowBytes), bar, pol);
     bulk_g2s(stg + kStDesc, a.tk + ti, 32, bar);
     if (vbytes) bulk_g2s(stg + kStVinv, a.Vinv + (int64_t)d.y * 6, vbytes, bar);
   };
-  int4 dnext = make_int4(0, 0, 0, 0);  // descriptor of the next tile to issue (thread 0)
-  if (tid == 0) {
+  int4 dnext = make_int4(0, 0, 0, 0);
+  if (lane == 0) {
     for (int q = 0; q < kStages && q < nq; ++q) issue(q, *reinterpret_cast<const int4*>(a.tk + wr.x + q));
     if (kStages < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + kStages);
   }
-
-  // camera-vector gathers run one tile ahead (issued once the current tile's
-  // vector is consumed), camera indices two tiles ahead; padding slots carry
-  // camera 0, so these loads need no descriptor
-  double tc[9];
+  // camera-vector gathers one tile ahead, camera indices two tiles ahead (padding
+  // slots carry camera 0, so neither needs the tile descriptor)
+  double tc[9], tn[9];
   int cn = 0;
   if (MODE == kModeTerm) {
-    const double* tv = a.tin + (int64_t)a.cam_s[(int64_t)wr.x * kTile + tid] * 9;
+    const double* tv = a.tin + (int64_t)a.cam_s[(int64_t)wr.x * kTile + lane] * 9;
 #pragma unroll
     for (int j = 0; j < 9; ++j) tc[j] = tv[j];
-    if (nq > 1) cn = a.cam_s[(int64_t)(wr.x + 1) * kTile + tid];
+    if (nq > 1) cn = a.cam_s[(int64_t)(wr.x + 1) * kTile + lane];
   }
-
+#ifdef POBA_PHASE_TIMING
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+#define PHASE(k) do { const long long tnow_ = clock64(); ph[k] += (unsigned long long)(tnow_ - tprev); tprev = tnow_; } while (0)
+#else
+#define PHASE(k) do { } while (0)
+#endif
   for (int q = 0; q < nq; ++q) {
-    const int ti = wr.x + q;
-    uint8_t* stg = smraw + (q % kStages) * kStageBytes;
-    mbar_wait(&bars[q % kStages], (uint32_t)((q / kStages) & 1));
-    const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
-    const bool valid = tid < t.n;
-    const bool is_long = t.flags & kTileLong;
-    double* acc = a.partials + (int64_t)t.part0 * 9;  // this chunk's slots, owned by this CTA
-    if (t.flags & kTileChunkFirst)
-      for (int k = tid; k < t.nslot * 9; k += kTile) acc[k] = 0.0;
-    double2* pl = reinterpret_cast<double2*>(stg);
-    // phase 1: operands out of the stage; w_o = J_l^T (J_p t_c) into the plane-9 area
-    double2 jr[kJPlanes];
-    int li = 0;
-    if (valid) {
+    if (MODE == kModeTerm) {
+      if (q + 1 < nq) {
+        const double* tv = a.tin + (int64_t)cn * 9;
 #pragma unroll
-      for (int p = 0; p < kJPlanes; ++p) jr[p] = pl[p * kTile + tid];
-      li = stg[kStLidx + tid];
-      if (!is_long && (tid == 0 || stg[kStLidx + tid - 1] != li)) lstart[li] = tid;
+        for (int j = 0; j < 9; ++j) tn[j] = tv[j];
+      }
+      if (q + 2 < nq) cn = a.cam_s[(int64_t)(wr.x + q + 2) * kTile + lane];
     }
-    if (tid == 0) lstart[t.nlm] = t.n;
-    __syncthreads();  // A: planes are in registers; the plane area is scratch from here on
-    double* wbuf = reinterpret_cast<double*>(stg + 9 * kTile * 16);  // 3 doubles per observation
-    double* gbuf = reinterpret_cast<double*>(stg);                     // 9 doubles per observation
+    const uint8_t* stg = wsm + (q % kStages) * kStageBytes;
+    mbar_wait(&bars[q % kStages], (uint32_t)((q / kStages) & 1));
+    PHASE(0);
+    const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
+    const bool valid = lane < t.n;
+    const bool is_long = t.flags & kTileLong;
+    const double2* row = reinterpret_cast<const double2*>(stg) + lane * kRow;
+    RowMeta m = {0, 0, 0, 0};
+    if (valid) m = *reinterpret_cast<const RowMeta*>(row + 12);
+    const int li = (m.packed >> 8) & 0xff;
+    // accumulator loads of this lane's camera segment, in flight during phases 1-3
+    const bool seg = lane < t.nseg;
+    double old[9];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) old[c] = seg ? acc[m.seg_slot * 9 + c] : 0.0;
+    double2 jr[kJPlanes];
+#pragma unroll
+    for (int p = 0; p < kJPlanes; ++p) jr[p] = valid ? row[p] : make_double2(0.0, 0.0);
+    if (valid) pbuf[lane] = (uint8_t)(m.packed & 0xff);
+    // landmark runs: heads, my run's last lane
+    const int lim = is_long ? 0 : li;
+    const int prev_li = __shfl_up_sync(0xffffffffu, lim, 1);
+    const bool head = valid && (lane == 0 || prev_li != lim);
+    const unsigned heads = __ballot_sync(0xffffffffu, head) | (1u << min(t.n, 31)) * (t.n < 32);
+    const unsigned above = heads & ~((2u << lane) - 1u);  // heads strictly after me
+    const int last = (above ? __ffs(above) - 1 : t.n) - 1;
+    const int first = 31 - __clz(heads & ((2u << lane) - 1u));
+    // phase 1: w_o = J_l^T (J_p t_c), then the landmark sums y_l by a segmented scan
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
     if (MODE == kModeTerm && valid && !is_long) {
       double u0 = 0.0, u1 = 0.0;
 #pragma unroll
@@ -330,99 +340,103 @@ __global__ void __launch_bounds__(kTile, 2) k_term(const TermArgs a) {
         u0 = fma(jr[j].x, tc[j], u0);
         u1 = fma(jr[j].y, tc[j], u1);
       }
-#pragma unroll
-      for (int b = 0; b < 3; ++b) wbuf[tid * 3 + b] = fma(jr[9 + b].x, u0, jr[9 + b].y * u1);
+      w0 = fma(jr[9].x, u0, jr[9].y * u1);
+      w1 = fma(jr[10].x, u0, jr[10].y * u1);
+      w2 = fma(jr[11].x, u0, jr[11].y * u1);
     }
     if (MODE == kModeTerm) {
-      if (q + 1 < nq) {  // tc is consumed: start the next tile's gather
-        const double* tv = a.tin + (int64_t)cn * 9;
 #pragma unroll
-        for (int j = 0; j < 9; ++j) tc[j] = tv[j];
-      }
-      if (q + 2 < nq) cn = a.cam_s[(int64_t)(ti + 2) * kTile + tid];
-      __syncthreads();  // A2
-    }
-    // phase 2: per landmark z_l, four lanes per landmark (lane c sums y_c)
-    {
-      const int lmi = tid >> 2, c = tid & 3;
-      double yc = 0.0;
-      const bool act = lmi < t.nlm;
-      const int lm = t.lm0 + lmi;
-      if (act && c < 3) {
-        if (MODE == kModeW) {
-          yc = a.lvec[lm * 3 + c];
-        } else if (MODE == kModeTerm && is_long) {
-          yc = a.zlong[lm * 3 + c];
-        } else if (MODE == kModeBt) {
-          yc = a.lvec[lm * 3 + c];
-        } else {
-          for (int r = lstart[lmi]; r < lstart[lmi + 1]; ++r) yc += wbuf[r * 3 + c];
+      for (int d = 1; d < 32; d <<= 1) {
+        const double o0 = __shfl_up_sync(0xffffffffu, w0, d);
+        const double o1 = __shfl_up_sync(0xffffffffu, w1, d);
+        const double o2 = __shfl_up_sync(0xffffffffu, w2, d);
+        if (lane - d >= first) {
+          w0 += o0;
+          w1 += o1;
+          w2 += o2;
         }
       }
-      const int base = (tid & 31) & ~3;
-      const double y0 = __shfl_sync(0xffffffffu, yc, base);
-      const double y1 = __shfl_sync(0xffffffffu, yc, base + 1);
-      const double y2 = __shfl_sync(0xffffffffu, yc, base + 2);
-      if (act && c < 3) {
-        double z;
-        if (MODE == kModeW || (MODE == kModeTerm && is_long)) {
-          z = yc;  // already z
+    }
+    PHASE(1);
+    // phase 2: z_l = V_l^-1 y_l on each landmark's last lane, broadcast to the run
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0;
+    if (valid && lane == last) {
+      const int lm = t.lm0 + li;
+      if (MODE == kModeW) {
+        z0 = a.lvec[lm * 3]; z1 = a.lvec[lm * 3 + 1]; z2 = a.lvec[lm * 3 + 2];
+      } else if (MODE == kModeTerm && is_long) {
+        z0 = a.zlong[lm * 3]; z1 = a.zlong[lm * 3 + 1]; z2 = a.zlong[lm * 3 + 2];
+      } else {
+        double y[3], z[3];
+        if (MODE == kModeBt) {
+          y[0] = a.lvec[lm * 3]; y[1] = a.lvec[lm * 3 + 1]; y[2] = a.lvec[lm * 3 + 2];
         } else {
-          const double* V = reinterpret_cast<const double*>(stg + kStVinv) + lmi * 6;
-          const int r0 = c == 0 ? 0 : (c == 1 ? 1 : 2), r1 = c == 0 ? 1 : (c == 1 ? 3 : 4),
-                    r2 = c == 0 ? 2 : (c == 1 ? 4 : 5);
-          z = V[r0] * y0 + V[r1] * y1 + V[r2] * y2;
+          y[0] = w0; y[1] = w1; y[2] = w2;
         }
-        zbuf[lmi * 3 + c] = z;
+        sym3_mv(reinterpret_cast<const double*>(stg + kStVinv) + (is_long ? 0 : li) * 6, y, z);
+        z0 = z[0]; z1 = z[1]; z2 = z[2];
       }
     }
-    __syncthreads();  // B
-    // phase 3: g_o = J_p^T (J_l z_l) into the plane-0..8 area
+    const int src = valid ? last : lane;
+    z0 = __shfl_sync(0xffffffffu, z0, src);
+    z1 = __shfl_sync(0xffffffffu, z1, src);
+    z2 = __shfl_sync(0xffffffffu, z2, src);
+    const int nseg = t.nseg, tn_ = t.n;
+    const int sstart = (m.packed >> 16) & 0xff;
+    const int snext = __shfl_down_sync(0xffffffffu, sstart, 1);
+    const int send = (lane + 1 < nseg) ? snext : tn_;
+    __syncwarp();  // every lane is done with the stage
+    PHASE(2);
+    // the stage is consumed: refill it two tiles ahead
+    if (lane == 0 && q + kStages < nq) {
+      issue(q + kStages, dnext);
+      if (q + kStages + 1 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + q + kStages + 1);
+    }
+    PHASE(3);
+    // phase 3: g_o = J_p^T (J_l z_l)
     if (valid) {
-      const double z0 = zbuf[li * 3], z1 = zbuf[li * 3 + 1], z2 = zbuf[li * 3 + 2];
       const double v0 = fma(jr[9].x, z0, fma(jr[10].x, z1, jr[11].x * z2));
       const double v1 = fma(jr[9].y, z0, fma(jr[10].y, z1, jr[11].y * z2));
+      double2* gr = reinterpret_cast<double2*>(gbuf + lane * 10);
 #pragma unroll
-      for (int p = 0; p < 9; ++p) gbuf[tid * 9 + p] = fma(jr[p].x, v0, jr[p].y * v1);
+      for (int p = 0; p < 4; ++p)
+        gr[p] = make_double2(fma(jr[2 * p].x, v0, jr[2 * p].y * v1), fma(jr[2 * p + 1].x, v0, jr[2 * p + 1].y * v1));
+      gr[4] = make_double2(fma(jr[8].x, v0, jr[8].y * v1), 0.0);
     }
-    __syncthreads();  // C
-    // phase 4: camera segments -> slot accumulators (fixed order), loads batched
-    {
-      const uint16_t* ss = reinterpret_cast<const uint16_t*>(stg + kStSegStart);
-      const uint16_t* sl = reinterpret_cast<const uint16_t*>(stg + kStSegSlot);
-      const uint8_t* pm = stg + kStPerm;
-      const int items = t.nseg * 9;
-      int dst[9];
-      double old[9];
+    __syncwarp();
+    PHASE(4);
+    // phase 4: lane s sums camera segment s in fixed order into its chunk slot
+    if (seg) {
+      double sum[10];
 #pragma unroll
-      for (int u = 0; u < 9; ++u) {
-        const int k = tid + u * kTile;
-        dst[u] = -1;
-        if (k < items) {
-          const int sg = k / 9;
-          dst[u] = sl[sg] * 9 + (k - sg * 9);
+      for (int c = 0; c < 10; ++c) sum[c] = 0.0;
+      for (int r = sstart; r < send; ++r) {
+        const double2* gr = reinterpret_cast<const double2*>(gbuf + pbuf[r] * 10);
+#pragma unroll
+        for (int p = 0; p < 5; ++p) {
+          const double2 v = gr[p];
+          sum[2 * p] += v.x;
+          sum[2 * p + 1] += v.y;
         }
       }
+      double* dst = acc + m.seg_slot * 9;
 #pragma unroll
-      for (int u = 0; u < 9; ++u) old[u] = dst[u] >= 0 ? acc[dst[u]] : 0.0;
+      for (int c = 0; c < 9; ++c) dst[c] = old[c] + sum[c];
+    }
+    __syncwarp();
+    if (MODE == kModeTerm) {
 #pragma unroll
-      for (int u = 0; u < 9; ++u) {
-        const int k = tid + u * kTile;
-        if (k < items) {
-          const int sg = k / 9, comp = k - sg * 9;
-          const int r0 = ss[sg], r1 = (sg + 1 < t.nseg) ? ss[sg + 1] : t.n;
-          double sum = 0.0;
-          for (int r = r0; r < r1; ++r) sum += gbuf[pm[r] * 9 + comp];
-          acc[dst[u]] = old[u] + sum;
-        }
-      }
+      for (int j = 0; j < 9; ++j) tc[j] = tn[j];
     }
-    __syncthreads();  // D: stage free, accumulator updates visible to the next tile
-    if (tid == 0 && q + kStages < nq) {
-      issue(q + kStages, dnext);
-      if (q + kStages + 1 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + ti + kStages + 1);
-    }
+    PHASE(5);
   }
+#ifdef POBA_PHASE_TIMING
+  if (lane == 0 && a.dbg) {
+    for (int k = 0; k < 6; ++k) atomicAdd(&a.dbg[k], ph[k]);
+    atomicAdd(&a.dbg[7], (unsigned long long)nq);
+  }
+#endif
+#undef PHASE
 }
 
 // ---------------------------------------------------------------------------
@@ -602,38 +616,45 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
 // ---------------------------------------------------------------------------
 
 template <int OUT>
-__global__ void __launch_bounds__(kTile)
-k_wt_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const uint8_t* __restrict__ lidx_s,
-          const double2* __restrict__ J, int64_t ns, const double* __restrict__ tin, const double* __restrict__ bl,
-          const double* __restrict__ Vinv, double* __restrict__ out, int* __restrict__ nonzero_flag) {
-  __shared__ double wbuf[kTile * 3];
-  __shared__ int lstart[kTile + 1];
-  const Tile t = tiles[blockIdx.x];
+__global__ void __launch_bounds__(kBlockTiles * kTile)
+k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
+          const uint8_t* __restrict__ lidx_s, const double2* __restrict__ J, const double* __restrict__ tin,
+          const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
+          int* __restrict__ nonzero_flag) {
+  __shared__ double wbuf_all[kBlockTiles][kTile * 3];
+  __shared__ int lstart_all[kBlockTiles][kTile + 1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ti = blockIdx.x * kBlockTiles + w;
+  if (ti >= n_tiles) return;
+  const Tile t = tiles[ti];
   if (t.flags & kTileLong) return;  // handled by k_wt_long
-  const int64_t s0 = (int64_t)blockIdx.x * kTile;
-  const int tid = threadIdx.x;
-  tile_landmark_starts(lidx_s + s0, t.n, t.nlm, lstart);
-  if (tid < t.n) {
-    const int64_t o = s0 + tid;
+  double* wbuf = wbuf_all[w];
+  int* lstart = lstart_all[w];
+  const int64_t o = (int64_t)ti * kTile + lane;
+  if (lane < t.n) {
     const double* tv = tin + (int64_t)cam_s[o] * 9;
+    const double2* row = J + o * kRow;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = J[j * ns + o];
+      const double2 v = row[j];
       u0 = fma(v.x, tv[j], u0);
       u1 = fma(v.y, tv[j], u1);
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const double2 v = J[(9 + b) * ns + o];
-      wbuf[tid * 3 + b] = fma(v.x, u0, v.y * u1);
+      const double2 v = row[9 + b];
+      wbuf[lane * 3 + b] = fma(v.x, u0, v.y * u1);
     }
+    const int li = lidx_s[o];
+    if (lane == 0 || lidx_s[o - 1] != li) lstart[li] = lane;
   }
-  __syncthreads();
-  if (tid < t.nlm) {
-    const int lm = t.lm0 + tid;
+  if (lane == 0) lstart[t.nlm] = t.n;
+  __syncwarp();
+  if (lane < t.nlm) {
+    const int lm = t.lm0 + lane;
     double y[3] = {0.0, 0.0, 0.0}, z[3];
-    for (int r = lstart[tid]; r < lstart[tid + 1]; ++r) {
+    for (int r = lstart[lane]; r < lstart[lane + 1]; ++r) {
       y[0] += wbuf[r * 3];
       y[1] += wbuf[r * 3 + 1];
       y[2] += wbuf[r * 3 + 2];
@@ -654,28 +675,31 @@ k_wt_tile(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, const u
   }
 }
 
+constexpr int kLongThreads = 256;
+
 template <int OUT>
-__global__ void __launch_bounds__(kTile)
+__global__ void __launch_bounds__(kLongThreads)
 k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, const int* __restrict__ lm_k,
           const int* __restrict__ cam_s, const double2* __restrict__ J, int64_t ns, const double* __restrict__ tin,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag, const SeriesState* __restrict__ st, int check_stop) {
-  __shared__ double red[kTile][3];
+  __shared__ double red[kLongThreads][3];
   if (check_stop && st->stopped) return;
   const int lm = long_lm[blockIdx.x];
   const int o0 = lm_slot0[lm], o1 = o0 + lm_k[lm];
   const int tid = threadIdx.x;
   double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-  for (int o = o0 + tid; o < o1; o += kTile) {
+  for (int o = o0 + tid; o < o1; o += kLongThreads) {
     const double* tv = tin + (int64_t)cam_s[o] * 9;
+    const double2* row = J + (int64_t)o * kRow;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = J[j * ns + o];
+      const double2 v = row[j];
       u0 = fma(v.x, tv[j], u0);
       u1 = fma(v.y, tv[j], u1);
     }
-    const double2 a = J[9 * ns + o], b = J[10 * ns + o], c = J[11 * ns + o];
+    const double2 a = row[9], b = row[10], c = row[11];
     y0 += fma(a.x, u0, a.y * u1);
     y1 += fma(b.x, u0, b.y * u1);
     y2 += fma(c.x, u0, c.y * u1);
@@ -684,7 +708,7 @@ k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, con
   red[tid][1] = y1;
   red[tid][2] = y2;
   __syncthreads();
-  for (int s = kTile / 2; s; s >>= 1) {
+  for (int s = kLongThreads / 2; s; s >>= 1) {
     if (tid < s)
       for (int k = 0; k < 3; ++k) red[tid][k] += red[tid + s][k];
     __syncthreads();
@@ -749,58 +773,27 @@ size_t term_smem(const Ctx& c) {
 }
 
 int configure_term(Ctx& c) {
+  (void)c;
   static thread_local int done_dev = -1;
   int dev = 0;
   PCK(cudaGetDevice(&dev));
   if (done_dev != dev) {
-    const int lim = (int)kTermSmem;
-    PCK(cudaFuncSetAttribute(k_term<kModeTerm>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-    PCK(cudaFuncSetAttribute(k_term<kModeBt>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
-    PCK(cudaFuncSetAttribute(k_term<kModeW>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+    PCK(cudaFuncSetAttribute(k_term<kModeTerm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeBt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
     done_dev = dev;
-  }
-  if (c.work_occ == 0) {
-    // one CTA per SM (or more if the accumulators are small): group whole chunks
-    // into contiguous tile ranges of about equal observation count
-    int occ = 0;
-    PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_term<kModeTerm>, kTile, term_smem(c)));
-    occ = std::max(occ, 1);
-    const int n_work = std::max(1, std::min(c.n_chunks, c.n_sm * occ));
-    std::vector<int64_t> cobs(c.n_chunks + 1, 0);
-    for (int q = 0; q < c.n_chunks; ++q) {
-      int64_t o = 0;
-      for (int t = c.chunks_host[q].tile0; t < c.chunks_host[q].tile1; ++t) o += c.tile_n_host[t];
-      cobs[q + 1] = cobs[q] + o;
-    }
-    std::vector<int2> wr;
-    int prev = 0;
-    for (int w = 1; w <= n_work && prev < c.n_chunks; ++w) {
-      const int64_t want = cobs[c.n_chunks] * w / n_work;
-      int e = (int)(std::lower_bound(cobs.begin(), cobs.end(), want) - cobs.begin());
-      e = std::min(std::max(e, prev + 1), c.n_chunks);
-      if (w == n_work) e = c.n_chunks;
-      wr.push_back(make_int2(c.chunks_host[prev].tile0, c.chunks_host[e - 1].tile1));
-      prev = e;
-    }
-    PTRY(c.work.alloc(wr.size() * sizeof(int2)));
-    PCK(cudaMemcpy(c.work.p, wr.data(), wr.size() * sizeof(int2), cudaMemcpyHostToDevice));
-    c.n_work = (int)wr.size();
-    c.work_occ = occ;
   }
   return POBA_OK;
 }
 
 TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_stop) {
   TermArgs a;
+  a.dbg = c.dbg.as<unsigned long long>();
   a.tk = c.tilek.as<TileK>();
-  a.work = c.work.as<int2>();
   a.cam_s = c.cam_s.as<int>();
-  a.perm_s = c.perm_s.as<uint8_t>();
-  a.lidx_s = c.lidx_s.as<uint8_t>();
-  a.seg_start = c.seg_start.as<uint16_t>();
-  a.seg_slot = c.seg_slot.as<uint16_t>();
+  a.work = c.work.as<int4>();
+  a.n_work = c.n_work;
   a.J = c.J.as<double2>();
-  a.ns = c.n_slots;
   a.tin = tin;
   a.lvec = lvec;
   a.Vinv = c.Vinv.as<double>();
@@ -837,19 +830,20 @@ int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool ch
   PTRY(configure_term(c));
   const TermArgs a = term_args(c, tin, lvec, check_stop);
   const size_t smem = term_smem(c);
+  const unsigned grid = grid_for(c.n_work, kTermWarps);
   if (mode == kModeTerm) {
     if (c.n_long) {
-      k_wt_long<kOutZ><<<c.n_long, kTile, 0, c.stream>>>(
+      k_wt_long<kOutZ><<<c.n_long, kLongThreads, 0, c.stream>>>(
           c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.as<double2>(),
           c.n_slots, tin, nullptr, c.Vinv.as<double>(), c.ltmp.as<double>(), nullptr, c.state.as<SeriesState>(),
           check_stop ? 1 : 0);
       c.launches++;
     }
-    k_term<kModeTerm><<<c.n_work, kTile, smem, c.stream>>>(a);
+    k_term<kModeTerm><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   } else if (mode == kModeBt) {
-    k_term<kModeBt><<<c.n_work, kTile, smem, c.stream>>>(a);
+    k_term<kModeBt><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   } else {
-    k_term<kModeW><<<c.n_work, kTile, smem, c.stream>>>(a);
+    k_term<kModeW><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   }
   c.launches++;
   PCK(cudaGetLastError());
@@ -1014,12 +1008,12 @@ int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero) {
   cudaStream_t s = c.stream;
   int* fl = c.flag.as<int>() + 1;
   PCK(cudaMemsetAsync(fl, 0, 4, s));
-  k_wt_tile<kOutBack><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(),
-                                                  c.J.as<double2>(), c.n_slots, d_dp, c.bl.as<double>(),
-                                                  c.Vinv.as<double>(), c.dl.as<double>(), fl);
+  k_wt_tile<kOutBack><<<grid_for(c.n_tiles, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
+      c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_dp,
+      c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl);
   c.launches++;
   if (c.n_long) {
-    k_wt_long<kOutBack><<<c.n_long, kTile, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
+    k_wt_long<kOutBack><<<c.n_long, kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
                                                    c.cam_s.as<int>(), c.J.as<double2>(), c.n_slots, d_dp,
                                                    c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl,
                                                    c.state.as<SeriesState>(), 0);
@@ -1052,12 +1046,12 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
       PCK(cudaMemcpyAsync(d_out, c.rvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, s));
       break;
     case POBA_OP_WT:
-      k_wt_tile<kOutWt><<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(),
-                                                    c.J.as<double2>(), c.n_slots, d_in, nullptr, nullptr, d_out,
-                                                    nullptr);
+      k_wt_tile<kOutWt><<<grid_for(c.n_tiles, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
+          c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_in, nullptr,
+          nullptr, d_out, nullptr);
       c.launches++;
       if (c.n_long) {
-        k_wt_long<kOutWt><<<c.n_long, kTile, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
+        k_wt_long<kOutWt><<<c.n_long, kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
                                                      c.cam_s.as<int>(), c.J.as<double2>(), c.n_slots, d_in, nullptr,
                                                      nullptr, d_out, nullptr, c.state.as<SeriesState>(), 0);
         c.launches++;

@@ -183,7 +183,7 @@ __device__ __forceinline__ int lower_bound_u64(const uint64_t* __restrict__ a, i
 __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restrict__ flag,
                            const int* __restrict__ segpos, Tile* __restrict__ tiles,
                            const Chunk* __restrict__ chunks, const uint64_t* __restrict__ ukey, int bc,
-                           uint8_t* __restrict__ perm_s, uint16_t* __restrict__ seg_start,
+                           uint8_t* __restrict__ perm_s, uint8_t* __restrict__ seg_start,
                            uint16_t* __restrict__ seg_slot) {
   const int ti = blockIdx.x;
   const Tile t = tiles[ti];
@@ -198,7 +198,7 @@ __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restri
       const uint64_t target = ((uint64_t)t.chunk << bc) | (uint64_t)cam;
       const int u = lower_bound_u64(ukey, ch.part0, ch.part0 + ch.nslot, target);
       const int64_t sl = s0 + (segpos[q] - segpos[t.obs0]);  // segment index within the tile
-      seg_start[sl] = (uint16_t)r;
+      seg_start[sl] = (uint8_t)r;
       seg_slot[sl] = (uint16_t)(u - ch.part0);
     }
   }
@@ -208,6 +208,22 @@ __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restri
     tiles[ti].seg0 = s_first;
     tiles[ti].nseg = s_end - s_first;
   }
+}
+
+// metadata column (row entry 12) of every slot
+__global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
+                            const uint8_t* __restrict__ perm_s, const uint8_t* __restrict__ lidx_s,
+                            const uint8_t* __restrict__ seg_start, const uint16_t* __restrict__ seg_slot,
+                            double2* __restrict__ J) {
+  const Tile t = tiles[blockIdx.x];
+  const int i = threadIdx.x;
+  const int64_t s = (int64_t)blockIdx.x * kTile + i;
+  RowMeta m;
+  m.cam = cam_s[s];
+  m.packed = (int)perm_s[s] | ((int)lidx_s[s] << 8) | ((int)seg_start[s] << 16);
+  m.seg_slot = i < t.nseg ? (int)seg_slot[s] : 0;
+  m.pad = 0;
+  *reinterpret_cast<RowMeta*>(J + s * kRow + 12) = m;
 }
 
 __global__ void k_cam_slot_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
@@ -409,7 +425,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
         }
         continue;
       }
-      if (open && (cur.n + k > kTile || cur.nlm >= kMaxLmPerTile)) close();
+      if (open && (cur.n + k > kTile || cur.nlm >= kTileLm)) close();
       if (!open) {
         cur = Tile{};
         cur.obs0 = (int)lm_first[j];
@@ -523,7 +539,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   // --- chunks + camera slots -------------------------------------------------------------------------
   std::vector<Chunk> chunks;
   {
-    const int target = std::max(1, std::min(c.n_tiles, 2 * c.n_sm));
+    const int target = std::max(1, std::min(c.n_tiles, kTermWarps * c.n_sm));
     std::vector<int64_t> cum(c.n_tiles + 1, 0);
     for (int i = 0; i < c.n_tiles; ++i) cum[i + 1] = cum[i] + tiles[i].n;
     int prev = 0;
@@ -550,7 +566,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PCK(cudaMemcpyAsync(c.tiles.p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice, s));
     const int bchunk = std::max(1, bitlen((uint64_t)chunks.size()));
     if (bchunk + bc > 63) return fail(POBA_EINVAL, "chunk key exceeds 64 bits");
-    k_chunk_cam_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
+    k_chunk_cam_keys<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
     PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     k_unique_flags<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, fl.as<int>());
     PCK(cudaMemsetAsync(fl.as<int>() + nl, 0, 4, s));
@@ -594,9 +610,14 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PTRY(c.chunks.alloc(chunks.size() * sizeof(Chunk)));
   PCK(cudaMemcpyAsync(c.chunks.p, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice, s));
   c.chunks_host = chunks;
-  c.tile_n_host.resize(c.n_tiles);
-  for (int i = 0; i < c.n_tiles; ++i) c.tile_n_host[i] = tiles[i].n;
-  c.work_occ = 0;  // work ranges planned at first launch
+  {  // one chunk per warp of the term kernel
+    std::vector<int4> wr(chunks.size());
+    for (size_t q = 0; q < chunks.size(); ++q)
+      wr[q] = make_int4(chunks[q].tile0, chunks[q].tile1, chunks[q].part0, chunks[q].nslot);
+    PTRY(c.work.alloc(wr.size() * sizeof(int4)));
+    PCK(cudaMemcpyAsync(c.work.p, wr.data(), wr.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+    c.n_work = (int)wr.size();
+  }
 
   // camera -> partials (chunk order)
   {
@@ -622,7 +643,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   {
     const int bt = std::max(1, bitlen((uint64_t)c.n_tiles));
     if (bt + bc + 8 > 63) return fail(POBA_EINVAL, "tile key exceeds 64 bits");
-    k_tile_cam_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
+    k_tile_cam_keys<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
     PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     k_seg_flags<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, fl.as<int>());
     PCK(cudaMemsetAsync(fl.as<int>() + nl, 0, 4, s));
@@ -632,13 +653,13 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PCK(cudaMemcpyAsync(&nseg, pos.as<int>() + nl, 4, cudaMemcpyDeviceToHost, s));
     PCK(cudaStreamSynchronize(s));
     c.n_segs = nseg;
-    PTRY(c.seg_start.alloc(ns * 2));
+    PTRY(c.seg_start.alloc(ns));
     PTRY(c.seg_slot.alloc(ns * 2));
-    PCK(cudaMemsetAsync(c.seg_start.p, 0, ns * 2, s));
+    PCK(cudaMemsetAsync(c.seg_start.p, 0, ns, s));
     PCK(cudaMemsetAsync(c.seg_slot.p, 0, ns * 2, s));
-    k_segments<<<c.n_tiles, B, 0, s>>>(kb.as<uint64_t>(), fl.as<int>(), pos.as<int>(), c.tiles.as<Tile>(),
+    k_segments<<<c.n_tiles, kTile, 0, s>>>(kb.as<uint64_t>(), fl.as<int>(), pos.as<int>(), c.tiles.as<Tile>(),
                                        c.chunks.as<Chunk>(), ukey.as<uint64_t>(), bc, c.perm_s.as<uint8_t>(),
-                                       c.seg_start.as<uint16_t>(), c.seg_slot.as<uint16_t>());
+                                       c.seg_start.as<uint8_t>(), c.seg_slot.as<uint16_t>());
     c.launches++;
   }
 
@@ -665,7 +686,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
 
   // camera-major permutation of slots for the U0 / b_p reduction
   {
-    k_cam_slot_keys<<<c.n_tiles, B, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), ka.as<uint64_t>());
+    k_cam_slot_keys<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), ka.as<uint64_t>());
     PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     PTRY(c.cperm.alloc(nl * 4));
     k_low32<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, c.cperm.as<int>());
@@ -687,11 +708,15 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     c.n_cchunks = ncc;
   }
 
-  // --- work buffers --------------------------------------------------------------------------------------
-  PTRY(c.J.alloc((size_t)kJPlanes * ns * 16));
+  // --- store rows (J + metadata) and work buffers ------------------------------------------------------------
+  PTRY(c.J.alloc((size_t)kRow * ns * 16));
   PTRY(c.Rz.alloc((size_t)ns * 16));
-  PCK(cudaMemsetAsync(c.J.p, 0, (size_t)kJPlanes * ns * 16, s));
+  PCK(cudaMemsetAsync(c.J.p, 0, (size_t)kRow * ns * 16, s));
   PCK(cudaMemsetAsync(c.Rz.p, 0, (size_t)ns * 16, s));
+  k_pack_meta<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.perm_s.as<uint8_t>(),
+                                          c.lidx_s.as<uint8_t>(), c.seg_start.as<uint8_t>(),
+                                          c.seg_slot.as<uint16_t>(), c.J.as<double2>());
+  c.launches++;
   const int64_t nc = n_cam, nlm1 = std::max<int64_t>(nlm, 1);
   for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.bt, &c.tvec, &c.xvec, &c.rvec, &c.ctmp, &c.ctmp2})
     PTRY(b->alloc(nc * 9 * 8));
