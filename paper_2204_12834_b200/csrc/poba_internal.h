@@ -31,15 +31,17 @@ constexpr int kSlotCap = 65535;   // uint16 camera-slot ids per chunk
 constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
 constexpr int kJPlanes = 12;      // Jacobian column pairs per row
 constexpr int kStages = 2;        // bulk-copy pipeline depth per warp of the term kernel
-constexpr int kTermWarps = 10;    // independent warps per CTA of the term kernel
+constexpr int kTermWarps = 8;     // independent warps per CTA of the term kernel
 
 // metadata word (row entry 12, as int4)
 struct RowMeta {
   int cam;
-  int packed;  // perm (bits 0-7) | landmark index in tile (8-15) | segment start (16-23)
-  int seg_slot;
-  int pad;
+  int packed;    // perm (bits 0-7) | landmark index in tile (8-15) | start of segment <lane> (16-23)
+                 // | this observation's segment (24-31)
+  int seg_slot;  // chunk slot of segment <lane>
+  int seg_cam;   // camera of segment <lane>
 };
+constexpr int kTStride = 10;      // doubles per camera record of the term vector / partials (80 B, 16-B aligned)
 
 // Error plumbing ---------------------------------------------------------------
 void set_error(const std::string& msg);
@@ -181,6 +183,8 @@ struct Ctx {
   DBuf lm_k;         // int32 [n_lm_l]
   DBuf seg_start;    // uint8 [n_slots] per tile: start position of segment s at tile*kTile + s
   DBuf seg_slot;     // uint16 [n_slots] per tile: chunk slot of segment s
+  DBuf seg_obs;      // uint8 [n_slots] segment of each observation
+  DBuf seg_cam;      // int32 [n_slots] per tile: camera of segment s
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
   DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
@@ -207,11 +211,11 @@ struct Ctx {
   DBuf Uinv;         // double [n_cam*45]
   DBuf Ud;           // double [n_cam*45] damped U
   DBuf bt;           // double [n_cam*9] b_tilde
-  DBuf tvec;         // double [n_cam*9] current term
+  DBuf tvec;         // double [n_cam*kTStride] current term (80-B records)
   DBuf xvec;         // double [n_cam*9] partial sum
   DBuf rvec;         // double [n_cam*9] reduced camera vector (pre U^-1)
   DBuf cc_part;      // double [n_cchunks*54]
-  DBuf partials;     // double [n_partials*9]
+  DBuf partials;     // double [n_partials*kTStride]
   DBuf blk_part;     // double [blocks*4] per-block reduction partials
   DBuf state;        // SeriesState
   DBuf state_aux;    // SeriesState for side computations (b_tilde read-back)
@@ -227,8 +231,8 @@ struct Ctx {
   DBuf Vd;           // double [n_lm_l*6] damped V
   DBuf dl;           // double [n_lm_l*3] last delta_l
   DBuf ltmp;         // double [n_lm_l*3] scratch / z of long landmarks
-  DBuf ctmp;         // double [n_cam*9] scratch
-  DBuf ctmp2;        // double [n_cam*9]
+  DBuf ctmp;         // double [n_cam*kTStride] scratch
+  DBuf ctmp2;        // double [n_cam*kTStride]
   DBuf flag;         // int [16]
   DBuf dbg;          // instrumentation counters (POBA_PHASE_TIMING builds)
   DBuf red;          // double scratch for reductions

@@ -206,7 +206,7 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 struct TermArgs {
   unsigned long long* dbg;  // POBA_PHASE_TIMING: per-phase cycle totals (8 entries)
   const TileK* tk;         // per warp-tile kernel descriptors
-  const int* cam_s;        // camera of each slot (prefetch of the camera-vector gather)
+  const int* seg_cam;      // camera of segment s of each tile (slot space)
   const int4* work;        // per warp: (tile0, tile1, part0, nslot) -- one chunk
   int n_work;
   const double2* J;        // slot rows
@@ -220,27 +220,32 @@ struct TermArgs {
 };
 
 // Per-warp shared memory (bytes): kStages stages of one warp-tile (32 rows of
-// 208 B, the 32-B descriptor and the V^-1 slice of its landmarks), plus
-// scratch for w, z, g and the segment/permutation tables.
+// 208 B, the 32-B descriptor and the V^-1 slice of its landmarks); the camera
+// records of the tile's distinct cameras (double-buffered, filled one tile
+// ahead), per-observation g rows, per-segment sums and the permutation.
 constexpr int kStDesc = kTile * kRowBytes;                 // 6656
 constexpr int kStVinv = kStDesc + 32;                      // 6688
 constexpr int kStageBytes = (kStVinv + kTileLm * 48 + 127) / 128 * 128;
+constexpr int kRecBytes = kTStride * 8;                    // 80-B camera record
 constexpr int kWOffBars = kStages * kStageBytes;
-constexpr int kWOffG = kWOffBars + 16 * kStages;           // g: 32 x 10 doubles (16-B aligned rows)
-constexpr int kWOffW = kWOffG + kTile * 10 * 8;
-constexpr int kWOffZ = kWOffW + kTile * 3 * 8;
-constexpr int kWOffL = kWOffZ + kTileLm * 3 * 8;           // landmark starts (33 ints)
-constexpr int kWOffP = kWOffL + (kTile + 4) * 4;           // permutation (32 B) + segment starts (36 B)
-constexpr int kWarpSmem = (kWOffP + 2 * kTile + 8 + 127) / 128 * 128;
+constexpr int kWOffT = kWOffBars + 16 * kStages;           // 2 x 32 camera records
+constexpr int kWOffG = kWOffT + 2 * kTile * kRecBytes;      // g rows (32 x 80 B)
+constexpr int kWOffS = kWOffG + kTile * kRecBytes;          // segment sums (32 x 80 B)
+constexpr int kWOffP = kWOffS + kTile * kRecBytes;          // permutation (32 B)
+constexpr int kWarpSmem = (kWOffP + kTile + 127) / 128 * 128;
 constexpr int kTermSmem = kTermWarps * kWarpSmem;
+constexpr int kPieces = kTile * (kRecBytes / 16) / 32;      // 16-B pieces per lane to cover 32 records = 5
 static_assert(kTermSmem <= 227 * 1024, "term kernel shared memory over budget");
 
 // One warp streams one chunk of warp-tiles through its own bulk-copy pipeline;
-// warps never wait on each other (no block-wide barrier in the loop).  Within a
-// warp-tile the landmark sums are a segmented warp scan (landmarks are runs of
-// consecutive lanes), V^-1 is applied by each landmark's last lane and z is
-// broadcast back by shuffle; camera segments are summed through shared memory
-// in the fixed camera-sorted order and accumulated into the warp's chunk.
+// warps never wait on each other.  Everything indexed by camera is moved per
+// DISTINCT camera of the tile (its camera segments), five lanes per 80-byte
+// record with 16-byte accesses: the camera vector t_c is gathered one tile
+// ahead into a shared table, the chunk accumulators are read and written the
+// same way.  Within a tile the landmark sums are a segmented warp scan
+// (landmarks are runs of consecutive lanes); V^-1 is applied on each run's last
+// lane and z broadcast back by shuffle; camera segments are summed in the fixed
+// camera-sorted order.
 template <int MODE>
 __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
@@ -250,17 +255,18 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   if (a.check_stop && a.st->stopped) return;
   uint8_t* wsm = smraw + wid * kWarpSmem;
   uint64_t* bars = reinterpret_cast<uint64_t*>(wsm + kWOffBars);
-  double* gbuf = reinterpret_cast<double*>(wsm + kWOffG);
+  double2* ttab = reinterpret_cast<double2*>(wsm + kWOffT);   // [2][32 records][5]
+  double2* gtab = reinterpret_cast<double2*>(wsm + kWOffG);   // [32 obs][5]
+  double2* stab = reinterpret_cast<double2*>(wsm + kWOffS);   // [32 segments][5]
   uint8_t* pbuf = wsm + kWOffP;
   const int4 wr = a.work[gw];
   const int nq = wr.y - wr.x;
-  double* acc = a.partials + (int64_t)wr.z * 9;  // this warp's chunk accumulators
-  for (int k = lane; k < wr.w * 9; k += 32) acc[k] = 0.0;
+  double* acc = a.partials + (int64_t)wr.z * kTStride;  // this warp's chunk accumulators
+  for (int k = lane; k < wr.w * kTStride; k += 32) acc[k] = 0.0;
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
-  __syncwarp();
 
   const uint64_t pol = policy_evict_first();
   auto issue = [&](int q, int4 d) {  // lane 0; d = (n, lm0, nlm, nseg) of tile wr.x + q
@@ -278,16 +284,23 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     for (int q = 0; q < kStages && q < nq; ++q) issue(q, *reinterpret_cast<const int4*>(a.tk + wr.x + q));
     if (kStages < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + kStages);
   }
-  // camera-vector gathers one tile ahead, camera indices two tiles ahead (padding
-  // slots carry camera 0, so neither needs the tile descriptor)
-  double tc[9], tn[9];
-  int cn = 0;
+  // camera records of the next tile's segments (gathered one tile ahead; segment
+  // cameras two tiles ahead; padding segments name camera 0)
+  const int rec = lane / 5;  // piece r of lane covers record (32 r + lane) / 5
+  double2 tp[kPieces];
+  int sc_next = 0;
   if (MODE == kModeTerm) {
-    const double* tv = a.tin + (int64_t)a.cam_s[(int64_t)wr.x * kTile + lane] * 9;
+    const int sc0 = a.seg_cam[(int64_t)wr.x * kTile + lane];
 #pragma unroll
-    for (int j = 0; j < 9; ++j) tc[j] = tv[j];
-    if (nq > 1) cn = a.cam_s[(int64_t)(wr.x + 1) * kTile + lane];
+    for (int r = 0; r < kPieces; ++r) {
+      const int k = 32 * r + lane;
+      const int c = __shfl_sync(0xffffffffu, sc0, k / 5);
+      ttab[k] = reinterpret_cast<const double2*>(a.tin + (int64_t)c * kTStride)[k % 5];
+    }
+    if (nq > 1) sc_next = a.seg_cam[(int64_t)(wr.x + 1) * kTile + lane];
   }
+  (void)rec;
+  __syncwarp();
 #ifdef POBA_PHASE_TIMING
   unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
@@ -296,13 +309,15 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
 #define PHASE(k) do { } while (0)
 #endif
   for (int q = 0; q < nq; ++q) {
-    if (MODE == kModeTerm) {
-      if (q + 1 < nq) {
-        const double* tv = a.tin + (int64_t)cn * 9;
+    const double2* tcur = ttab + (q & 1) * (kTile * 5);
+    if (MODE == kModeTerm && q + 1 < nq) {
 #pragma unroll
-        for (int j = 0; j < 9; ++j) tn[j] = tv[j];
+      for (int r = 0; r < kPieces; ++r) {
+        const int k = 32 * r + lane;
+        const int c = __shfl_sync(0xffffffffu, sc_next, k / 5);
+        tp[r] = reinterpret_cast<const double2*>(a.tin + (int64_t)c * kTStride)[k % 5];
       }
-      if (q + 2 < nq) cn = a.cam_s[(int64_t)(wr.x + q + 2) * kTile + lane];
+      sc_next = (q + 2 < nq) ? a.seg_cam[(int64_t)(wr.x + q + 2) * kTile + lane] : 0;
     }
     const uint8_t* stg = wsm + (q % kStages) * kStageBytes;
     mbar_wait(&bars[q % kStages], (uint32_t)((q / kStages) & 1));
@@ -314,26 +329,44 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     RowMeta m = {0, 0, 0, 0};
     if (valid) m = *reinterpret_cast<const RowMeta*>(row + 12);
     const int li = (m.packed >> 8) & 0xff;
-    // accumulator loads of this lane's camera segment, in flight during phases 1-3
-    const bool seg = lane < t.nseg;
-    double old[9];
+    const int my_seg = (m.packed >> 24) & 0xff;
+    const int nseg = t.nseg;
+    // chunk-accumulator pieces of this tile's segments (read before this tile's
+    // writes, after the previous tile's), 16 B per lane per round
+    double2 oldp[kPieces];
+    int slotp[kPieces];
 #pragma unroll
-    for (int c = 0; c < 9; ++c) old[c] = seg ? acc[m.seg_slot * 9 + c] : 0.0;
+    for (int r = 0; r < kPieces; ++r) {
+      const int k = 32 * r + lane;
+      const int sg = k / 5;
+      const int sl = __shfl_sync(0xffffffffu, m.seg_slot, sg & 31);
+      slotp[r] = (sg < nseg) ? sl : -1;
+      oldp[r] = (sg < nseg) ? reinterpret_cast<const double2*>(acc + (int64_t)sl * kTStride)[k % 5]
+                            : make_double2(0.0, 0.0);
+    }
     double2 jr[kJPlanes];
 #pragma unroll
     for (int p = 0; p < kJPlanes; ++p) jr[p] = valid ? row[p] : make_double2(0.0, 0.0);
     if (valid) pbuf[lane] = (uint8_t)(m.packed & 0xff);
-    // landmark runs: heads, my run's last lane
+    // landmark runs: heads, my run's first and last lane
     const int lim = is_long ? 0 : li;
     const int prev_li = __shfl_up_sync(0xffffffffu, lim, 1);
     const bool head = valid && (lane == 0 || prev_li != lim);
-    const unsigned heads = __ballot_sync(0xffffffffu, head) | (1u << min(t.n, 31)) * (t.n < 32);
-    const unsigned above = heads & ~((2u << lane) - 1u);  // heads strictly after me
+    const unsigned heads = __ballot_sync(0xffffffffu, head) | (t.n < 32 ? (1u << t.n) : 0u);
+    const unsigned above = heads & ~((2u << lane) - 1u);
     const int last = (above ? __ffs(above) - 1 : t.n) - 1;
     const int first = 31 - __clz(heads & ((2u << lane) - 1u));
     // phase 1: w_o = J_l^T (J_p t_c), then the landmark sums y_l by a segmented scan
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;
     if (MODE == kModeTerm && valid && !is_long) {
+      const double2* tr = tcur + my_seg * 5;
+      double tc[10];
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        const double2 v = tr[p];
+        tc[2 * p] = v.x;
+        tc[2 * p + 1] = v.y;
+      }
       double u0 = 0.0, u1 = 0.0;
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
@@ -381,23 +414,22 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     z0 = __shfl_sync(0xffffffffu, z0, src);
     z1 = __shfl_sync(0xffffffffu, z1, src);
     z2 = __shfl_sync(0xffffffffu, z2, src);
-    const int nseg = t.nseg, tn_ = t.n;
     const int sstart = (m.packed >> 16) & 0xff;
     const int snext = __shfl_down_sync(0xffffffffu, sstart, 1);
-    const int send = (lane + 1 < nseg) ? snext : tn_;
+    const int send = (lane + 1 < nseg) ? snext : t.n;
+    const int tn_ = t.n;
     __syncwarp();  // every lane is done with the stage
     PHASE(2);
-    // the stage is consumed: refill it two tiles ahead
-    if (lane == 0 && q + kStages < nq) {
+    if (lane == 0 && q + kStages < nq) {  // refill the stage two tiles ahead
       issue(q + kStages, dnext);
       if (q + kStages + 1 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + q + kStages + 1);
     }
     PHASE(3);
-    // phase 3: g_o = J_p^T (J_l z_l)
+    // phase 3: g_o = J_p^T (J_l z_l) into this lane's g row
     if (valid) {
       const double v0 = fma(jr[9].x, z0, fma(jr[10].x, z1, jr[11].x * z2));
       const double v1 = fma(jr[9].y, z0, fma(jr[10].y, z1, jr[11].y * z2));
-      double2* gr = reinterpret_cast<double2*>(gbuf + lane * 10);
+      double2* gr = gtab + lane * 5;
 #pragma unroll
       for (int p = 0; p < 4; ++p)
         gr[p] = make_double2(fma(jr[2 * p].x, v0, jr[2 * p].y * v1), fma(jr[2 * p + 1].x, v0, jr[2 * p + 1].y * v1));
@@ -405,29 +437,41 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     }
     __syncwarp();
     PHASE(4);
-    // phase 4: lane s sums camera segment s in fixed order into its chunk slot
-    if (seg) {
-      double sum[10];
+    // phase 4: lane s sums camera segment s in fixed (camera-sorted) order
+    if (lane < nseg) {
+      double2 sum[5];
 #pragma unroll
-      for (int c = 0; c < 10; ++c) sum[c] = 0.0;
+      for (int p = 0; p < 5; ++p) sum[p] = make_double2(0.0, 0.0);
       for (int r = sstart; r < send; ++r) {
-        const double2* gr = reinterpret_cast<const double2*>(gbuf + pbuf[r] * 10);
+        const double2* gr = gtab + pbuf[r] * 5;
 #pragma unroll
         for (int p = 0; p < 5; ++p) {
           const double2 v = gr[p];
-          sum[2 * p] += v.x;
-          sum[2 * p + 1] += v.y;
+          sum[p].x += v.x;
+          sum[p].y += v.y;
         }
       }
-      double* dst = acc + m.seg_slot * 9;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) dst[c] = old[c] + sum[c];
+      for (int p = 0; p < 5; ++p) stab[lane * 5 + p] = sum[p];
+    }
+    (void)tn_;
+    __syncwarp();
+    // ... and the chunk accumulators are updated 16 B per lane
+#pragma unroll
+    for (int r = 0; r < kPieces; ++r) {
+      const int k = 32 * r + lane;
+      if (slotp[r] >= 0) {
+        const double2 v = stab[k];
+        reinterpret_cast<double2*>(acc + (int64_t)slotp[r] * kTStride)[k % 5] =
+            make_double2(oldp[r].x + v.x, oldp[r].y + v.y);
+      }
+    }
+    if (MODE == kModeTerm && q + 1 < nq) {
+      double2* tnext = ttab + ((q + 1) & 1) * (kTile * 5);
+#pragma unroll
+      for (int r = 0; r < kPieces; ++r) tnext[32 * r + lane] = tp[r];
     }
     __syncwarp();
-    if (MODE == kModeTerm) {
-#pragma unroll
-      for (int j = 0; j < 9; ++j) tc[j] = tn[j];
-    }
     PHASE(5);
   }
 #ifdef POBA_PHASE_TIMING
@@ -477,7 +521,7 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
     if (kFromPartials) {
       const int p0 = a.part_cam_off[cam], p1 = a.part_cam_off[cam + 1];
       for (int p = p0 + lane; p < p1; p += 32) {
-        const double* src = a.partials + (int64_t)a.part_idx[p] * 9;
+        const double* src = a.partials + (int64_t)a.part_idx[p] * kTStride;
 #pragma unroll
         for (int j = 0; j < 9; ++j) r[j] += src[j];
       }
@@ -513,7 +557,7 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
       double t = 0.0;
 #pragma unroll
       for (int j = 0; j < 9; ++j) t = fma(U[sym9(i, j)], v[j], t);
-      a.tvec[q] = t;
+      a.tvec[(int64_t)cam * kTStride + i] = t;
       if (MODE == kCamBt) {
         a.xvec[q] = t;
         xx = t * t;
@@ -618,7 +662,7 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
 template <int OUT>
 __global__ void __launch_bounds__(kBlockTiles * kTile)
 k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
-          const uint8_t* __restrict__ lidx_s, const double2* __restrict__ J, const double* __restrict__ tin,
+          const uint8_t* __restrict__ lidx_s, const double2* __restrict__ J, const double* __restrict__ tin, int ts,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag) {
   __shared__ double wbuf_all[kBlockTiles][kTile * 3];
@@ -632,7 +676,7 @@ k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ c
   int* lstart = lstart_all[w];
   const int64_t o = (int64_t)ti * kTile + lane;
   if (lane < t.n) {
-    const double* tv = tin + (int64_t)cam_s[o] * 9;
+    const double* tv = tin + (int64_t)cam_s[o] * ts;
     const double2* row = J + o * kRow;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
@@ -680,7 +724,7 @@ constexpr int kLongThreads = 256;
 template <int OUT>
 __global__ void __launch_bounds__(kLongThreads)
 k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, const int* __restrict__ lm_k,
-          const int* __restrict__ cam_s, const double2* __restrict__ J, int64_t ns, const double* __restrict__ tin,
+          const int* __restrict__ cam_s, const double2* __restrict__ J, int ts, const double* __restrict__ tin,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag, const SeriesState* __restrict__ st, int check_stop) {
   __shared__ double red[kLongThreads][3];
@@ -690,7 +734,7 @@ k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, con
   const int tid = threadIdx.x;
   double y0 = 0.0, y1 = 0.0, y2 = 0.0;
   for (int o = o0 + tid; o < o1; o += kLongThreads) {
-    const double* tv = tin + (int64_t)cam_s[o] * 9;
+    const double* tv = tin + (int64_t)cam_s[o] * ts;
     const double2* row = J + (int64_t)o * kRow;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
@@ -734,7 +778,7 @@ k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, con
 
 // elementwise block-diagonal products
 __global__ void k_cam_mv(const double* __restrict__ M45, const double* __restrict__ v, int64_t n_cam,
-                         double* __restrict__ out) {
+                         double* __restrict__ out, int os = 9) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= n_cam * 9) return;
   const int64_t c = q / 9;
@@ -742,7 +786,14 @@ __global__ void k_cam_mv(const double* __restrict__ M45, const double* __restric
   double s = 0.0;
 #pragma unroll
   for (int j = 0; j < 9; ++j) s = fma(M45[c * 45 + sym9(i, j)], v[c * 9 + j], s);
-  out[q] = s;
+  out[c * os + i] = s;
+}
+
+__global__ void k_restride(const double* __restrict__ in, int is, int64_t n_cam, double* __restrict__ out, int os) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_cam * 9) return;
+  const int64_t c = q / 9;
+  out[c * os + (q - c * 9)] = in[c * is + (q - c * 9)];
 }
 
 __global__ void k_lm_mv(const double* __restrict__ M6, const double* __restrict__ v, int64_t n_lm,
@@ -790,7 +841,7 @@ TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_sto
   TermArgs a;
   a.dbg = c.dbg.as<unsigned long long>();
   a.tk = c.tilek.as<TileK>();
-  a.cam_s = c.cam_s.as<int>();
+  a.seg_cam = c.seg_cam.as<int>();
   a.work = c.work.as<int4>();
   a.n_work = c.n_work;
   a.J = c.J.as<double2>();
@@ -835,7 +886,7 @@ int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool ch
     if (c.n_long) {
       k_wt_long<kOutZ><<<c.n_long, kLongThreads, 0, c.stream>>>(
           c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.as<double2>(),
-          c.n_slots, tin, nullptr, c.Vinv.as<double>(), c.ltmp.as<double>(), nullptr, c.state.as<SeriesState>(),
+          kTStride, tin, nullptr, c.Vinv.as<double>(), c.ltmp.as<double>(), nullptr, c.state.as<SeriesState>(),
           check_stop ? 1 : 0);
       c.launches++;
     }
@@ -990,8 +1041,10 @@ int points_accept_device(Ctx& c) {
 int series_apply_device(Ctx& c, const double* d_v, int order, double* d_out) {
   // apply_series_inverse (power_series.py:80-91): x = sum_{i<=order} P^i U^-1 v
   cudaStream_t s = c.stream;
-  k_cam_mv<<<grid_for(c.n_cam * 9, 256), 256, 0, s>>>(c.Uinv.as<double>(), d_v, c.n_cam, c.tvec.as<double>());
-  PCK(cudaMemcpyAsync(c.xvec.p, c.tvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, s));
+  k_cam_mv<<<grid_for(c.n_cam * 9, 256), 256, 0, s>>>(c.Uinv.as<double>(), d_v, c.n_cam, c.tvec.as<double>(),
+                                                     kTStride);
+  k_restride<<<grid_for(c.n_cam * 9, 256), 256, 0, s>>>(c.tvec.as<double>(), kTStride, c.n_cam, c.xvec.as<double>(), 9);
+  c.launches++;
   PCK(cudaMemsetAsync(c.state.p, 0, sizeof(SeriesState), s));
   c.launches++;
   for (int i = 1; i <= order; ++i) {
@@ -1009,12 +1062,12 @@ int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero) {
   int* fl = c.flag.as<int>() + 1;
   PCK(cudaMemsetAsync(fl, 0, 4, s));
   k_wt_tile<kOutBack><<<grid_for(c.n_tiles, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
-      c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_dp,
+      c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_dp, 9,
       c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl);
   c.launches++;
   if (c.n_long) {
     k_wt_long<kOutBack><<<c.n_long, kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
-                                                   c.cam_s.as<int>(), c.J.as<double2>(), c.n_slots, d_dp,
+                                                   c.cam_s.as<int>(), c.J.as<double2>(), 9, d_dp,
                                                    c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl,
                                                    c.state.as<SeriesState>(), 0);
     c.launches++;
@@ -1047,12 +1100,12 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
       break;
     case POBA_OP_WT:
       k_wt_tile<kOutWt><<<grid_for(c.n_tiles, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
-          c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_in, nullptr,
+          c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_in, 9, nullptr,
           nullptr, d_out, nullptr);
       c.launches++;
       if (c.n_long) {
         k_wt_long<kOutWt><<<c.n_long, kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
-                                                     c.cam_s.as<int>(), c.J.as<double2>(), c.n_slots, d_in, nullptr,
+                                                     c.cam_s.as<int>(), c.J.as<double2>(), 9, d_in, nullptr,
                                                      nullptr, d_out, nullptr, c.state.as<SeriesState>(), 0);
         c.launches++;
       }

@@ -184,7 +184,8 @@ __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restri
                            const int* __restrict__ segpos, Tile* __restrict__ tiles,
                            const Chunk* __restrict__ chunks, const uint64_t* __restrict__ ukey, int bc,
                            uint8_t* __restrict__ perm_s, uint8_t* __restrict__ seg_start,
-                           uint16_t* __restrict__ seg_slot) {
+                           uint16_t* __restrict__ seg_slot, uint8_t* __restrict__ seg_obs,
+                           int* __restrict__ seg_cam) {
   const int ti = blockIdx.x;
   const Tile t = tiles[ti];
   const Chunk ch = chunks[t.chunk];
@@ -193,6 +194,7 @@ __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restri
     const int64_t q = t.obs0 + r;
     const uint64_t k = key[q];
     perm_s[s0 + r] = (uint8_t)(k & 0xff);
+    seg_obs[s0 + (k & 0xff)] = (uint8_t)(segpos[q] + flag[q] - 1 - segpos[t.obs0]);
     if (flag[q]) {
       const int cam = (int)((k >> 8) & ((1ull << bc) - 1));
       const uint64_t target = ((uint64_t)t.chunk << bc) | (uint64_t)cam;
@@ -200,6 +202,7 @@ __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restri
       const int64_t sl = s0 + (segpos[q] - segpos[t.obs0]);  // segment index within the tile
       seg_start[sl] = (uint8_t)r;
       seg_slot[sl] = (uint16_t)(u - ch.part0);
+      seg_cam[sl] = cam;
     }
   }
   if (threadIdx.x == 0) {
@@ -214,15 +217,16 @@ __global__ void k_segments(const uint64_t* __restrict__ key, const int* __restri
 __global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
                             const uint8_t* __restrict__ perm_s, const uint8_t* __restrict__ lidx_s,
                             const uint8_t* __restrict__ seg_start, const uint16_t* __restrict__ seg_slot,
+                            const uint8_t* __restrict__ seg_obs, const int* __restrict__ seg_cam,
                             double2* __restrict__ J) {
   const Tile t = tiles[blockIdx.x];
   const int i = threadIdx.x;
   const int64_t s = (int64_t)blockIdx.x * kTile + i;
   RowMeta m;
   m.cam = cam_s[s];
-  m.packed = (int)perm_s[s] | ((int)lidx_s[s] << 8) | ((int)seg_start[s] << 16);
+  m.packed = (int)perm_s[s] | ((int)lidx_s[s] << 8) | ((int)seg_start[s] << 16) | ((int)seg_obs[s] << 24);
   m.seg_slot = i < t.nseg ? (int)seg_slot[s] : 0;
-  m.pad = 0;
+  m.seg_cam = i < t.nseg ? seg_cam[s] : 0;
   *reinterpret_cast<RowMeta*>(J + s * kRow + 12) = m;
 }
 
@@ -655,11 +659,16 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     c.n_segs = nseg;
     PTRY(c.seg_start.alloc(ns));
     PTRY(c.seg_slot.alloc(ns * 2));
+    PTRY(c.seg_obs.alloc(ns));
+    PTRY(c.seg_cam.alloc(ns * 4));
+    PCK(cudaMemsetAsync(c.seg_obs.p, 0, ns, s));
+    PCK(cudaMemsetAsync(c.seg_cam.p, 0, ns * 4, s));
     PCK(cudaMemsetAsync(c.seg_start.p, 0, ns, s));
     PCK(cudaMemsetAsync(c.seg_slot.p, 0, ns * 2, s));
     k_segments<<<c.n_tiles, kTile, 0, s>>>(kb.as<uint64_t>(), fl.as<int>(), pos.as<int>(), c.tiles.as<Tile>(),
                                        c.chunks.as<Chunk>(), ukey.as<uint64_t>(), bc, c.perm_s.as<uint8_t>(),
-                                       c.seg_start.as<uint8_t>(), c.seg_slot.as<uint16_t>());
+                                       c.seg_start.as<uint8_t>(), c.seg_slot.as<uint16_t>(),
+                                       c.seg_obs.as<uint8_t>(), c.seg_cam.as<int>());
     c.launches++;
   }
 
@@ -715,17 +724,19 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PCK(cudaMemsetAsync(c.Rz.p, 0, (size_t)ns * 16, s));
   k_pack_meta<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.perm_s.as<uint8_t>(),
                                           c.lidx_s.as<uint8_t>(), c.seg_start.as<uint8_t>(),
-                                          c.seg_slot.as<uint16_t>(), c.J.as<double2>());
+                                          c.seg_slot.as<uint16_t>(), c.seg_obs.as<uint8_t>(),
+                                          c.seg_cam.as<int>(), c.J.as<double2>());
   c.launches++;
   const int64_t nc = n_cam, nlm1 = std::max<int64_t>(nlm, 1);
-  for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.bt, &c.tvec, &c.xvec, &c.rvec, &c.ctmp, &c.ctmp2})
+  for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.bt, &c.xvec, &c.rvec})
     PTRY(b->alloc(nc * 9 * 8));
+  for (DBuf* b : {&c.tvec, &c.ctmp, &c.ctmp2}) PTRY(b->alloc(nc * kTStride * 8));
   for (DBuf* b : {&c.cams_prep, &c.trial_prep}) PTRY(b->alloc(nc * 16 * 8));
   for (DBuf* b : {&c.U0, &c.Uinv, &c.Ud}) PTRY(b->alloc(nc * 45 * 8));
   for (DBuf* b : {&c.points, &c.bl, &c.Dl, &c.dl, &c.ltmp}) PTRY(b->alloc(nlm1 * 3 * 8));
   for (DBuf* b : {&c.V0, &c.Vinv, &c.Vd}) PTRY(b->alloc(nlm1 * 6 * 8));
   PTRY(c.cc_part.alloc(std::max(c.n_cchunks, 1) * 54 * 8));
-  PTRY(c.partials.alloc(std::max(c.n_partials, 1) * 9 * 8));
+  PTRY(c.partials.alloc(std::max(c.n_partials, 1) * kTStride * 8));
   PTRY(c.state.alloc(sizeof(SeriesState)));
   PTRY(c.blk_part.alloc((grid_for(n_cam, 8) + 8) * 4 * 8));
   PTRY(c.flag.alloc(64));
