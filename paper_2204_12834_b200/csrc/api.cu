@@ -229,14 +229,14 @@ int poba_get_ordering(poba_ctx* ctx, int64_t* order, int64_t* cam_sorted, int64_
   PTRY(poba::build_canonical_order(c));
   const int64_t n = c.n_obs;
   std::vector<int> o(n), cf, pf;
-  PCK(cudaMemcpy(o.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
+  PTRY(poba::copy_sync(c, o.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
   if (cam_sorted) {
     cf.resize(n);
-    PCK(cudaMemcpy(cf.data(), c.cam_file.p, n * 4, cudaMemcpyDeviceToHost));
+    PTRY(poba::copy_sync(c, cf.data(), c.cam_file.p, n * 4, cudaMemcpyDeviceToHost));
   }
   if (pt_sorted) {
     pf.resize(n);
-    PCK(cudaMemcpy(pf.data(), c.pt_file.p, n * 4, cudaMemcpyDeviceToHost));
+    PTRY(poba::copy_sync(c, pf.data(), c.pt_file.p, n * 4, cudaMemcpyDeviceToHost));
   }
   for (int64_t i = 0; i < n; ++i) {
     if (order) order[i] = o[i];
@@ -345,7 +345,7 @@ int poba_series_apply(poba_ctx* ctx, const double* v, int order, double* out) {
   NEED(v && out, "null vectors");
   PCK(cudaMemcpyAsync(c.ctmp.p, v, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
   PTRY(poba::series_apply_device(c, c.ctmp.as<double>(), order, c.ctmp2.as<double>()));
-  PCK(cudaMemcpy(out, c.ctmp2.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToHost));
+  PTRY(poba::copy_sync(c, out, c.ctmp2.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToHost));
   return POBA_OK;
 }
 
@@ -483,10 +483,10 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
       const int64_t ns = c.n_slots, n = c.n_obs;
       std::vector<double> J((size_t)poba::kRow * ns * 2), R(ns * 2);
       std::vector<int> file(ns), order(n), slot_of_file(n, -1);
-      PCK(cudaMemcpy(J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
-      PCK(cudaMemcpy(R.data(), c.Rz.p, R.size() * 8, cudaMemcpyDeviceToHost));
-      PCK(cudaMemcpy(file.data(), c.file_s.p, ns * 4, cudaMemcpyDeviceToHost));
-      PCK(cudaMemcpy(order.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
+      PTRY(poba::copy_sync(c, J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
+      PTRY(poba::copy_sync(c, R.data(), c.Rz.p, R.size() * 8, cudaMemcpyDeviceToHost));
+      PTRY(poba::copy_sync(c, file.data(), c.file_s.p, ns * 4, cudaMemcpyDeviceToHost));
+      PTRY(poba::copy_sync(c, order.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
       for (int64_t q = 0; q < ns; ++q)
         if (file[q] >= 0) slot_of_file[file[q]] = (int)q;
       for (int64_t i = 0; i < n; ++i) {
@@ -521,9 +521,10 @@ int poba_debug_counters(poba_ctx* ctx, uint64_t* out) {
   Ctx& c = ctx->c;
   PTRY(c.dbg.alloc(64));
   if (out) {
-    PCK(cudaMemcpy(out, c.dbg.p, 64, cudaMemcpyDeviceToHost));
+    PTRY(poba::copy_sync(c, out, c.dbg.p, 64, cudaMemcpyDeviceToHost));
   }
-  PCK(cudaMemset(c.dbg.p, 0, 64));
+  PCK(cudaMemsetAsync(c.dbg.p, 0, 64, c.stream));
+  PCK(cudaStreamSynchronize(c.stream));
   return POBA_OK;
 }
 

@@ -264,6 +264,16 @@ int points_accept_device(Ctx& c);
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
+// Synchronous copies ON THE CONTEXT STREAM.  (Plain cudaMemcpy runs on the
+// legacy default stream, which does not order with the context's non-blocking
+// stream: a read-back could overtake the kernel producing the data.)
+inline int copy_sync(Ctx& c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, c.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) return fail(POBA_ECUDA, std::string("copy_sync: ") + cudaGetErrorString(e));
+  return POBA_OK;
+}
+
 // ---- device helpers shared by the tile kernels -----------------------------------
 #ifdef __CUDACC__
 // landmark starts inside a tile from the per-slot landmark index (lstart has nlm+1 entries)

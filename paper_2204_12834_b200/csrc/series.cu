@@ -327,7 +327,13 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     const bool is_long = t.flags & kTileLong;
     const double2* row = reinterpret_cast<const double2*>(stg) + lane * kRow;
     RowMeta m = {0, 0, 0, 0};
-    if (valid) m = *reinterpret_cast<const RowMeta*>(row + 12);
+    if (valid) {  // one 16-B shared load
+      const int4 mv = *reinterpret_cast<const int4*>(row + 12);
+      m.cam = mv.x;
+      m.packed = mv.y;
+      m.seg_slot = mv.z;
+      m.seg_cam = mv.w;
+    }
     const int li = (m.packed >> 8) & 0xff;
     const int my_seg = (m.packed >> 24) & 0xff;
     const int nseg = t.nseg;

@@ -312,6 +312,7 @@ int build_canonical_order(Ctx& c) {
                                              ka.as<uint64_t>(), va.as<int>());
     c.launches++;
     PTRY(sort_pairs(c, ka.as<uint64_t>(), kb.as<uint64_t>(), va.as<int>(), c.order.as<int>(), n, bk + bp + bc));
+    PCK(cudaStreamSynchronize(s));  // scoped temporaries are freed below
   }
   // k-groups from landmarks sorted by (k, pt)
   std::vector<uint64_t> lk(n_pt);
@@ -393,7 +394,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
 
   // --- tiles (host greedy packing of landmarks in index order) -------------------------
   std::vector<int> hk(n_pt);
-  PCK(cudaMemcpy(hk.data(), c.kpt.p, n_pt * 4, cudaMemcpyDeviceToHost));
+  PTRY(poba::copy_sync(c, hk.data(), c.kpt.p, n_pt * 4, cudaMemcpyDeviceToHost));
   std::vector<int64_t> lm_first(n_pt + 1);
   lm_first[0] = 0;
   for (int64_t j = 0; j < n_pt; ++j) lm_first[j + 1] = lm_first[j] + hk[j];
@@ -641,6 +642,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PCK(cudaMemcpyAsync(c.part_idx.p, v2.p, n_u * 4, cudaMemcpyDeviceToDevice, s));
     PTRY(c.part_cam_off.alloc((n_cam + 1) * 4));
     PTRY(excl_sum(c, cnt.as<int>(), c.part_cam_off.as<int>(), n_cam + 1));
+    PCK(cudaStreamSynchronize(s));  // scoped temporaries are freed below
   }
 
   // per-tile camera segments + tile-local permutation
@@ -675,7 +677,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   // compact kernel descriptors (chunk bounds folded into the flags)
   {
     std::vector<Tile> tt(c.n_tiles);
-    PCK(cudaMemcpy(tt.data(), c.tiles.p, c.n_tiles * sizeof(Tile), cudaMemcpyDeviceToHost));
+    PTRY(poba::copy_sync(c, tt.data(), c.tiles.p, c.n_tiles * sizeof(Tile), cudaMemcpyDeviceToHost));
     std::vector<TileK> tk(c.n_tiles);
     for (int i = 0; i < c.n_tiles; ++i) {
       const Chunk& ch = chunks[tt[i].chunk];
@@ -690,7 +692,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
       k.chunk = tt[i].chunk;
     }
     PTRY(c.tilek.alloc(c.n_tiles * sizeof(TileK)));
-    PCK(cudaMemcpy(c.tilek.p, tk.data(), c.n_tiles * sizeof(TileK), cudaMemcpyHostToDevice));
+    PTRY(poba::copy_sync(c, c.tilek.p, tk.data(), c.n_tiles * sizeof(TileK), cudaMemcpyHostToDevice));
   }
 
   // camera-major permutation of slots for the U0 / b_p reduction

@@ -140,7 +140,7 @@ def test_explicit_systems(P):
             q = f"{pre}sys_solve{i}_"
             eps = float(z[q + "eps"])
             r = P.power_series_solve(s, eps, int(z[q + "m"]))
-            if eps >= 1e-12:
+            if eps >= 1e-12 or not bool(z[q + "converged"]):
                 assert r.order_used == int(z[q + "order"]) and r.converged == bool(z[q + "converged"])
             else:
                 # epsilon at the fp64 noise floor: the stop ratio is rounding noise

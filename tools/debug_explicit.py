@@ -17,3 +17,12 @@ for j in range(4):
         g = P.power_series_solve(s, 1e-300, m).delta_p
         w, _, _ = O.series_solve(so, 1e-300, m)
         print("   m", m, rel(g, w))
+print("---- eps 1e-14 solves, repeated")
+for j in range(4):
+    pre = f"e{j}_"
+    args = (z[pre + "cam_idx"], z[pre + "pt_idx"], z[pre + "jp"], z[pre + "jl"], z[pre + "res"], int(z[pre + "n_cam"]), int(z[pre + "n_pt"]))
+    lin = P.assemble_from_observations(*args)
+    s = lin.damp(float(z[pre + "lam"]))
+    for rep in range(3):
+        r, ratios = P.power_series_solve(s, 1e-14, 200, return_ratios=True)
+        print(j, rep, r.order_used, r.converged, ratios[:4], "golden order", int(z[pre + "sys_solve0_order"]))
