@@ -238,6 +238,7 @@ struct Ctx {
   DBuf red;          // double scratch for reductions
   DBuf cub_tmp;      // CUB temp storage
 
+  bool l2_window_set = false;
   double lam = 0;
   int identity = 0;
   int64_t n_invalid = 0;

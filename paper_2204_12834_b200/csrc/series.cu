@@ -829,8 +829,32 @@ size_t term_smem(const Ctx& c) {
   return (size_t)kTermSmem;
 }
 
+// Keep the chunk accumulators resident in L2 while the Jacobians stream past
+// (persisting access-policy window on the context stream).
+int configure_l2(Ctx& c) {
+  if (c.l2_window_set) return POBA_OK;
+  c.l2_window_set = true;
+  cudaDeviceProp prop;
+  PCK(cudaGetDeviceProperties(&prop, c.device));
+  if (prop.persistingL2CacheMaxSize <= 0 || prop.accessPolicyMaxWindowSize <= 0) return POBA_OK;
+  const size_t want = (size_t)std::max(c.n_partials, 1) * kTStride * 8;
+  const size_t carve = std::min<size_t>(want, (size_t)prop.persistingL2CacheMaxSize);
+  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) {
+    cudaGetLastError();
+    return POBA_OK;
+  }
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.base_ptr = c.partials.p;
+  v.accessPolicyWindow.num_bytes = std::min<size_t>(want, (size_t)prop.accessPolicyMaxWindowSize);
+  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)carve / (float)v.accessPolicyWindow.num_bytes);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  if (cudaStreamSetAttribute(c.stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
+  return POBA_OK;
+}
+
 int configure_term(Ctx& c) {
-  (void)c;
+  if (getenv("POBA_NO_L2_WINDOW") == nullptr) PTRY(configure_l2(c));
   static thread_local int done_dev = -1;
   int dev = 0;
   PCK(cudaGetDevice(&dev));
