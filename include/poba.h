@@ -154,6 +154,9 @@ int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_ter
 int64_t poba_launch_count(poba_ctx* ctx);
 /* the cudaStream_t every kernel of this context runs on (for external events) */
 int poba_stream(poba_ctx* ctx, void** stream);
+/* landmark bounds [lm_bounds[r], lm_bounds[r+1]) of each rank's shard, as
+ * poba_create_sharded contexts choose them (host-only, callable without a GPU) */
+int poba_shard_bounds(int64_t n_pt, const int64_t* k_per_point, int nranks, int64_t* lm_bounds);
 /* instrumentation counters of POBA_PHASE_TIMING builds (8 x uint64, reset on read) */
 int poba_debug_counters(poba_ctx* ctx, uint64_t* out);
 

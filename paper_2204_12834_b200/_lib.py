@@ -55,6 +55,7 @@ _SIGS = {
     "poba_launch_count": (ctypes.c_int64, [_P]),
     "poba_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "poba_debug_counters": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+    "poba_shard_bounds": (ctypes.c_int, [ctypes.c_int64, _I64P, ctypes.c_int, _I64P]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -102,6 +103,14 @@ def _f64(a, shape=None):
     out = np.ascontiguousarray(a, dtype=np.float64)
     if shape is not None:
         out = out.reshape(shape)
+    return out
+
+
+def shard_bounds(k_per_point, nranks: int) -> np.ndarray:
+    """Landmark bounds of each rank's shard (host-only; same plan as sharded contexts)."""
+    k = np.ascontiguousarray(k_per_point, dtype=np.int64)
+    out = np.zeros(nranks + 1, dtype=np.int64)
+    _check(load().poba_shard_bounds(len(k), _i64(k), int(nranks), _i64(out)))
     return out
 
 

@@ -515,6 +515,24 @@ int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_ter
 
 int64_t poba_launch_count(poba_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+// landmark bounds of every rank's shard (host-only; no GPU needed)
+int poba_shard_bounds(int64_t n_pt, const int64_t* k_per_point, int nranks, int64_t* lm_bounds) {
+  if (n_pt <= 0 || !k_per_point || !lm_bounds || nranks < 1) return poba::fail(POBA_EINVAL, "bad arguments");
+  std::vector<int> k(n_pt);
+  for (int64_t j = 0; j < n_pt; ++j) {
+    if (k_per_point[j] < 1) return poba::fail(POBA_EINVAL, "every point must be observed at least once");
+    k[j] = (int)k_per_point[j];
+  }
+  poba::TilePlan plan;
+  poba::plan_tiles(k.data(), n_pt, plan);
+  const int64_t n_obs = plan.lm_first[n_pt];
+  for (int r = 0; r <= nranks; ++r) {
+    const size_t t = poba::shard_cut(plan, n_obs, r, nranks);
+    lm_bounds[r] = t < plan.tiles.size() ? plan.tiles[t].lm0 : n_pt;
+  }
+  return POBA_OK;
+}
+
 // instrumentation (POBA_PHASE_TIMING builds): read and reset 8 counters
 int poba_debug_counters(poba_ctx* ctx, uint64_t* out) {
   CTX_CHECK(ctx);

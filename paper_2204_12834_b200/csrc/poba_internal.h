@@ -247,6 +247,16 @@ struct Ctx {
   DBuf scratch_a, scratch_b, scratch_c;
 };
 
+// ---- host-only planning (no GPU needed) ------------------------------------------
+struct TilePlan {
+  std::vector<int64_t> lm_first;       // first observation of each landmark (store order)
+  std::vector<Tile> tiles;             // global warp-tiles
+  std::vector<char> cut_ok;            // may a shard boundary sit before this tile?
+  std::vector<int> lm_tile, lm_off_in_tile;
+};
+void plan_tiles(const int* k_per_point, int64_t n_pt, TilePlan& plan);
+size_t shard_cut(const TilePlan& plan, int64_t n_obs, int r, int nranks);
+
 // ---- host-side orchestration entry points ---------------------------------------
 int build_structure(Ctx& c, const int64_t* cam_idx, const int64_t* pt_idx, const double* pixels);
 int build_canonical_order(Ctx& c);

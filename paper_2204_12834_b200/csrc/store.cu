@@ -292,6 +292,73 @@ int excl_sum(Ctx& c, int* in, int* out, int64_t n) {
 
 }  // namespace
 
+// Host-only: greedy packing of landmarks (index order) into warp-tiles.
+void plan_tiles(const int* k_per_point, int64_t n_pt, TilePlan& plan) {
+  plan.lm_first.assign(n_pt + 1, 0);
+  for (int64_t j = 0; j < n_pt; ++j) plan.lm_first[j + 1] = plan.lm_first[j] + k_per_point[j];
+  plan.tiles.clear();
+  plan.cut_ok.clear();
+  plan.lm_tile.assign(n_pt, 0);
+  plan.lm_off_in_tile.assign(n_pt, 0);
+  plan.tiles.reserve(plan.lm_first[n_pt] / kTile * 11 / 10 + 16);
+  Tile cur{};
+  bool open = false;
+  auto close = [&]() {
+    if (open) {
+      plan.tiles.push_back(cur);
+      plan.cut_ok.push_back(1);
+      open = false;
+    }
+  };
+  for (int64_t j = 0; j < n_pt; ++j) {
+    const int k = k_per_point[j];
+    if (k > kTile) {
+      close();
+      plan.lm_tile[j] = (int)plan.tiles.size();
+      plan.lm_off_in_tile[j] = 0;
+      for (int sub = 0; sub < k; sub += kTile) {
+        Tile t{};
+        t.obs0 = (int)(plan.lm_first[j] + sub);
+        t.n = std::min(kTile, k - sub);
+        t.lm0 = (int)j;
+        t.nlm = 1;
+        t.flags = kTileLong;
+        plan.tiles.push_back(t);
+        plan.cut_ok.push_back(sub == 0);
+      }
+      continue;
+    }
+    if (open && (cur.n + k > kTile || cur.nlm >= kTileLm)) close();
+    if (!open) {
+      cur = Tile{};
+      cur.obs0 = (int)plan.lm_first[j];
+      cur.lm0 = (int)j;
+      open = true;
+    }
+    plan.lm_tile[j] = (int)plan.tiles.size();
+    plan.lm_off_in_tile[j] = cur.n;
+    cur.n += k;
+    cur.nlm += 1;
+  }
+  close();
+}
+
+// First tile of rank r's contiguous shard: balanced by observations, cut only
+// where a tile starts a new landmark (a long landmark never straddles ranks).
+size_t shard_cut(const TilePlan& plan, int64_t n_obs, int r, int nranks) {
+  const auto& gt = plan.tiles;
+  if (r <= 0) return 0;
+  if (r >= nranks) return gt.size();
+  const int64_t target = (n_obs * r) / nranks;
+  size_t lo = 0, hi = gt.size();
+  while (lo < hi) {
+    size_t mid = (lo + hi) / 2;
+    if (gt[mid].obs0 < target) lo = mid + 1; else hi = mid;
+  }
+  while (lo < gt.size() && !plan.cut_ok[lo]) ++lo;
+  return lo;
+}
+
 // Canonical (reference) order and k-groups, built on first export request.
 int build_canonical_order(Ctx& c) {
   if (c.have_order) return POBA_OK;
@@ -392,76 +459,19 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   const int bp = std::max(1, bitlen((uint64_t)(n_pt - 1)));
   if (bp + bc > 64) return fail(POBA_EINVAL, "store key exceeds 64 bits");
 
-  // --- tiles (host greedy packing of landmarks in index order) -------------------------
+  // --- tiles (host greedy packing of landmarks in index order) + this rank's shard -------
   std::vector<int> hk(n_pt);
   PTRY(poba::copy_sync(c, hk.data(), c.kpt.p, n_pt * 4, cudaMemcpyDeviceToHost));
-  std::vector<int64_t> lm_first(n_pt + 1);
-  lm_first[0] = 0;
-  for (int64_t j = 0; j < n_pt; ++j) lm_first[j + 1] = lm_first[j] + hk[j];
-  std::vector<Tile> gt;
-  std::vector<char> cut_ok;
-  std::vector<int> lm_tile(n_pt), lm_off_in_tile(n_pt);
-  gt.reserve(n / kTile * 11 / 10 + 16);
-  {
-    Tile cur{};
-    bool open = false;
-    auto close = [&]() {
-      if (open) {
-        gt.push_back(cur);
-        cut_ok.push_back(1);
-        open = false;
-      }
-    };
-    for (int64_t j = 0; j < n_pt; ++j) {
-      const int k = hk[j];
-      if (k > kTile) {
-        close();
-        lm_tile[j] = (int)gt.size();
-        lm_off_in_tile[j] = 0;
-        for (int sub = 0; sub < k; sub += kTile) {
-          Tile t{};
-          t.obs0 = (int)(lm_first[j] + sub);
-          t.n = std::min(kTile, k - sub);
-          t.lm0 = (int)j;
-          t.nlm = 1;
-          t.flags = kTileLong;
-          gt.push_back(t);
-          cut_ok.push_back(sub == 0);
-        }
-        continue;
-      }
-      if (open && (cur.n + k > kTile || cur.nlm >= kTileLm)) close();
-      if (!open) {
-        cur = Tile{};
-        cur.obs0 = (int)lm_first[j];
-        cur.lm0 = (int)j;
-        open = true;
-      }
-      lm_tile[j] = (int)gt.size();
-      lm_off_in_tile[j] = cur.n;
-      cur.n += k;
-      cur.nlm += 1;
-    }
-    close();
-  }
-
-  // --- shard: contiguous tile range balanced by observations ------------------------------
+  TilePlan plan;
+  plan_tiles(hk.data(), n_pt, plan);
+  std::vector<int64_t>& lm_first = plan.lm_first;
+  std::vector<Tile>& gt = plan.tiles;
+  std::vector<int>& lm_tile = plan.lm_tile;
+  std::vector<int>& lm_off_in_tile = plan.lm_off_in_tile;
   size_t t_lo = 0, t_hi = gt.size();
   if (c.nranks > 1) {
-    auto cut_at = [&](int r) -> size_t {
-      if (r <= 0) return 0;
-      if (r >= c.nranks) return gt.size();
-      const int64_t target = (n * r) / c.nranks;
-      size_t lo = 0, hi = gt.size();
-      while (lo < hi) {
-        size_t mid = (lo + hi) / 2;
-        if (gt[mid].obs0 < target) lo = mid + 1; else hi = mid;
-      }
-      while (lo < gt.size() && !cut_ok[lo]) ++lo;
-      return lo;
-    };
-    t_lo = cut_at(c.rank);
-    t_hi = cut_at(c.rank + 1);
+    t_lo = shard_cut(plan, n, c.rank, c.nranks);
+    t_hi = shard_cut(plan, n, c.rank + 1, c.nranks);
   }
   if (t_hi <= t_lo) return fail(POBA_EINVAL, "shard received no landmarks (too many ranks)");
   c.lm_lo = gt[t_lo].lm0;
