@@ -19,29 +19,42 @@ namespace poba {
 // landmarks; a landmark with k > kTile spans consecutive full sub-tiles.  Each
 // slot is one 208-byte row of 13 double2: the 2x9 pose Jacobian (9 column
 // pairs), the 2x3 point Jacobian (3 column pairs) and a 16-byte metadata word
-// (camera, tile-local camera permutation, landmark index, camera segment) --
+// (camera, chunk slot of the camera, landmark index in the tile) --
 // the reference's 2x13 block row with the residual column replaced by the
 // metadata (residuals live in their own array; the series never reads them).
 constexpr int kTile = 32;         // observation slots per warp-tile (one warp)
-constexpr int kTileLm = 32;       // landmarks per warp-tile (bounds the staged V^-1 slice)
+constexpr int kTileLm = 16;       // landmarks per warp-tile (bounds the staged V^-1 slice)
 constexpr int kRow = 13;          // double2 per slot row
 constexpr int kRowBytes = kRow * 16;
 constexpr int kBlockTiles = 8;    // warp-tiles per CTA in the streaming kernels (256 threads)
-constexpr int kSlotCap = 65535;   // uint16 camera-slot ids per chunk
 constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
 constexpr int kJPlanes = 12;      // Jacobian column pairs per row
-constexpr int kStages = 2;        // bulk-copy pipeline depth per warp of the term kernel
-constexpr int kTermWarps = 8;     // independent warps per CTA of the term kernel
+constexpr int kTermWarps = 8;     // warps per CTA of the term kernel (one CTA per SM)
+constexpr int kTStride = 10;      // doubles per camera record of the term vector / partials (80 B, 16-B aligned)
+// Term-kernel shared memory: per warp one bulk-copy stage (32 rows, the tile
+// descriptor, the V^-1 slice of its <= kTileLm landmarks) and the gathered
+// camera records of its tile; per CTA the chunk accumulator table (one 80-B
+// record per camera slot of the chunk) and the stage / turn barriers.
+constexpr int kStRows = kTile * kRowBytes;                       // 6656
+constexpr int kStDesc = kStRows;                                 // 32-B tile descriptor
+constexpr int kStVinv = kStDesc + 32;                            // V^-1 slice
+constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7456
+constexpr int kTRecBytes = kTStride * 8;                         // 80
+constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera records = 10016
+constexpr int kTermSmemMax = 227 * 1024;
+constexpr int kTermBars = 2 * kTermWarps * 8;                    // stage + turn barriers
+constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermBars) / kTRecBytes) / 32 * 32;
+constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermBars + kAccSlots * kTRecBytes;
+static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
+static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 
 // metadata word (row entry 12, as int4)
 struct RowMeta {
   int cam;
-  int packed;    // perm (bits 0-7) | landmark index in tile (8-15) | start of segment <lane> (16-23)
-                 // | this observation's segment (24-31)
-  int seg_slot;  // chunk slot of segment <lane>
-  int seg_cam;   // camera of segment <lane>
+  int slot;      // slot of the camera in the chunk accumulator table
+  int li;        // landmark index within the tile (0 for a long landmark's sub-tile)
+  int pad;
 };
-constexpr int kTStride = 10;      // doubles per camera record of the term vector / partials (80 B, 16-B aligned)
 
 // Error plumbing ---------------------------------------------------------------
 void set_error(const std::string& msg);
@@ -123,21 +136,20 @@ struct Tile {
   int n;       // observations in tile
   int lm0;     // first local landmark
   int nlm;     // landmarks in tile (1 for a sub-tile of a long landmark)
-  int seg0;    // first camera segment of the tile
-  int nseg;    // number of camera segments
   int chunk;   // owning chunk
-  int flags;   // bit0: sub-tile of a landmark with k > kTile
+  int flags;   // kTileLong | kTileDupCam | kTileChunkLast
 };
-constexpr int kTileLong = 1;
-constexpr int kTileChunkFirst = 2;
-constexpr int kTileChunkLast = 4;
+constexpr int kTileLong = 1;      // sub-tile of a landmark with k > kTile
+constexpr int kTileDupCam = 2;    // some camera appears twice in the tile
+constexpr int kTileChunkLast = 4; // last tile of its chunk: flush the accumulator table after it
 
 // Compact per-tile descriptor streamed into the term kernel's stage (32 B).
 struct TileK {
-  int n, lm0, nlm, nseg;
-  int flags, part0, nslot, chunk;
+  int n, lm0, nlm, flags;
+  int chunk, part0, nslot, pad;
 };
 
+// A chunk: contiguous tiles of one CTA whose distinct cameras fit kAccSlots.
 struct Chunk {
   int tile0, tile1;  // tile range
   int part0;         // first partial (slot 0)
@@ -169,22 +181,17 @@ struct Ctx {
   // local shard: points [lm_lo, lm_hi), its observations, tiles
   int64_t lm_lo = 0, lm_hi = 0, n_lm_l = 0, n_obs_l = 0;
   int64_t n_slots = 0;  // n_tiles * kTile
-  int n_tiles = 0, n_chunks = 0, n_partials = 0, max_slots = 0, n_long = 0, n_segs = 0, n_work = 0;
+  int n_tiles = 0, n_chunks = 0, n_partials = 0, max_slots = 0, n_long = 0, n_cta = 0;
   DBuf tiles;        // Tile [n_tiles]
   DBuf tilek;        // TileK [n_tiles]
   DBuf chunks;       // Chunk [n_chunks]
-  DBuf work;         // int4 [n_work] (tile0, tile1, part0, nslot): one chunk per warp of the term kernel
+  DBuf cta_tiles;    // int2 [n_cta] tile range of each CTA of the term kernel
   DBuf cam_s;        // int32 [n_slots] camera of each slot
   DBuf file_s;       // int32 [n_slots] file index of each slot (-1 padding)
   DBuf pix_s;        // double2 [n_slots] pixels
   DBuf lidx_s;       // uint8 [n_slots] landmark index within its tile
-  DBuf perm_s;       // uint8 [n_slots] tile-local position sorted by camera
   DBuf lm_slot0;     // int32 [n_lm_l] first slot of each local landmark
   DBuf lm_k;         // int32 [n_lm_l]
-  DBuf seg_start;    // uint8 [n_slots] per tile: start position of segment s at tile*kTile + s
-  DBuf seg_slot;     // uint16 [n_slots] per tile: chunk slot of segment s
-  DBuf seg_obs;      // uint8 [n_slots] segment of each observation
-  DBuf seg_cam;      // int32 [n_slots] per tile: camera of segment s
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
   DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
@@ -238,7 +245,6 @@ struct Ctx {
   DBuf red;          // double scratch for reductions
   DBuf cub_tmp;      // CUB temp storage
 
-  bool l2_window_set = false;
   double lam = 0;
   int identity = 0;
   int64_t n_invalid = 0;

@@ -203,12 +203,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 struct TermArgs {
-  unsigned long long* dbg;  // POBA_PHASE_TIMING: per-phase cycle totals (8 entries)
   const TileK* tk;         // per warp-tile kernel descriptors
-  const int* seg_cam;      // camera of segment s of each tile (slot space)
-  const int4* work;        // per warp: (tile0, tile1, part0, nslot) -- one chunk
-  int n_work;
+  const int2* cta_tiles;   // tile range of each CTA
+  const int* cam_s;        // camera of each slot (gathered two tiles ahead)
   const double2* J;        // slot rows
   const double* tin;       // camera vector (kModeTerm)
   const double* lvec;      // b_l (kModeBt) or landmark input (kModeW)
@@ -219,153 +221,126 @@ struct TermArgs {
   int check_stop;
 };
 
-// Per-warp shared memory (bytes): kStages stages of one warp-tile (32 rows of
-// 208 B, the 32-B descriptor and the V^-1 slice of its landmarks); the camera
-// records of the tile's distinct cameras (double-buffered, filled one tile
-// ahead), per-observation g rows, per-segment sums and the permutation.
-constexpr int kStDesc = kTile * kRowBytes;                 // 6656
-constexpr int kStVinv = kStDesc + 32;                      // 6688
-constexpr int kStageBytes = (kStVinv + kTileLm * 48 + 127) / 128 * 128;
-constexpr int kRecBytes = kTStride * 8;                    // 80-B camera record
-constexpr int kWOffBars = kStages * kStageBytes;
-constexpr int kWOffT = kWOffBars + 16 * kStages;           // 2 x 32 camera records
-constexpr int kWOffG = kWOffT + 2 * kTile * kRecBytes;      // g rows (32 x 80 B)
-constexpr int kWOffS = kWOffG + kTile * kRecBytes;          // segment sums (32 x 80 B)
-constexpr int kWOffP = kWOffS + kTile * kRecBytes;          // permutation (32 B)
-constexpr int kWarpSmem = (kWOffP + kTile + 127) / 128 * 128;
-constexpr int kTermSmem = kTermWarps * kWarpSmem;
-constexpr int kPieces = kTile * (kRecBytes / 16) / 32;      // 16-B pieces per lane to cover 32 records = 5
-static_assert(kTermSmem <= 227 * 1024, "term kernel shared memory over budget");
-
-// One warp streams one chunk of warp-tiles through its own bulk-copy pipeline;
-// warps never wait on each other.  Everything indexed by camera is moved per
-// DISTINCT camera of the tile (its camera segments), five lanes per 80-byte
-// record with 16-byte accesses: the camera vector t_c is gathered one tile
-// ahead into a shared table, the chunk accumulators are read and written the
-// same way.  Within a tile the landmark sums are a segmented warp scan
-// (landmarks are runs of consecutive lanes); V^-1 is applied on each run's last
-// lane and z broadcast back by shuffle; camera segments are summed in the fixed
-// camera-sorted order.
+// One CTA per SM streams a contiguous range of warp-tiles; warp w of the CTA
+// takes tiles range.x + w, + w + 8, ... through its own one-stage bulk-copy
+// pipeline (the stage is released as soon as the tile's rows are in
+// registers, so the next tile's copy overlaps the whole tile's math).
+//   phase 1  u_o = J_p t_c with t_c from the warp's gathered camera records
+//            (five lanes per 80-B record, 16-B loads, one tile ahead),
+//            w_o = J_l^T u_o, landmark sums y_l by a segmented warp scan
+//   phase 2  z_l = V_l^-1 y_l on each landmark's last lane, shuffled back
+//   phase 3  g_o = J_p^T (J_l z_l), nine doubles in registers
+//   apply    g_o is added into the CTA's shared-memory accumulator record of
+//            its camera slot.  Tiles apply strictly in tile order (a turn
+//            barrier is passed from warp to warp), so every camera sum is
+//            formed in one fixed order: no atomics, bitwise reproducible.  A
+//            camera seen twice in one tile is pre-summed in lane order.
+// At the last tile of a chunk the table is written out once (one 80-B
+// partial per (chunk, camera)) and cleared for the next chunk.
 template <int MODE>
 __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kTermWarps + wid;
-  if (gw >= a.n_work) return;
   if (a.check_stop && a.st->stopped) return;
-  uint8_t* wsm = smraw + wid * kWarpSmem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wsm + kWOffBars);
-  double2* ttab = reinterpret_cast<double2*>(wsm + kWOffT);   // [2][32 records][5]
-  double2* gtab = reinterpret_cast<double2*>(wsm + kWOffG);   // [32 obs][5]
-  double2* stab = reinterpret_cast<double2*>(wsm + kWOffS);   // [32 segments][5]
-  uint8_t* pbuf = wsm + kWOffP;
-  const int4 wr = a.work[gw];
-  const int nq = wr.y - wr.x;
-  double* acc = a.partials + (int64_t)wr.z * kTStride;  // this warp's chunk accumulators
-  for (int k = lane; k < wr.w * kTStride; k += 32) acc[k] = 0.0;
-  if (lane == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+  const int2 range = a.cta_tiles[blockIdx.x];
+  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(smraw + kTermWarps * kWarpSmem);
+  uint64_t* turn_bar = stage_bar + kTermWarps;
+  double2* acc = reinterpret_cast<double2*>(smraw + kTermWarps * kWarpSmem + kTermBars);  // [kAccSlots][5]
+  for (int k = threadIdx.x; k < kAccSlots * 5; k += blockDim.x) acc[k] = make_double2(0.0, 0.0);
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < kTermWarps; ++w) {
+      mbar_init(&stage_bar[w], 1);
+      mbar_init(&turn_bar[w], 1);
+    }
     fence_mbar_init();
   }
-
+  __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive(&turn_bar[0]);  // the range's first tile applies first
+  const int t_first = range.x + wid;
+  if (t_first >= range.y) return;
+  const int nq = (range.y - t_first + kTermWarps - 1) / kTermWarps;
+  uint8_t* stg = smraw + wid * kWarpSmem;
+  double2* ttab = reinterpret_cast<double2*>(stg + kStageBytes);  // [32 observations][5]
+  uint64_t* sbar = &stage_bar[wid];
   const uint64_t pol = policy_evict_first();
-  auto issue = [&](int q, int4 d) {  // lane 0; d = (n, lm0, nlm, nseg) of tile wr.x + q
-    const int ti = wr.x + q;
-    uint8_t* stg = wsm + (q % kStages) * kStageBytes;
-    uint64_t* bar = &bars[q % kStages];
+
+  auto issue = [&](int ti, int4 d) {  // lane 0; d = (n, lm0, nlm, flags) of tile ti
     const uint32_t vbytes = (MODE != kModeW) ? (uint32_t)(d.z * 48) : 0u;
-    mbar_expect_tx(bar, (uint32_t)(d.x * kRowBytes + 32) + vbytes);
-    bulk_g2s_stream(stg, a.J + (int64_t)ti * kTile * kRow, (uint32_t)(d.x * kRowBytes), bar, pol);
-    bulk_g2s(stg + kStDesc, a.tk + ti, 32, bar);
-    if (vbytes) bulk_g2s(stg + kStVinv, a.Vinv + (int64_t)d.y * 6, vbytes, bar);
+    mbar_expect_tx(sbar, (uint32_t)(d.x * kRowBytes + 32) + vbytes);
+    bulk_g2s_stream(stg, a.J + (int64_t)ti * kTile * kRow, (uint32_t)(d.x * kRowBytes), sbar, pol);
+    bulk_g2s(stg + kStDesc, a.tk + ti, 32, sbar);
+    if (vbytes) bulk_g2s(stg + kStVinv, a.Vinv + (int64_t)d.y * 6, vbytes, sbar);
+  };
+  auto gather = [&](int cam_lane, double2* tp) {  // 5 x 16-B pieces of the tile's 32 camera records
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const int k = 32 * r + lane;
+      const int cam = __shfl_sync(0xffffffffu, cam_lane, k / 5);
+      tp[r] = reinterpret_cast<const double2*>(a.tin + (int64_t)cam * kTStride)[k % 5];
+    }
   };
   int4 dnext = make_int4(0, 0, 0, 0);
   if (lane == 0) {
-    for (int q = 0; q < kStages && q < nq; ++q) issue(q, *reinterpret_cast<const int4*>(a.tk + wr.x + q));
-    if (kStages < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + kStages);
+    issue(t_first, *reinterpret_cast<const int4*>(a.tk + t_first));
+    if (nq > 1) dnext = *reinterpret_cast<const int4*>(a.tk + t_first + kTermWarps);
   }
-  // camera records of the next tile's segments (gathered one tile ahead; segment
-  // cameras two tiles ahead; padding segments name camera 0)
-  const int rec = lane / 5;  // piece r of lane covers record (32 r + lane) / 5
-  double2 tp[kPieces];
-  int sc_next = 0;
+  double2 tp[5];
+  int cam_next = 0;
   if (MODE == kModeTerm) {
-    const int sc0 = a.seg_cam[(int64_t)wr.x * kTile + lane];
+    gather(a.cam_s[(int64_t)t_first * kTile + lane], tp);
 #pragma unroll
-    for (int r = 0; r < kPieces; ++r) {
-      const int k = 32 * r + lane;
-      const int c = __shfl_sync(0xffffffffu, sc0, k / 5);
-      ttab[k] = reinterpret_cast<const double2*>(a.tin + (int64_t)c * kTStride)[k % 5];
-    }
-    if (nq > 1) sc_next = a.seg_cam[(int64_t)(wr.x + 1) * kTile + lane];
+    for (int r = 0; r < 5; ++r) ttab[32 * r + lane] = tp[r];
+    if (nq > 1) cam_next = a.cam_s[(int64_t)(t_first + kTermWarps) * kTile + lane];
   }
-  (void)rec;
   __syncwarp();
-#ifdef POBA_PHASE_TIMING
-  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long tprev = clock64();
-#define PHASE(k) do { const long long tnow_ = clock64(); ph[k] += (unsigned long long)(tnow_ - tprev); tprev = tnow_; } while (0)
-#else
-#define PHASE(k) do { } while (0)
-#endif
+
   for (int q = 0; q < nq; ++q) {
-    const double2* tcur = ttab + (q & 1) * (kTile * 5);
-    if (MODE == kModeTerm && q + 1 < nq) {
-#pragma unroll
-      for (int r = 0; r < kPieces; ++r) {
-        const int k = 32 * r + lane;
-        const int c = __shfl_sync(0xffffffffu, sc_next, k / 5);
-        tp[r] = reinterpret_cast<const double2*>(a.tin + (int64_t)c * kTStride)[k % 5];
-      }
-      sc_next = (q + 2 < nq) ? a.seg_cam[(int64_t)(wr.x + q + 2) * kTile + lane] : 0;
+    const int ti = t_first + q * kTermWarps;
+    if (MODE == kModeTerm && q + 1 < nq) {  // next tile's camera records, in flight during this tile
+      gather(cam_next, tp);
+      cam_next = (q + 2 < nq) ? a.cam_s[(int64_t)(ti + 2 * kTermWarps) * kTile + lane] : 0;
     }
-    const uint8_t* stg = wsm + (q % kStages) * kStageBytes;
-    mbar_wait(&bars[q % kStages], (uint32_t)((q / kStages) & 1));
-    PHASE(0);
+    mbar_wait(sbar, (uint32_t)(q & 1));
     const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
     const bool valid = lane < t.n;
     const bool is_long = t.flags & kTileLong;
     const double2* row = reinterpret_cast<const double2*>(stg) + lane * kRow;
-    RowMeta m = {0, 0, 0, 0};
-    if (valid) {  // one 16-B shared load
+    int slot = 0, li = 0;
+    if (valid) {
       const int4 mv = *reinterpret_cast<const int4*>(row + 12);
-      m.cam = mv.x;
-      m.packed = mv.y;
-      m.seg_slot = mv.z;
-      m.seg_cam = mv.w;
+      slot = mv.y;
+      li = mv.z;
     }
-    const int li = (m.packed >> 8) & 0xff;
-    const int my_seg = (m.packed >> 24) & 0xff;
-    const int nseg = t.nseg;
-    // chunk-accumulator pieces of this tile's segments (read before this tile's
-    // writes, after the previous tile's), 16 B per lane per round
-    double2 oldp[kPieces];
-    int slotp[kPieces];
-#pragma unroll
-    for (int r = 0; r < kPieces; ++r) {
-      const int k = 32 * r + lane;
-      const int sg = k / 5;
-      const int sl = __shfl_sync(0xffffffffu, m.seg_slot, sg & 31);
-      slotp[r] = (sg < nseg) ? sl : -1;
-      oldp[r] = (sg < nseg) ? reinterpret_cast<const double2*>(acc + (int64_t)sl * kTStride)[k % 5]
-                            : make_double2(0.0, 0.0);
-    }
-    double2 jr[kJPlanes];
-#pragma unroll
-    for (int p = 0; p < kJPlanes; ++p) jr[p] = valid ? row[p] : make_double2(0.0, 0.0);
-    if (valid) pbuf[lane] = (uint8_t)(m.packed & 0xff);
     // landmark runs: heads, my run's first and last lane
-    const int lim = is_long ? 0 : li;
-    const int prev_li = __shfl_up_sync(0xffffffffu, lim, 1);
-    const bool head = valid && (lane == 0 || prev_li != lim);
+    const int prev_li = __shfl_up_sync(0xffffffffu, li, 1);
+    const bool head = valid && (lane == 0 || prev_li != li);
     const unsigned heads = __ballot_sync(0xffffffffu, head) | (t.n < 32 ? (1u << t.n) : 0u);
     const unsigned above = heads & ~((2u << lane) - 1u);
     const int last = (above ? __ffs(above) - 1 : t.n) - 1;
     const int first = 31 - __clz(heads & ((2u << lane) - 1u));
-    // phase 1: w_o = J_l^T (J_p t_c), then the landmark sums y_l by a segmented scan
+    const bool is_last = valid && lane == last;
+    double vi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (MODE != kModeW && is_last && !(MODE == kModeTerm && is_long)) {
+      const double2* vs = reinterpret_cast<const double2*>(stg + kStVinv) + li * 3;
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const double2 v = vs[p];
+        vi[2 * p] = v.x;
+        vi[2 * p + 1] = v.y;
+      }
+    }
+    double2 jr[kJPlanes];
+#pragma unroll
+    for (int p = 0; p < kJPlanes; ++p) jr[p] = valid ? row[p] : make_double2(0.0, 0.0);
+    __syncwarp();  // every lane is done with the stage: refill it with this warp's next tile
+    if (lane == 0 && q + 1 < nq) {
+      issue(ti + kTermWarps, dnext);
+      if (q + 2 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + ti + 2 * kTermWarps);
+    }
+    // phase 1
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;
     if (MODE == kModeTerm && valid && !is_long) {
-      const double2* tr = tcur + my_seg * 5;
+      const double2* tr = ttab + lane * 5;
       double tc[10];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
@@ -396,10 +371,9 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
         }
       }
     }
-    PHASE(1);
-    // phase 2: z_l = V_l^-1 y_l on each landmark's last lane, broadcast to the run
+    // phase 2
     double z0 = 0.0, z1 = 0.0, z2 = 0.0;
-    if (valid && lane == last) {
+    if (is_last) {
       const int lm = t.lm0 + li;
       if (MODE == kModeW) {
         z0 = a.lvec[lm * 3]; z1 = a.lvec[lm * 3 + 1]; z2 = a.lvec[lm * 3 + 2];
@@ -412,7 +386,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
         } else {
           y[0] = w0; y[1] = w1; y[2] = w2;
         }
-        sym3_mv(reinterpret_cast<const double*>(stg + kStVinv) + (is_long ? 0 : li) * 6, y, z);
+        sym3_mv(vi, y, z);
         z0 = z[0]; z1 = z[1]; z2 = z[2];
       }
     }
@@ -420,73 +394,56 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     z0 = __shfl_sync(0xffffffffu, z0, src);
     z1 = __shfl_sync(0xffffffffu, z1, src);
     z2 = __shfl_sync(0xffffffffu, z2, src);
-    const int sstart = (m.packed >> 16) & 0xff;
-    const int snext = __shfl_down_sync(0xffffffffu, sstart, 1);
-    const int send = (lane + 1 < nseg) ? snext : t.n;
-    const int tn_ = t.n;
-    __syncwarp();  // every lane is done with the stage
-    PHASE(2);
-    if (lane == 0 && q + kStages < nq) {  // refill the stage two tiles ahead
-      issue(q + kStages, dnext);
-      if (q + kStages + 1 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + wr.x + q + kStages + 1);
-    }
-    PHASE(3);
-    // phase 3: g_o = J_p^T (J_l z_l) into this lane's g row
-    if (valid) {
+    // phase 3
+    double g[9];
+    {
       const double v0 = fma(jr[9].x, z0, fma(jr[10].x, z1, jr[11].x * z2));
       const double v1 = fma(jr[9].y, z0, fma(jr[10].y, z1, jr[11].y * z2));
-      double2* gr = gtab + lane * 5;
 #pragma unroll
-      for (int p = 0; p < 4; ++p)
-        gr[p] = make_double2(fma(jr[2 * p].x, v0, jr[2 * p].y * v1), fma(jr[2 * p + 1].x, v0, jr[2 * p + 1].y * v1));
-      gr[4] = make_double2(fma(jr[8].x, v0, jr[8].y * v1), 0.0);
+      for (int j = 0; j < 9; ++j) g[j] = fma(jr[j].x, v0, jr[j].y * v1);
     }
-    __syncwarp();
-    PHASE(4);
-    // phase 4: lane s sums camera segment s in fixed (camera-sorted) order
-    if (lane < nseg) {
-      double2 sum[5];
+    bool apply = valid;
+    if (t.flags & kTileDupCam) {  // cameras seen twice in this tile: pre-sum on the lowest lane, lane order
+      const unsigned grp = __match_any_sync(0xffffffffu, valid ? slot : -1 - lane);
+      const int leader = __ffs(grp) - 1;
+      unsigned pend = (valid && lane == leader) ? (grp & ~(1u << lane)) : 0u;
+      apply = valid && lane == leader;
+      while (__any_sync(0xffffffffu, pend != 0u)) {
+        const int from = pend ? __ffs(pend) - 1 : lane;
 #pragma unroll
-      for (int p = 0; p < 5; ++p) sum[p] = make_double2(0.0, 0.0);
-      for (int r = sstart; r < send; ++r) {
-        const double2* gr = gtab + pbuf[r] * 5;
-#pragma unroll
-        for (int p = 0; p < 5; ++p) {
-          const double2 v = gr[p];
-          sum[p].x += v.x;
-          sum[p].y += v.y;
+        for (int j = 0; j < 9; ++j) {
+          const double v = __shfl_sync(0xffffffffu, g[j], from);
+          if (pend) g[j] += v;
         }
+        pend &= pend - 1u;
       }
-#pragma unroll
-      for (int p = 0; p < 5; ++p) stab[lane * 5 + p] = sum[p];
     }
-    (void)tn_;
+    mbar_wait(&turn_bar[wid], (uint32_t)(q & 1));
+    if (apply) {
+      double2* r = acc + slot * 5;
+      const double2 o0 = r[0], o1 = r[1], o2 = r[2], o3 = r[3], o4 = r[4];
+      r[0] = make_double2(o0.x + g[0], o0.y + g[1]);
+      r[1] = make_double2(o1.x + g[2], o1.y + g[3]);
+      r[2] = make_double2(o2.x + g[4], o2.y + g[5]);
+      r[3] = make_double2(o3.x + g[6], o3.y + g[7]);
+      r[4] = make_double2(o4.x + g[8], o4.y);
+    }
     __syncwarp();
-    // ... and the chunk accumulators are updated 16 B per lane
-#pragma unroll
-    for (int r = 0; r < kPieces; ++r) {
-      const int k = 32 * r + lane;
-      if (slotp[r] >= 0) {
-        const double2 v = stab[k];
-        reinterpret_cast<double2*>(acc + (int64_t)slotp[r] * kTStride)[k % 5] =
-            make_double2(oldp[r].x + v.x, oldp[r].y + v.y);
+    if (t.flags & kTileChunkLast) {  // write the chunk's partials, clear the table
+      double2* out = reinterpret_cast<double2*>(a.partials) + (int64_t)t.part0 * 5;
+      for (int k = lane; k < t.nslot * 5; k += 32) {
+        out[k] = acc[k];
+        acc[k] = make_double2(0.0, 0.0);
       }
+      __syncwarp();
     }
+    if (lane == 0 && ti + 1 < range.y) mbar_arrive(&turn_bar[(wid + 1) % kTermWarps]);
     if (MODE == kModeTerm && q + 1 < nq) {
-      double2* tnext = ttab + ((q + 1) & 1) * (kTile * 5);
 #pragma unroll
-      for (int r = 0; r < kPieces; ++r) tnext[32 * r + lane] = tp[r];
+      for (int r = 0; r < 5; ++r) ttab[32 * r + lane] = tp[r];
     }
     __syncwarp();
-    PHASE(5);
   }
-#ifdef POBA_PHASE_TIMING
-  if (lane == 0 && a.dbg) {
-    for (int k = 0; k < 6; ++k) atomicAdd(&a.dbg[k], ph[k]);
-    atomicAdd(&a.dbg[7], (unsigned long long)nq);
-  }
-#endif
-#undef PHASE
 }
 
 // ---------------------------------------------------------------------------
@@ -824,37 +781,7 @@ __global__ void k_add_inplace(double* __restrict__ a, const double* __restrict__
   if (q < n) a[q] += b[q];
 }
 
-size_t term_smem(const Ctx& c) {
-  (void)c;
-  return (size_t)kTermSmem;
-}
-
-// Keep the chunk accumulators resident in L2 while the Jacobians stream past
-// (persisting access-policy window on the context stream).
-int configure_l2(Ctx& c) {
-  if (c.l2_window_set) return POBA_OK;
-  c.l2_window_set = true;
-  cudaDeviceProp prop;
-  PCK(cudaGetDeviceProperties(&prop, c.device));
-  if (prop.persistingL2CacheMaxSize <= 0 || prop.accessPolicyMaxWindowSize <= 0) return POBA_OK;
-  const size_t want = (size_t)std::max(c.n_partials, 1) * kTStride * 8;
-  const size_t carve = std::min<size_t>(want, (size_t)prop.persistingL2CacheMaxSize);
-  if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) {
-    cudaGetLastError();
-    return POBA_OK;
-  }
-  cudaStreamAttrValue v = {};
-  v.accessPolicyWindow.base_ptr = c.partials.p;
-  v.accessPolicyWindow.num_bytes = std::min<size_t>(want, (size_t)prop.accessPolicyMaxWindowSize);
-  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)carve / (float)v.accessPolicyWindow.num_bytes);
-  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  if (cudaStreamSetAttribute(c.stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) cudaGetLastError();
-  return POBA_OK;
-}
-
 int configure_term(Ctx& c) {
-  if (getenv("POBA_NO_L2_WINDOW") == nullptr) PTRY(configure_l2(c));
   static thread_local int done_dev = -1;
   int dev = 0;
   PCK(cudaGetDevice(&dev));
@@ -869,11 +796,9 @@ int configure_term(Ctx& c) {
 
 TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_stop) {
   TermArgs a;
-  a.dbg = c.dbg.as<unsigned long long>();
   a.tk = c.tilek.as<TileK>();
-  a.seg_cam = c.seg_cam.as<int>();
-  a.work = c.work.as<int4>();
-  a.n_work = c.n_work;
+  a.cta_tiles = c.cta_tiles.as<int2>();
+  a.cam_s = c.cam_s.as<int>();
   a.J = c.J.as<double2>();
   a.tin = tin;
   a.lvec = lvec;
@@ -910,8 +835,8 @@ CamArgs cam_args(Ctx& c, int order, double eps, bool check_stop) {
 int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool check_stop) {
   PTRY(configure_term(c));
   const TermArgs a = term_args(c, tin, lvec, check_stop);
-  const size_t smem = term_smem(c);
-  const unsigned grid = grid_for(c.n_work, kTermWarps);
+  const size_t smem = kTermSmem;
+  const unsigned grid = (unsigned)c.n_cta;
   if (mode == kModeTerm) {
     if (c.n_long) {
       k_wt_long<kOutZ><<<c.n_long, kLongThreads, 0, c.stream>>>(

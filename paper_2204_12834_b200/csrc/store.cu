@@ -116,117 +116,15 @@ __global__ void k_fill_i32(int* __restrict__ a, int64_t n, int v) {
   if (i < n) a[i] = v;
 }
 
-// key (chunk, cam) per slot; padding slots -> sentinel
-__global__ void k_chunk_cam_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, int bc,
-                                 uint64_t* __restrict__ key) {
-  const Tile t = tiles[blockIdx.x];
-  const int64_t s0 = (int64_t)blockIdx.x * kTile;
-  for (int i = threadIdx.x; i < kTile; i += blockDim.x)
-    key[s0 + i] = i < t.n ? (((uint64_t)t.chunk << bc) | (uint64_t)cam_s[s0 + i]) : kSentinel;
-}
-
-__global__ void k_unique_flags(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ flag) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
-}
-
-__global__ void k_unique_compact(const uint64_t* __restrict__ key, const int* __restrict__ flag,
-                                 const int* __restrict__ pos, int64_t n, uint64_t* __restrict__ out) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n && flag[i]) out[pos[i]] = key[i];
-}
-
-__global__ void k_chunk_first(const uint64_t* __restrict__ ukey, int n_u, int bc, int* __restrict__ first) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_u) return;
-  int ch = (int)(ukey[i] >> bc);
-  if (i == 0 || (int)(ukey[i - 1] >> bc) != ch) first[ch] = i;
-}
-
-__global__ void k_part_keys(const uint64_t* __restrict__ ukey, int n_u, int bc, int bch, uint64_t* __restrict__ key,
-                            int* __restrict__ val, int* __restrict__ cam_cnt) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_u) return;
-  uint64_t u = ukey[i];
-  int cam = (int)(u & ((1ull << bc) - 1));
-  int ch = (int)(u >> bc);
-  key[i] = ((uint64_t)cam << bch) | (uint64_t)ch;
-  val[i] = i;
-  atomicAdd(&cam_cnt[cam], 1);
-}
-
-// key (tile, cam, tile position) per slot; padding -> sentinel
-__global__ void k_tile_cam_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s, int bc,
-                                uint64_t* __restrict__ key) {
-  const Tile t = tiles[blockIdx.x];
-  const int64_t s0 = (int64_t)blockIdx.x * kTile;
-  for (int i = threadIdx.x; i < kTile; i += blockDim.x)
-    key[s0 + i] = i < t.n ? (((uint64_t)blockIdx.x << (bc + 8)) | ((uint64_t)cam_s[s0 + i] << 8) | (uint64_t)i)
-                          : kSentinel;
-}
-
-__global__ void k_seg_flags(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ flag) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n) return;
-  flag[q] = (q == 0 || (key[q] >> 8) != (key[q - 1] >> 8)) ? 1 : 0;
-}
-
-__device__ __forceinline__ int lower_bound_u64(const uint64_t* __restrict__ a, int lo, int hi, uint64_t target) {
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < target) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// per tile: permutation (position sorted by camera) and camera segments
-__global__ void k_segments(const uint64_t* __restrict__ key, const int* __restrict__ flag,
-                           const int* __restrict__ segpos, Tile* __restrict__ tiles,
-                           const Chunk* __restrict__ chunks, const uint64_t* __restrict__ ukey, int bc,
-                           uint8_t* __restrict__ perm_s, uint8_t* __restrict__ seg_start,
-                           uint16_t* __restrict__ seg_slot, uint8_t* __restrict__ seg_obs,
-                           int* __restrict__ seg_cam) {
-  const int ti = blockIdx.x;
-  const Tile t = tiles[ti];
-  const Chunk ch = chunks[t.chunk];
-  const int64_t s0 = (int64_t)ti * kTile;
-  for (int r = threadIdx.x; r < t.n; r += blockDim.x) {
-    const int64_t q = t.obs0 + r;
-    const uint64_t k = key[q];
-    perm_s[s0 + r] = (uint8_t)(k & 0xff);
-    seg_obs[s0 + (k & 0xff)] = (uint8_t)(segpos[q] + flag[q] - 1 - segpos[t.obs0]);
-    if (flag[q]) {
-      const int cam = (int)((k >> 8) & ((1ull << bc) - 1));
-      const uint64_t target = ((uint64_t)t.chunk << bc) | (uint64_t)cam;
-      const int u = lower_bound_u64(ukey, ch.part0, ch.part0 + ch.nslot, target);
-      const int64_t sl = s0 + (segpos[q] - segpos[t.obs0]);  // segment index within the tile
-      seg_start[sl] = (uint8_t)r;
-      seg_slot[sl] = (uint16_t)(u - ch.part0);
-      seg_cam[sl] = cam;
-    }
-  }
-  if (threadIdx.x == 0) {
-    const int s_first = segpos[t.obs0];
-    const int s_end = segpos[t.obs0 + t.n - 1] + flag[t.obs0 + t.n - 1];
-    tiles[ti].seg0 = s_first;
-    tiles[ti].nseg = s_end - s_first;
-  }
-}
-
 // metadata column (row entry 12) of every slot
-__global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
-                            const uint8_t* __restrict__ perm_s, const uint8_t* __restrict__ lidx_s,
-                            const uint8_t* __restrict__ seg_start, const uint16_t* __restrict__ seg_slot,
-                            const uint8_t* __restrict__ seg_obs, const int* __restrict__ seg_cam,
-                            double2* __restrict__ J) {
-  const Tile t = tiles[blockIdx.x];
-  const int i = threadIdx.x;
-  const int64_t s = (int64_t)blockIdx.x * kTile + i;
+__global__ void k_pack_meta(const int* __restrict__ cam_s, const int* __restrict__ slot_s,
+                            const uint8_t* __restrict__ lidx_s, double2* __restrict__ J) {
+  const int64_t s = (int64_t)blockIdx.x * kTile + threadIdx.x;
   RowMeta m;
   m.cam = cam_s[s];
-  m.packed = (int)perm_s[s] | ((int)lidx_s[s] << 8) | ((int)seg_start[s] << 16) | ((int)seg_obs[s] << 24);
-  m.seg_slot = i < t.nseg ? (int)seg_slot[s] : 0;
-  m.seg_cam = i < t.nseg ? seg_cam[s] : 0;
+  m.slot = slot_s[s];
+  m.li = lidx_s[s];
+  m.pad = 0;
   *reinterpret_cast<RowMeta*>(J + s * kRow + 12) = m;
 }
 
@@ -517,12 +415,10 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PTRY(c.file_s.alloc(ns * 4));
   PTRY(c.pix_s.alloc(ns * 16));
   PTRY(c.lidx_s.alloc(ns));
-  PTRY(c.perm_s.alloc(ns));
   PCK(cudaMemsetAsync(c.cam_s.p, 0, ns * 4, s));
   k_fill_i32<<<grid_for(ns, B), B, 0, s>>>(c.file_s.as<int>(), ns, -1);
   PCK(cudaMemsetAsync(c.pix_s.p, 0, ns * 16, s));
   PCK(cudaMemsetAsync(c.lidx_s.p, 0, ns, s));
-  PCK(cudaMemsetAsync(c.perm_s.p, 0, ns, s));
   c.launches++;
   {
     DBuf ka, kb, va, vb, pixf, dfirst, dtidx;
@@ -551,159 +447,109 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   }
   c.have_pixels = h_pix != nullptr;
 
-  // --- chunks + camera slots -------------------------------------------------------------------------
+  // --- term-kernel work: CTA tile ranges, chunks, camera slots (host) ----------------------------
+  // Each CTA of the term kernel owns a contiguous tile range (balanced by
+  // observations); the range is cut greedily into chunks whose distinct cameras
+  // fit the shared-memory accumulator table (kAccSlots records).  Slots are
+  // numbered in first-appearance order; partial p = part0 + slot of a chunk
+  // holds that camera's sum over the chunk.
+  std::vector<int> obs_slot(ns, 0);
   std::vector<Chunk> chunks;
+  std::vector<int> part_cam;  // camera of each partial
   {
-    const int target = std::max(1, std::min(c.n_tiles, kTermWarps * c.n_sm));
+    std::vector<int> hcam(ns);
+    PTRY(poba::copy_sync(c, hcam.data(), c.cam_s.p, ns * 4, cudaMemcpyDeviceToHost));
+    const int n_cta = std::max(1, std::min(c.n_sm, (c.n_tiles + kTermWarps - 1) / kTermWarps));
     std::vector<int64_t> cum(c.n_tiles + 1, 0);
     for (int i = 0; i < c.n_tiles; ++i) cum[i + 1] = cum[i] + tiles[i].n;
+    std::vector<int2> cta(n_cta);
     int prev = 0;
-    for (int q = 1; q <= target && prev < c.n_tiles; ++q) {
-      int64_t want = (nl * q) / target;
-      int e = (int)(std::lower_bound(cum.begin(), cum.end(), want) - cum.begin());
-      e = std::min(std::max(e, prev + 1), c.n_tiles);
-      if (q == target) e = c.n_tiles;
-      chunks.push_back(Chunk{prev, e, 0, 0});
+    for (int b = 0; b < n_cta; ++b) {
+      int e = c.n_tiles;
+      if (b + 1 < n_cta) {
+        const int64_t want = (nl * (b + 1)) / n_cta;
+        e = (int)(std::lower_bound(cum.begin(), cum.end(), want) - cum.begin());
+        e = std::min(std::max(e, prev + 1), c.n_tiles - (n_cta - 1 - b));
+      }
+      cta[b] = make_int2(prev, e);
       prev = e;
     }
-  }
-  DBuf ka, kb, ukey, fl, pos;
-  PTRY(ka.alloc(ns * 8));
-  PTRY(kb.alloc(ns * 8));
-  PTRY(ukey.alloc(nl * 8));
-  PTRY(fl.alloc((nl + 1) * 4));
-  PTRY(pos.alloc((nl + 1) * 4));
-  int n_u = 0;
-  for (int iter = 0;; ++iter) {
-    for (size_t q = 0; q < chunks.size(); ++q)
-      for (int t = chunks[q].tile0; t < chunks[q].tile1; ++t) tiles[t].chunk = (int)q;
-    PTRY(c.tiles.alloc(tiles.size() * sizeof(Tile)));
-    PCK(cudaMemcpyAsync(c.tiles.p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice, s));
-    const int bchunk = std::max(1, bitlen((uint64_t)chunks.size()));
-    if (bchunk + bc > 63) return fail(POBA_EINVAL, "chunk key exceeds 64 bits");
-    k_chunk_cam_keys<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
-    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
-    k_unique_flags<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, fl.as<int>());
-    PCK(cudaMemsetAsync(fl.as<int>() + nl, 0, 4, s));
-    PTRY(excl_sum(c, fl.as<int>(), pos.as<int>(), nl + 1));
-    k_unique_compact<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), fl.as<int>(), pos.as<int>(), nl,
-                                                  ukey.as<uint64_t>());
-    c.launches += 3;
-    PCK(cudaMemcpyAsync(&n_u, pos.as<int>() + nl, 4, cudaMemcpyDeviceToHost, s));
-    PCK(cudaStreamSynchronize(s));
-    DBuf dfirst;
-    PTRY(dfirst.alloc(chunks.size() * 4));
-    k_chunk_first<<<grid_for(n_u, B), B, 0, s>>>(ukey.as<uint64_t>(), n_u, bc, dfirst.as<int>());
-    c.launches++;
-    std::vector<int> first(chunks.size() + 1, 0);
-    PCK(cudaMemcpyAsync(first.data(), dfirst.p, chunks.size() * 4, cudaMemcpyDeviceToHost, s));
-    PCK(cudaStreamSynchronize(s));
-    first[chunks.size()] = n_u;
-    bool split = false;
-    std::vector<Chunk> next;
-    for (size_t q = 0; q < chunks.size(); ++q) {
-      chunks[q].part0 = first[q];
-      chunks[q].nslot = first[q + 1] - first[q];
-      if (chunks[q].nslot > kSlotCap && chunks[q].tile1 - chunks[q].tile0 > 1) {
-        const int mid = (chunks[q].tile0 + chunks[q].tile1) / 2;
-        next.push_back(Chunk{chunks[q].tile0, mid, 0, 0});
-        next.push_back(Chunk{mid, chunks[q].tile1, 0, 0});
-        split = true;
-      } else {
-        next.push_back(chunks[q]);
+    std::vector<int> stamp(n_cam, -1), tstamp(n_cam, -1), slot_of(n_cam, 0);
+    for (int b = 0; b < n_cta; ++b) {
+      int ch = -1, cnt = 0;
+      for (int ti = cta[b].x; ti < cta[b].y; ++ti) {
+        Tile& t = tiles[ti];
+        const int64_t s0 = (int64_t)ti * kTile;
+        int fresh = 0;
+        bool dup = false;
+        for (int i = 0; i < t.n; ++i) {
+          const int cam = hcam[s0 + i];
+          if (tstamp[cam] == ti) {
+            dup = true;
+            continue;
+          }
+          tstamp[cam] = ti;
+          if (ch < 0 || stamp[cam] != ch) ++fresh;
+        }
+        if (ch < 0 || cnt + fresh > kAccSlots) {
+          if (ch >= 0) chunks.back().tile1 = ti;
+          chunks.push_back(Chunk{ti, ti, (int)part_cam.size(), 0});
+          ch = (int)chunks.size() - 1;
+          cnt = 0;
+        }
+        for (int i = 0; i < t.n; ++i) {
+          const int cam = hcam[s0 + i];
+          if (stamp[cam] != ch) {
+            stamp[cam] = ch;
+            slot_of[cam] = cnt++;
+            part_cam.push_back(cam);
+          }
+          obs_slot[s0 + i] = slot_of[cam];
+        }
+        chunks.back().nslot = cnt;
+        t.chunk = ch;
+        if (dup) t.flags |= kTileDupCam;
       }
+      chunks.back().tile1 = cta[b].y;
     }
-    if (!split) break;
-    chunks.swap(next);
-    if (iter > 60) return fail(POBA_EINVAL, "cannot split chunks under the camera-slot cap");
+    for (const Chunk& q : chunks) tiles[q.tile1 - 1].flags |= kTileChunkLast;
+    c.n_cta = n_cta;
+    PTRY(c.cta_tiles.alloc(n_cta * sizeof(int2)));
+    PTRY(poba::copy_sync(c, c.cta_tiles.p, cta.data(), n_cta * sizeof(int2), cudaMemcpyHostToDevice));
   }
   c.n_chunks = (int)chunks.size();
-  c.n_partials = n_u;
+  c.n_partials = (int)part_cam.size();
   c.max_slots = 0;
   for (auto& q : chunks) c.max_slots = std::max(c.max_slots, q.nslot);
-  if (c.max_slots > kSlotCap) return fail(POBA_EINVAL, "a single tile touches more cameras than the slot cap");
-  PTRY(c.chunks.alloc(chunks.size() * sizeof(Chunk)));
-  PCK(cudaMemcpyAsync(c.chunks.p, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice, s));
   c.chunks_host = chunks;
-  {  // one chunk per warp of the term kernel
-    std::vector<int4> wr(chunks.size());
-    for (size_t q = 0; q < chunks.size(); ++q)
-      wr[q] = make_int4(chunks[q].tile0, chunks[q].tile1, chunks[q].part0, chunks[q].nslot);
-    PTRY(c.work.alloc(wr.size() * sizeof(int4)));
-    PCK(cudaMemcpyAsync(c.work.p, wr.data(), wr.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-    c.n_work = (int)wr.size();
-  }
-
-  // camera -> partials (chunk order)
-  {
-    DBuf k1, k2, v1, v2, cnt;
-    PTRY(k1.alloc(n_u * 8));
-    PTRY(k2.alloc(n_u * 8));
-    PTRY(v1.alloc(n_u * 4));
-    PTRY(v2.alloc(n_u * 4));
-    PTRY(cnt.alloc((n_cam + 1) * 4));
-    PCK(cudaMemsetAsync(cnt.p, 0, (n_cam + 1) * 4, s));
-    const int bchunk = std::max(1, bitlen((uint64_t)chunks.size()));
-    k_part_keys<<<grid_for(n_u, B), B, 0, s>>>(ukey.as<uint64_t>(), n_u, bc, bchunk, k1.as<uint64_t>(),
-                                              v1.as<int>(), cnt.as<int>());
-    c.launches++;
-    PTRY(sort_pairs(c, k1.as<uint64_t>(), k2.as<uint64_t>(), v1.as<int>(), v2.as<int>(), n_u, bc + bchunk));
-    PTRY(c.part_idx.alloc(n_u * 4));
-    PCK(cudaMemcpyAsync(c.part_idx.p, v2.p, n_u * 4, cudaMemcpyDeviceToDevice, s));
-    PTRY(c.part_cam_off.alloc((n_cam + 1) * 4));
-    PTRY(excl_sum(c, cnt.as<int>(), c.part_cam_off.as<int>(), n_cam + 1));
-    PCK(cudaStreamSynchronize(s));  // scoped temporaries are freed below
-  }
-
-  // per-tile camera segments + tile-local permutation
-  {
-    const int bt = std::max(1, bitlen((uint64_t)c.n_tiles));
-    if (bt + bc + 8 > 63) return fail(POBA_EINVAL, "tile key exceeds 64 bits");
-    k_tile_cam_keys<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), bc, ka.as<uint64_t>());
-    PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
-    k_seg_flags<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, fl.as<int>());
-    PCK(cudaMemsetAsync(fl.as<int>() + nl, 0, 4, s));
-    PTRY(excl_sum(c, fl.as<int>(), pos.as<int>(), nl + 1));
-    c.launches += 2;
-    int nseg = 0;
-    PCK(cudaMemcpyAsync(&nseg, pos.as<int>() + nl, 4, cudaMemcpyDeviceToHost, s));
-    PCK(cudaStreamSynchronize(s));
-    c.n_segs = nseg;
-    PTRY(c.seg_start.alloc(ns));
-    PTRY(c.seg_slot.alloc(ns * 2));
-    PTRY(c.seg_obs.alloc(ns));
-    PTRY(c.seg_cam.alloc(ns * 4));
-    PCK(cudaMemsetAsync(c.seg_obs.p, 0, ns, s));
-    PCK(cudaMemsetAsync(c.seg_cam.p, 0, ns * 4, s));
-    PCK(cudaMemsetAsync(c.seg_start.p, 0, ns, s));
-    PCK(cudaMemsetAsync(c.seg_slot.p, 0, ns * 2, s));
-    k_segments<<<c.n_tiles, kTile, 0, s>>>(kb.as<uint64_t>(), fl.as<int>(), pos.as<int>(), c.tiles.as<Tile>(),
-                                       c.chunks.as<Chunk>(), ukey.as<uint64_t>(), bc, c.perm_s.as<uint8_t>(),
-                                       c.seg_start.as<uint8_t>(), c.seg_slot.as<uint16_t>(),
-                                       c.seg_obs.as<uint8_t>(), c.seg_cam.as<int>());
-    c.launches++;
-  }
-
-  // compact kernel descriptors (chunk bounds folded into the flags)
-  {
-    std::vector<Tile> tt(c.n_tiles);
-    PTRY(poba::copy_sync(c, tt.data(), c.tiles.p, c.n_tiles * sizeof(Tile), cudaMemcpyDeviceToHost));
+  PTRY(c.chunks.alloc(chunks.size() * sizeof(Chunk)));
+  PTRY(poba::copy_sync(c, c.chunks.p, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
+  PTRY(c.tiles.alloc(tiles.size() * sizeof(Tile)));
+  PTRY(poba::copy_sync(c, c.tiles.p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+  {  // compact kernel descriptors
     std::vector<TileK> tk(c.n_tiles);
     for (int i = 0; i < c.n_tiles; ++i) {
-      const Chunk& ch = chunks[tt[i].chunk];
-      TileK& k = tk[i];
-      k.n = tt[i].n;
-      k.lm0 = tt[i].lm0;
-      k.nlm = tt[i].nlm;
-      k.nseg = tt[i].nseg;
-      k.flags = tt[i].flags | (i == ch.tile0 ? kTileChunkFirst : 0) | (i + 1 == ch.tile1 ? kTileChunkLast : 0);
-      k.part0 = ch.part0;
-      k.nslot = ch.nslot;
-      k.chunk = tt[i].chunk;
+      const Chunk& ch = chunks[tiles[i].chunk];
+      tk[i] = TileK{tiles[i].n, tiles[i].lm0, tiles[i].nlm, tiles[i].flags, tiles[i].chunk, ch.part0, ch.nslot, 0};
     }
     PTRY(c.tilek.alloc(c.n_tiles * sizeof(TileK)));
     PTRY(poba::copy_sync(c, c.tilek.p, tk.data(), c.n_tiles * sizeof(TileK), cudaMemcpyHostToDevice));
   }
+  {  // camera -> partials, chunk order
+    const int n_u = c.n_partials;
+    std::vector<int> off(n_cam + 1, 0), idx(std::max(n_u, 1));
+    for (int p = 0; p < n_u; ++p) off[part_cam[p] + 1]++;
+    for (int64_t q = 0; q < n_cam; ++q) off[q + 1] += off[q];
+    std::vector<int> pos(off.begin(), off.end() - 1);
+    for (int p = 0; p < n_u; ++p) idx[pos[part_cam[p]]++] = p;
+    PTRY(c.part_idx.alloc(std::max(n_u, 1) * 4));
+    PTRY(poba::copy_sync(c, c.part_idx.p, idx.data(), std::max(n_u, 1) * 4, cudaMemcpyHostToDevice));
+    PTRY(c.part_cam_off.alloc((n_cam + 1) * 4));
+    PTRY(poba::copy_sync(c, c.part_cam_off.p, off.data(), (n_cam + 1) * 4, cudaMemcpyHostToDevice));
+  }
+  DBuf ka, kb;
+  PTRY(ka.alloc(ns * 8));
+  PTRY(kb.alloc(ns * 8));
 
   // camera-major permutation of slots for the U0 / b_p reduction
   {
@@ -734,10 +580,14 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PTRY(c.Rz.alloc((size_t)ns * 16));
   PCK(cudaMemsetAsync(c.J.p, 0, (size_t)kRow * ns * 16, s));
   PCK(cudaMemsetAsync(c.Rz.p, 0, (size_t)ns * 16, s));
-  k_pack_meta<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.perm_s.as<uint8_t>(),
-                                          c.lidx_s.as<uint8_t>(), c.seg_start.as<uint8_t>(),
-                                          c.seg_slot.as<uint16_t>(), c.seg_obs.as<uint8_t>(),
-                                          c.seg_cam.as<int>(), c.J.as<double2>());
+  {
+    DBuf dslot;
+    PTRY(dslot.alloc(ns * 4));
+    PCK(cudaMemcpyAsync(dslot.p, obs_slot.data(), ns * 4, cudaMemcpyHostToDevice, s));
+    k_pack_meta<<<c.n_tiles, kTile, 0, s>>>(c.cam_s.as<int>(), dslot.as<int>(), c.lidx_s.as<uint8_t>(),
+                                            c.J.as<double2>());
+    PCK(cudaStreamSynchronize(s));
+  }
   c.launches++;
   const int64_t nc = n_cam, nlm1 = std::max<int64_t>(nlm, 1);
   for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.bt, &c.xvec, &c.rvec})
