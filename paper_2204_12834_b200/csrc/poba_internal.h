@@ -34,7 +34,7 @@ constexpr int kTStride = 10;      // doubles per camera record of the term vecto
 // Term-kernel shared memory: per warp one bulk-copy stage (32 rows, the tile
 // descriptor, the V^-1 slice of its <= kTileLm landmarks) and the gathered
 // camera records of its tile; per CTA the chunk accumulator table (one 80-B
-// record per camera slot of the chunk) and the stage / turn barriers.
+// record per camera slot of the chunk), the stage barriers and the turn word.
 constexpr int kStRows = kTile * kRowBytes;                       // 6656
 constexpr int kStDesc = kStRows;                                 // 32-B tile descriptor
 constexpr int kStVinv = kStDesc + 32;                            // V^-1 slice
@@ -42,18 +42,19 @@ constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7456
 constexpr int kTRecBytes = kTStride * 8;                         // 80
 constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera records = 10016
 constexpr int kTermSmemMax = 227 * 1024;
-constexpr int kTermBars = 2 * kTermWarps * 8;                    // stage + turn barriers
-constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermBars) / kTRecBytes) / 32 * 32;
-constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermBars + kAccSlots * kTRecBytes;
+constexpr int kTermCtl = kTermWarps * 8 + 16;                    // stage barriers + turn word
+constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kTRecBytes) / 32 * 32;
+constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kTRecBytes;
 static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
 static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 
 // metadata word (row entry 12, as int4)
 struct RowMeta {
-  int cam;
   int slot;      // slot of the camera in the chunk accumulator table
-  int li;        // landmark index within the tile (0 for a long landmark's sub-tile)
+  int run;       // landmark index in the tile (bits 0-7; 0 for a long landmark's sub-tile),
+                 // first (8-15) and last (16-23) lane of the landmark's run
   int pad;
+  int cam;
 };
 
 // Error plumbing ---------------------------------------------------------------
@@ -141,12 +142,13 @@ struct Tile {
 };
 constexpr int kTileLong = 1;      // sub-tile of a landmark with k > kTile
 constexpr int kTileDupCam = 2;    // some camera appears twice in the tile
-constexpr int kTileChunkLast = 4; // last tile of its chunk: flush the accumulator table after it
+constexpr int kTileChunkLast = 4; // last tile of its chunk: write the partials after applying it
 
 // Compact per-tile descriptor streamed into the term kernel's stage (32 B).
 struct TileK {
   int n, lm0, nlm, flags;
-  int chunk, part0, nslot, pad;
+  int part0, nslot;  // the owning chunk's partials
+  int nx_n, nx_lm0;  // copy sizes of the same warp's next tile (n | nlm << 8), 0 if none
 };
 
 // A chunk: contiguous tiles of one CTA whose distinct cameras fit kAccSlots.

@@ -201,10 +201,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// named barriers 1..kTermWarps pass the apply turn between consecutive warps
+// (64 threads: the arriving warp and the waiting warp)
+__device__ __forceinline__ void turn_pass(int to_warp) {
+  asm volatile("bar.arrive %0, 64;" ::"r"(1 + to_warp) : "memory");
+}
+__device__ __forceinline__ void turn_wait(int warp) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + warp) : "memory");
 }
 
 struct TermArgs {
@@ -231,31 +235,31 @@ struct TermArgs {
 //   phase 2  z_l = V_l^-1 y_l on each landmark's last lane, shuffled back
 //   phase 3  g_o = J_p^T (J_l z_l), nine doubles in registers
 //   apply    g_o is added into the CTA's shared-memory accumulator record of
-//            its camera slot.  Tiles apply strictly in tile order (a turn
-//            barrier is passed from warp to warp), so every camera sum is
-//            formed in one fixed order: no atomics, bitwise reproducible.  A
-//            camera seen twice in one tile is pre-summed in lane order.
-// At the last tile of a chunk the table is written out once (one 80-B
-// partial per (chunk, camera)) and cleared for the next chunk.
+//            its camera slot.  Tiles apply strictly in tile order: the turn
+//            is passed from warp to warp through named barriers (arrive /
+//            sync pairs, no memory fences), so every camera sum is formed
+//            in one fixed order -- no atomics, bitwise reproducible.  A warp
+//            holds its tile's g_o in registers and applies it only after it
+//            has computed its NEXT tile, so the turn's round trip overlaps a
+//            whole tile of math.  A camera seen twice in one tile is
+//            pre-summed in lane order.
+// After the last tile of a chunk its warp writes the table out once (one 80-B
+// partial per (chunk, camera)) and clears it before passing the turn on.
 template <int MODE>
 __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (a.check_stop && a.st->stopped) return;
   const int2 range = a.cta_tiles[blockIdx.x];
-  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(smraw + kTermWarps * kWarpSmem);
-  uint64_t* turn_bar = stage_bar + kTermWarps;
-  double2* acc = reinterpret_cast<double2*>(smraw + kTermWarps * kWarpSmem + kTermBars);  // [kAccSlots][5]
+  uint8_t* ctl = smraw + kTermWarps * kWarpSmem;
+  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(ctl);
+  double2* acc = reinterpret_cast<double2*>(ctl + kTermCtl);                              // [kAccSlots][5]
   for (int k = threadIdx.x; k < kAccSlots * 5; k += blockDim.x) acc[k] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
-    for (int w = 0; w < kTermWarps; ++w) {
-      mbar_init(&stage_bar[w], 1);
-      mbar_init(&turn_bar[w], 1);
-    }
+    for (int w = 0; w < kTermWarps; ++w) mbar_init(&stage_bar[w], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0) mbar_arrive(&turn_bar[0]);  // the range's first tile applies first
   const int t_first = range.x + wid;
   if (t_first >= range.y) return;
   const int nq = (range.y - t_first + kTermWarps - 1) / kTermWarps;
@@ -264,12 +268,12 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   uint64_t* sbar = &stage_bar[wid];
   const uint64_t pol = policy_evict_first();
 
-  auto issue = [&](int ti, int4 d) {  // lane 0; d = (n, lm0, nlm, flags) of tile ti
-    const uint32_t vbytes = (MODE != kModeW) ? (uint32_t)(d.z * 48) : 0u;
-    mbar_expect_tx(sbar, (uint32_t)(d.x * kRowBytes + 32) + vbytes);
-    bulk_g2s_stream(stg, a.J + (int64_t)ti * kTile * kRow, (uint32_t)(d.x * kRowBytes), sbar, pol);
+  auto issue = [&](int ti, int n, int nlm, int lm0) {  // lane 0
+    const uint32_t vbytes = (MODE != kModeW) ? (uint32_t)(nlm * 48) : 0u;
+    mbar_expect_tx(sbar, (uint32_t)(n * kRowBytes + 32) + vbytes);
+    bulk_g2s_stream(stg, a.J + (int64_t)ti * kTile * kRow, (uint32_t)(n * kRowBytes), sbar, pol);
     bulk_g2s(stg + kStDesc, a.tk + ti, 32, sbar);
-    if (vbytes) bulk_g2s(stg + kStVinv, a.Vinv + (int64_t)d.y * 6, vbytes, sbar);
+    if (vbytes) bulk_g2s(stg + kStVinv, a.Vinv + (int64_t)lm0 * 6, vbytes, sbar);
   };
   auto gather = [&](int cam_lane, double2* tp) {  // 5 x 16-B pieces of the tile's 32 camera records
 #pragma unroll
@@ -279,10 +283,9 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
       tp[r] = reinterpret_cast<const double2*>(a.tin + (int64_t)cam * kTStride)[k % 5];
     }
   };
-  int4 dnext = make_int4(0, 0, 0, 0);
   if (lane == 0) {
-    issue(t_first, *reinterpret_cast<const int4*>(a.tk + t_first));
-    if (nq > 1) dnext = *reinterpret_cast<const int4*>(a.tk + t_first + kTermWarps);
+    const int4 d = *reinterpret_cast<const int4*>(a.tk + t_first);
+    issue(t_first, d.x, d.z, d.y);
   }
   double2 tp[5];
   int cam_next = 0;
@@ -293,6 +296,33 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     if (nq > 1) cam_next = a.cam_s[(int64_t)(t_first + kTermWarps) * kTile + lane];
   }
   __syncwarp();
+
+  // the previous tile's contributions, applied after this tile's math
+  double hg[9];
+  int h_slot = 0, h_ti = -1, h_flags = 0, h_part0 = 0, h_nslot = 0;
+  bool h_apply = false;
+  auto apply_held = [&]() {
+    if (h_ti != range.x) turn_wait(wid);
+    if (h_apply) {
+      double2* r = acc + h_slot * 5;
+      const double2 o0 = r[0], o1 = r[1], o2 = r[2], o3 = r[3], o4 = r[4];
+      r[0] = make_double2(o0.x + hg[0], o0.y + hg[1]);
+      r[1] = make_double2(o1.x + hg[2], o1.y + hg[3]);
+      r[2] = make_double2(o2.x + hg[4], o2.y + hg[5]);
+      r[3] = make_double2(o3.x + hg[6], o3.y + hg[7]);
+      r[4] = make_double2(o4.x + hg[8], o4.y);
+    }
+    __syncwarp();
+    if (h_flags & kTileChunkLast) {  // write the chunk's partials, clear the table
+      double2* out = reinterpret_cast<double2*>(a.partials) + (int64_t)h_part0 * 5;
+      for (int k = lane; k < h_nslot * 5; k += 32) {
+        out[k] = acc[k];
+        acc[k] = make_double2(0.0, 0.0);
+      }
+      __syncwarp();
+    }
+    if (h_ti + 1 < range.y) turn_pass((wid + 1) % kTermWarps);
+  };
 
   for (int q = 0; q < nq; ++q) {
     const int ti = t_first + q * kTermWarps;
@@ -305,19 +335,14 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     const bool valid = lane < t.n;
     const bool is_long = t.flags & kTileLong;
     const double2* row = reinterpret_cast<const double2*>(stg) + lane * kRow;
-    int slot = 0, li = 0;
-    if (valid) {
+    int slot = 0, li = 0, first = lane, last = lane;
+    if (valid) {  // one 16-B shared load: slot, landmark run
       const int4 mv = *reinterpret_cast<const int4*>(row + 12);
-      slot = mv.y;
-      li = mv.z;
+      slot = mv.x;
+      li = mv.y & 0xff;
+      first = (mv.y >> 8) & 0xff;
+      last = (mv.y >> 16) & 0xff;
     }
-    // landmark runs: heads, my run's first and last lane
-    const int prev_li = __shfl_up_sync(0xffffffffu, li, 1);
-    const bool head = valid && (lane == 0 || prev_li != li);
-    const unsigned heads = __ballot_sync(0xffffffffu, head) | (t.n < 32 ? (1u << t.n) : 0u);
-    const unsigned above = heads & ~((2u << lane) - 1u);
-    const int last = (above ? __ffs(above) - 1 : t.n) - 1;
-    const int first = 31 - __clz(heads & ((2u << lane) - 1u));
     const bool is_last = valid && lane == last;
     double vi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (MODE != kModeW && is_last && !(MODE == kModeTerm && is_long)) {
@@ -334,8 +359,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     for (int p = 0; p < kJPlanes; ++p) jr[p] = valid ? row[p] : make_double2(0.0, 0.0);
     __syncwarp();  // every lane is done with the stage: refill it with this warp's next tile
     if (lane == 0 && q + 1 < nq) {
-      issue(ti + kTermWarps, dnext);
-      if (q + 2 < nq) dnext = *reinterpret_cast<const int4*>(a.tk + ti + 2 * kTermWarps);
+      issue(ti + kTermWarps, t.nx_n & 0xff, t.nx_n >> 8, t.nx_lm0);
     }
     // phase 1
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;
@@ -418,32 +442,22 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
         pend &= pend - 1u;
       }
     }
-    mbar_wait(&turn_bar[wid], (uint32_t)(q & 1));
-    if (apply) {
-      double2* r = acc + slot * 5;
-      const double2 o0 = r[0], o1 = r[1], o2 = r[2], o3 = r[3], o4 = r[4];
-      r[0] = make_double2(o0.x + g[0], o0.y + g[1]);
-      r[1] = make_double2(o1.x + g[2], o1.y + g[3]);
-      r[2] = make_double2(o2.x + g[4], o2.y + g[5]);
-      r[3] = make_double2(o3.x + g[6], o3.y + g[7]);
-      r[4] = make_double2(o4.x + g[8], o4.y);
-    }
-    __syncwarp();
-    if (t.flags & kTileChunkLast) {  // write the chunk's partials, clear the table
-      double2* out = reinterpret_cast<double2*>(a.partials) + (int64_t)t.part0 * 5;
-      for (int k = lane; k < t.nslot * 5; k += 32) {
-        out[k] = acc[k];
-        acc[k] = make_double2(0.0, 0.0);
-      }
-      __syncwarp();
-    }
-    if (lane == 0 && ti + 1 < range.y) mbar_arrive(&turn_bar[(wid + 1) % kTermWarps]);
+    if (q > 0) apply_held();
+#pragma unroll
+    for (int j = 0; j < 9; ++j) hg[j] = g[j];
+    h_slot = slot;
+    h_apply = apply;
+    h_ti = ti;
+    h_flags = t.flags;
+    h_part0 = t.part0;
+    h_nslot = t.nslot;
     if (MODE == kModeTerm && q + 1 < nq) {
 #pragma unroll
       for (int r = 0; r < 5; ++r) ttab[32 * r + lane] = tp[r];
     }
     __syncwarp();
   }
+  apply_held();
 }
 
 // ---------------------------------------------------------------------------

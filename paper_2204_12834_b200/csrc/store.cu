@@ -116,15 +116,26 @@ __global__ void k_fill_i32(int* __restrict__ a, int64_t n, int v) {
   if (i < n) a[i] = v;
 }
 
-// metadata column (row entry 12) of every slot
-__global__ void k_pack_meta(const int* __restrict__ cam_s, const int* __restrict__ slot_s,
-                            const uint8_t* __restrict__ lidx_s, double2* __restrict__ J) {
-  const int64_t s = (int64_t)blockIdx.x * kTile + threadIdx.x;
+// metadata column (row entry 12) of every slot; one warp per tile
+__global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
+                            const int* __restrict__ slot_s, const uint8_t* __restrict__ lidx_s,
+                            double2* __restrict__ J) {
+  const Tile t = tiles[blockIdx.x];
+  const int lane = threadIdx.x;
+  const int64_t s = (int64_t)blockIdx.x * kTile + lane;
+  const bool valid = lane < t.n;
+  const int li = valid ? lidx_s[s] : -1;
+  const int prev = __shfl_up_sync(0xffffffffu, li, 1);
+  const bool head = valid && (lane == 0 || prev != li);
+  const unsigned heads = __ballot_sync(0xffffffffu, head) | (t.n < 32 ? (1u << t.n) : 0u);
+  const unsigned above = heads & ~((2u << lane) - 1u);
+  const int last = (above ? __ffs(above) - 1 : t.n) - 1;
+  const int first = 31 - __clz(heads & ((2u << lane) - 1u));
   RowMeta m;
-  m.cam = cam_s[s];
-  m.slot = slot_s[s];
-  m.li = lidx_s[s];
+  m.slot = valid ? slot_s[s] : 0;
   m.pad = 0;
+  m.run = valid ? (li | (first << 8) | (last << 16)) : 0;
+  m.cam = cam_s[s];
   *reinterpret_cast<RowMeta*>(J + s * kRow + 12) = m;
 }
 
@@ -528,9 +539,19 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PTRY(poba::copy_sync(c, c.tiles.p, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice));
   {  // compact kernel descriptors
     std::vector<TileK> tk(c.n_tiles);
+    std::vector<int> cta_end(c.n_tiles, 0);  // end of the CTA range holding each tile
+    {
+      std::vector<int2> cta(c.n_cta);
+      PTRY(poba::copy_sync(c, cta.data(), c.cta_tiles.p, c.n_cta * sizeof(int2), cudaMemcpyDeviceToHost));
+      for (const int2& r : cta)
+        for (int i = r.x; i < r.y; ++i) cta_end[i] = r.y;
+    }
     for (int i = 0; i < c.n_tiles; ++i) {
       const Chunk& ch = chunks[tiles[i].chunk];
-      tk[i] = TileK{tiles[i].n, tiles[i].lm0, tiles[i].nlm, tiles[i].flags, tiles[i].chunk, ch.part0, ch.nslot, 0};
+      const int nx = i + kTermWarps;
+      const bool has = nx < cta_end[i];
+      tk[i] = TileK{tiles[i].n, tiles[i].lm0, tiles[i].nlm, tiles[i].flags, ch.part0, ch.nslot,
+                    has ? (tiles[nx].n | (tiles[nx].nlm << 8)) : 0, has ? tiles[nx].lm0 : 0};
     }
     PTRY(c.tilek.alloc(c.n_tiles * sizeof(TileK)));
     PTRY(poba::copy_sync(c, c.tilek.p, tk.data(), c.n_tiles * sizeof(TileK), cudaMemcpyHostToDevice));
@@ -584,8 +605,8 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     DBuf dslot;
     PTRY(dslot.alloc(ns * 4));
     PCK(cudaMemcpyAsync(dslot.p, obs_slot.data(), ns * 4, cudaMemcpyHostToDevice, s));
-    k_pack_meta<<<c.n_tiles, kTile, 0, s>>>(c.cam_s.as<int>(), dslot.as<int>(), c.lidx_s.as<uint8_t>(),
-                                            c.J.as<double2>());
+    k_pack_meta<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), dslot.as<int>(),
+                                            c.lidx_s.as<uint8_t>(), c.J.as<double2>());
     PCK(cudaStreamSynchronize(s));
   }
   c.launches++;
