@@ -108,6 +108,29 @@ int poba_series_apply(poba_ctx* ctx, const double* v, int order, double* out);
  * this rank's landmarks are written).  nonzero: 1 if dx_p or dx_l != 0.      */
 int poba_back_substitute(poba_ctx* ctx, const double* delta_p, double* delta_l, int* nonzero);
 
+/* ---- PCG baselines on the same operators (solvers.py:30-118) --------------
+ * poba_schur_diagonal: the exact 9x9 diagonal blocks of S = U - W V^-1 W^T of
+ * the damped system (schur_diagonal_blocks, solvers.py:71-85), written as
+ * n_cam full row-major 9x9 blocks (nullable: only prepare the inverses).
+ * poba_pcg: preconditioned CG on S dx_p = -b_tilde (pcg, solvers.py:30-64)
+ * with the Schur-Jacobi preconditioner (pcg_schur_jacobi, solvers.py:98-102)
+ * or the order-`order` power-series preconditioner
+ * (pcg_power_series_preconditioner, solvers.py:105-118).  Stops when
+ * sqrt(r^T M^-1 r / r0^T M^-1 r0) < tol or after max_iter iterations.
+ * resume != 0 continues the previous solve for up to max_iter more
+ * iterations (the Python layer uses it to honour a per-iteration callback).
+ * rel_history (nullable, max_iter entries) receives the relative residual of
+ * each iteration of this call.  The solution also becomes the device-side
+ * delta_p used by poba_back_substitute(ctx, NULL, ...).
+ * POBA_ENOTSPD: "Schur diagonal blocks are not positive definite",
+ * "preconditioner is not positive definite", "reduced system is not positive
+ * definite" (the reference's asserts).                                      */
+#define POBA_PRECOND_SCHUR_JACOBI 1
+#define POBA_PRECOND_SERIES 2
+int poba_schur_diagonal(poba_ctx* ctx, double* blocks_81);
+int poba_pcg(poba_ctx* ctx, int precond, int order, double tol, int max_iter, int resume, double* delta_p,
+             int* iterations, double* final_rel, int* converged, double* rel_history);
+
 /* ---- K8: cost (lm.residual_cost, lm.py:107-119) ------------------------------
  * 0.5 sum ||r||^2 and the invalid count.  points NULL: device points, plus
  * the last back-substituted delta_l when trial != 0 (lm.apply_update,

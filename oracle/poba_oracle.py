@@ -392,6 +392,74 @@ def back_sub(system, delta_p):
     return -system.apply_v_inv(system.b_l + system.apply_wt(delta_p))
 
 
+def series_apply(system, v, order):
+    """power_series.py:80-91 (apply_series_inverse): x = sum_{i<=order} (U^-1 W V^-1 W^T)^i U^-1 v."""
+    if order < 0:
+        raise ValueError("order must be non-negative")
+    t = system.apply_u_inv(np.asarray(v, dtype=np.float64))
+    x = t.copy()
+    for _ in range(order):
+        t = system.apply_u_inv(system.apply_w(system.apply_v_inv(system.apply_wt(t))))
+        x += t
+    return x
+
+
+# ---------------------------------------------------------------------------
+# preconditioned CG baselines (solvers.py:30-118)
+# ---------------------------------------------------------------------------
+
+def schur_diagonal_blocks(system):
+    """solvers.py:71-85: U_c - sum_{o in c} W_o V_l^-1 W_o^T, W_o = J_p^T J_l (9x3)."""
+    M = system.U.copy()
+    for g, blk in system._views():
+        jp, jl = blk[..., 0:POSE], blk[..., POSE:POSE + POINT]
+        w_obs = _f64sum("gkai,gkaj->gkij", jp, jl)
+        tmp = _f64sum("gkij,gjl->gkil", w_obs, system.V_inv[g.lm_ids])
+        np.add.at(M, g.cam_ids, -_f64sum("gkil,gkjl->gkij", tmp, w_obs))
+    return M
+
+
+def schur_jacobi(system):
+    """solvers.py:88-95: block-Jacobi preconditioner from the exact 9x9 diagonal of S."""
+    m_inv = spd_inverse(schur_diagonal_blocks(system), "Schur diagonal")
+
+    def apply(v):
+        return _f64sum("pij,pj->pi", m_inv, np.asarray(v).reshape(system.n_cameras, POSE)).ravel()
+    return apply
+
+
+def pcg(system, apply_preconditioner, tol=1e-6, max_iter=500):
+    """solvers.py:30-64: PCG on S dx_p = -b_tilde.  Returns (delta_p, iterations, rel, converged, rels)."""
+    rhs = -system.b_tilde()
+    x = np.zeros_like(rhs)
+    if not np.any(rhs):
+        return x, 0, 0.0, True, []
+    r = rhs.copy()
+    z = apply_preconditioner(r)
+    rz = float(r @ z)
+    assert rz > 0, "preconditioner is not positive definite"
+    rz0 = rz
+    p = z
+    rel = 1.0
+    rels = []
+    for it in range(1, max_iter + 1):
+        sp = system.apply_schur(p)
+        psp = float(p @ sp)
+        assert psp > 0, "reduced system is not positive definite"
+        alpha = rz / psp
+        x = x + alpha * p
+        r = r - alpha * sp
+        z = apply_preconditioner(r)
+        rz_new = float(r @ z)
+        rel = np.sqrt(max(rz_new, 0.0) / rz0)
+        rels.append(rel)
+        if rel < tol:
+            return x, it, rel, True, rels
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, max_iter, rel, False, rels
+
+
 # ---------------------------------------------------------------------------
 # cost, retraction, LM loop (lm.py:107-144, 167-232)
 # ---------------------------------------------------------------------------
@@ -426,6 +494,7 @@ class OracleIter:
     order_m: int
     accepted: bool
     n_invalid: int
+    inner: int = 0
 
 
 @dataclass
@@ -438,8 +507,8 @@ class OracleTrace:
 def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
            max_outer_iterations=50, relative_function_tolerance=1e-6,
            epsilon=0.01, max_order=20, lambda_decrease=2.0, lambda_increase=4.0,
-           damping="marquardt", clock=None):
-    """lm.py:167-232 restricted to solver='poba', precision=64."""
+           damping="marquardt", clock=None, solver="poba", cg_tolerance=1e-6, cg_max_iterations=500):
+    """lm.py:167-232 for solver in {'poba', 'pcg', 'pcg-power'} (dispatch lm.py:147-164), precision=64."""
     import time
     clock = clock or time.perf_counter
     t0 = clock()
@@ -457,10 +526,21 @@ def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
         if lin is None:
             lin = linearize(cam_idx, pt_idx, pixels, cams, pts)
         sys_ = OracleSystem(lin, lam, damping)
-        dp, order, _ = series_solve(sys_, epsilon, max_order)
+        if solver == "poba":
+            dp, order, _ = series_solve(sys_, epsilon, max_order)
+            inner = order
+        elif solver == "pcg":
+            dp, inner, _, _, _ = pcg(sys_, schur_jacobi(sys_), cg_tolerance, cg_max_iterations)
+            order = 0
+        elif solver == "pcg-power":
+            dp, inner, _, _, _ = pcg(sys_, lambda v: series_apply(sys_, v, max_order), cg_tolerance,
+                                     cg_max_iterations)
+            order = max_order
+        else:
+            raise ValueError(f"unknown solver {solver!r}")
         dl = back_sub(sys_, dp)
         if not dp.any() and not dl.any():
-            tr.iterations.append(OracleIter(it, c, lam, order, True, lin.n_invalid))
+            tr.iterations.append(OracleIter(it, c, lam, order, True, lin.n_invalid, inner))
             tr.times.append(clock() - t0)
             tr.converged = True
             break
@@ -471,13 +551,13 @@ def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
             cams, pts, c = tc, tp, nc
             lam /= lambda_decrease
             lin = None
-            tr.iterations.append(OracleIter(it, c, lam, order, True, tbad))
+            tr.iterations.append(OracleIter(it, c, lam, order, True, tbad, inner))
             tr.times.append(clock() - t0)
             if rel < relative_function_tolerance:
                 tr.converged = True
                 break
         else:
             lam *= lambda_increase
-            tr.iterations.append(OracleIter(it, c, lam, order, False, tbad))
+            tr.iterations.append(OracleIter(it, c, lam, order, False, tbad, inner))
             tr.times.append(clock() - t0)
     return tr, cams, pts

@@ -11,5 +11,7 @@ from .lm import (BaState, LmConfig, SolverTrace, apply_update, evaluate_cost, re
 from .power_series import (PowerSeriesResult, apply_series_inverse, back_substitute,  # noqa: F401
                            power_series_solve, stop_criterion)
 from .problem import Problem  # noqa: F401
+from .solvers import (CgReport, make_schur_jacobi_preconditioner, pcg, pcg_power_series_preconditioner,  # noqa: F401
+                      pcg_schur_jacobi, schur_diagonal_blocks)
 
 __version__ = "0.1.0"

@@ -56,7 +56,12 @@ _SIGS = {
     "poba_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "poba_debug_counters": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "poba_shard_bounds": (ctypes.c_int, [ctypes.c_int64, _I64P, ctypes.c_int, _I64P]),
+    "poba_schur_diagonal": (ctypes.c_int, [_P, _DP]),
+    "poba_pcg": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, _DP,
+                                _IP, _DP, _IP, _DP]),
 }
+PRECOND_SCHUR_JACOBI, PRECOND_SERIES = 1, 2
+_ASSERT_MESSAGES = ("preconditioner is not positive definite", "reduced system is not positive definite")
 
 EXPORTED = tuple(_SIGS)
 
@@ -86,6 +91,8 @@ def _check(status):
     if status == POBA_OK:
         return
     msg = load().poba_last_error().decode(errors="replace")
+    if status == POBA_ENOTSPD and msg.startswith(_ASSERT_MESSAGES):
+        raise AssertionError(msg)  # the reference asserts these (solvers.py:47, 53)
     if status in (POBA_EINVAL, POBA_ENOTSPD, POBA_ENONFINITE, POBA_EVANISH):
         raise ValueError(msg)
     raise PobaError(f"libpoba status {status}: {msg}")
@@ -219,6 +226,21 @@ class Device:
         out = np.empty(9 * self.n_cam)
         _check(self._lib.poba_series_apply(self._h, _d(_f64(v)), int(order), _d(out)))
         return out
+
+    def schur_diagonal(self):
+        out = np.empty((self.n_cam, 9, 9))
+        _check(self._lib.poba_schur_diagonal(self._h, _d(out)))
+        return out
+
+    def pcg(self, precond, order, tol, max_iter, resume=False, want_history=False):
+        """Device PCG; returns (delta_p, iterations, final_rel, converged, rel_history)."""
+        dp = np.empty(9 * self.n_cam)
+        it, conv = ctypes.c_int(0), ctypes.c_int(0)
+        rel = ctypes.c_double(0.0)
+        hist = np.zeros(max(int(max_iter), 1)) if want_history else None
+        _check(self._lib.poba_pcg(self._h, int(precond), int(order), float(tol), int(max_iter), int(bool(resume)),
+                                  _d(dp), ctypes.byref(it), ctypes.byref(rel), ctypes.byref(conv), _d(hist)))
+        return dp, it.value, rel.value, bool(conv.value), hist
 
     def back_substitute(self, delta_p=None, want_delta_l=True):
         nz = ctypes.c_int(0)

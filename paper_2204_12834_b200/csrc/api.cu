@@ -349,6 +349,43 @@ int poba_series_apply(poba_ctx* ctx, const double* v, int order, double* out) {
   return POBA_OK;
 }
 
+int poba_schur_diagonal(poba_ctx* ctx, double* blocks_81) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  PTRY(poba::schur_diag_device(c, nullptr));
+  if (blocks_81) {
+    std::vector<double> m45(c.n_cam * 45);
+    PTRY(poba::copy_sync(c, m45.data(), c.Mbuf.p, m45.size() * 8, cudaMemcpyDeviceToHost));
+    for (int64_t q = 0; q < c.n_cam; ++q)
+      for (int i = 0, k = 0; i < 9; ++i)
+        for (int j = i; j < 9; ++j, ++k) {
+          blocks_81[q * 81 + i * 9 + j] = m45[q * 45 + k];
+          blocks_81[q * 81 + j * 9 + i] = m45[q * 45 + k];
+        }
+  }
+  return POBA_OK;
+}
+
+int poba_pcg(poba_ctx* ctx, int precond, int order, double tol, int max_iter, int resume, double* delta_p,
+             int* iterations, double* final_rel, int* converged, double* rel_history) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  NEED(precond == POBA_PRECOND_SCHUR_JACOBI || precond == POBA_PRECOND_SERIES, "unknown preconditioner");
+  if (precond == POBA_PRECOND_SERIES && order < 0) return poba::fail(POBA_EINVAL, "order must be non-negative");
+  NEED(max_iter >= 0, "max_iter must be non-negative");
+  NEED(iterations && final_rel && converged, "null outputs");
+  c.have_solution = false;
+  PTRY(poba::pcg_device(c, precond, order, tol, max_iter, resume != 0, delta_p, iterations, final_rel, converged,
+                        rel_history));
+  // the PCG iterate is the device-side delta_p for poba_back_substitute(ctx, NULL, ...)
+  PCK(cudaMemcpyAsync(c.xvec.p, c.pcg_vec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, c.stream));
+  PCK(cudaStreamSynchronize(c.stream));
+  c.have_solution = true;
+  return POBA_OK;
+}
+
 int poba_back_substitute(poba_ctx* ctx, const double* delta_p, double* delta_l, int* nonzero) {
   CTX_CHECK(ctx);
   Ctx& c = ctx->c;

@@ -158,6 +158,24 @@ struct Chunk {
   int nslot;         // distinct cameras (slots)
 };
 
+// An instantiated CUDA graph of one complete series solve (b_tilde + m terms,
+// device-side stop test), replayed while the problem's buffers stay put.
+struct SeriesGraph {
+  cudaGraphExec_t exec = nullptr;
+  double eps = 0;
+  int max_order = 0;
+  bool forced = false;
+  const void* ratios = nullptr;
+  int64_t launches = 0;
+};
+
+// host-side state of a (resumable) device PCG solve
+struct PcgState {
+  bool active = false;
+  int precond = 0, order = 0, it = 0;
+  double rz = 0, rz0 = 0, rel = 0;
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -253,6 +271,17 @@ struct Ctx {
   int last_order = 0;
 
   DBuf scratch_a, scratch_b, scratch_c;
+  DBuf Mbuf;         // double [n_cam*45] Schur diagonal blocks (PCG)
+  DBuf Minv;         // double [n_cam*45] their inverses
+  DBuf pcg_vec;      // double [5*9*n_cam] x, r, z, p, S p
+  PcgState pcg;
+  std::vector<SeriesGraph> graphs;
+  void drop_graphs() {
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
+  ~Ctx() { drop_graphs(); }
 };
 
 // ---- host-only planning (no GPU needed) ------------------------------------------
@@ -279,6 +308,9 @@ int cameras_prep(Ctx& c, const double* d_cams, double* d_prep);
 int allreduce_sum(Ctx& c, double* d_buf, size_t n);
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches);
 int b_tilde_device(Ctx& c);
+int schur_diag_device(Ctx& c, double* d_out45);
+int pcg_device(Ctx& c, int precond, int order, double tol, int max_iter, bool resume, double* h_delta_p,
+               int* iterations, double* final_rel, int* converged, double* rel_history);
 int points_accept_device(Ctx& c);
 
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }

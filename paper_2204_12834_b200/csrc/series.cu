@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   __syncwarp();
 
   // the previous tile's contributions, applied after this tile's math
-  double hg[9];
+  double hg[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   int h_slot = 0, h_ti = -1, h_flags = 0, h_part0 = 0, h_nslot = 0;
   bool h_apply = false;
   auto apply_held = [&]() {
@@ -942,9 +942,10 @@ int damp_device(Ctx& c, double lam, int identity) {
   return POBA_OK;
 }
 
-int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_used, int* converged) {
+// the launches of one series solve (b_tilde, t0, then max_order terms; every
+// kernel checks the device-side stop flag, so the sequence is fixed)
+int enqueue_series(Ctx& c, double eps, int max_order, bool forced) {
   cudaStream_t s = c.stream;
-  PTRY(ensure_ratios(c, max_order));
   PCK(cudaMemsetAsync(c.state.p, 0, sizeof(SeriesState), s));
   k_fill<<<grid_for(max_order + 1, 128), 128, 0, s>>>(c.ratios.as<double>(), max_order + 1,
                                                      std::numeric_limits<double>::quiet_NaN());
@@ -955,6 +956,46 @@ int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_use
   for (int i = 1; i <= max_order; ++i) {
     PTRY(launch_term(c, kModeTerm, c.tvec.as<double>(), nullptr, true));
     PTRY(launch_cam(c, kCamTerm, i, eps, !forced));
+  }
+  return POBA_OK;
+}
+
+int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_used, int* converged) {
+  cudaStream_t s = c.stream;
+  PTRY(ensure_ratios(c, max_order));
+  PTRY(configure_term(c));
+  if (c.nranks > 1 || getenv("POBA_NO_GRAPH")) {
+    PTRY(enqueue_series(c, eps, max_order, forced));
+  } else {  // single GPU: the whole solve is one CUDA graph, captured once per (eps, m)
+    SeriesGraph* g = nullptr;
+    for (auto& x : c.graphs)
+      if (x.eps == eps && x.max_order == max_order && x.forced == forced && x.ratios == c.ratios.p) g = &x;
+    if (!g) {
+      SeriesGraph ng;
+      ng.eps = eps;
+      ng.max_order = max_order;
+      ng.forced = forced;
+      ng.ratios = c.ratios.p;
+      const int64_t l0 = c.launches;
+      PCK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      const int st_enq = enqueue_series(c, eps, max_order, forced);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t e_end = cudaStreamEndCapture(s, &graph);
+      if (st_enq != POBA_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st_enq;
+      }
+      PCK(e_end);
+      const cudaError_t e_inst = cudaGraphInstantiate(&ng.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      PCK(e_inst);
+      ng.launches = c.launches - l0;
+      c.launches = l0;
+      c.graphs.push_back(ng);
+      g = &c.graphs.back();
+    }
+    PCK(cudaGraphLaunch(g->exec, s));
+    c.launches += g->launches;
   }
   SeriesState st;
   PCK(cudaMemcpyAsync(&st, c.state.p, sizeof(st), cudaMemcpyDeviceToHost, s));
@@ -1109,6 +1150,41 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
   }
   PCK(cudaGetLastError());
   return POBA_OK;
+}
+
+// S p = U p - W V^-1 W^T p (apply_schur, blocks.py:252-254) with ONE pass of the
+// fused term kernel: p (stride 9) -> 80-B records, term kernel + merge -> W V^-1 W^T p
+int schur_product_device(Ctx& c, const double* d_p, double* d_out) {
+  cudaStream_t s = c.stream;
+  const unsigned g = grid_for(c.n_cam * 9, 256);
+  k_restride<<<g, 256, 0, s>>>(d_p, 9, c.n_cam, c.tvec.as<double>(), kTStride);
+  c.launches++;
+  PTRY(launch_term(c, kModeTerm, c.tvec.as<double>(), nullptr, false));
+  PTRY(launch_cam(c, kCamMerge, 0, 0.0, false));
+  k_cam_mv<<<g, 256, 0, s>>>(c.Ud.as<double>(), d_p, c.n_cam, c.ctmp.as<double>());
+  k_axpy_sub<<<g, 256, 0, s>>>(c.ctmp.as<double>(), c.rvec.as<double>(), c.n_cam * 9, d_out);
+  c.launches += 2;
+  PCK(cudaGetLastError());
+  return POBA_OK;
+}
+
+// SPD inverse of 45-packed 9x9 blocks (the damped-U Cholesky path with no damping)
+int damp_u_blocks(Ctx& c, const double* M45, double* M45_copy, double* Minv45, const char* what) {
+  cudaStream_t s = c.stream;
+  int* fl = c.flag.as<int>() + 3;
+  PCK(cudaMemsetAsync(fl, 0, 4, s));
+  k_damp_u<<<grid_for(c.n_cam, 64), 64, 0, s>>>(M45, c.Dp.as<double>(), c.n_cam, 0.0, 1, M45_copy, Minv45, fl);
+  c.launches++;
+  PCK(cudaGetLastError());
+  int h = 0;
+  PTRY(copy_sync(c, &h, fl, 4, cudaMemcpyDeviceToHost));
+  if (h & 1) return fail(POBA_ENOTSPD, what);
+  return POBA_OK;
+}
+
+void launch_cam_mv(Ctx& c, const double* M45, const double* v, double* out) {
+  k_cam_mv<<<grid_for(c.n_cam * 9, 256), 256, 0, c.stream>>>(M45, v, c.n_cam, out);
+  c.launches++;
 }
 
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches) {

@@ -327,6 +327,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   if (n >= (1ll << 31) - 1 || n_pt >= (1ll << 31) - 1 || n_cam >= (1ll << 24))
     return fail(POBA_EINVAL, "problem too large for 32-bit observation indexing");
   c.have_order = false;
+  c.drop_graphs();
 
   // --- upload + validate indices, histograms ---------------------------------------
   DBuf cam64, pt64, kcam, flag;

@@ -26,7 +26,7 @@ sys.path.insert(0, REPO)
 sys.path.insert(0, os.path.join(os.path.dirname(REF), "tests"))
 
 import numpy as np  # noqa: E402
-from powerba import bal_io, blocks, lm, synthetic  # noqa: E402
+from powerba import bal_io, blocks, lm, solvers, synthetic  # noqa: E402
 from powerba.power_series import back_substitute, power_series_solve  # noqa: E402
 
 import helpers  # noqa: E402  (the reference's own test oracles: random_block_system)
@@ -149,7 +149,50 @@ def explicit_bundle():
     print("wrote explicit.npz")
 
 
+def pcg_bundle():
+    """Reference PCG baselines (solvers.py:30-118) on the c1 and noisy4x60 problems."""
+    from paper_2204_12834_b200 import configs
+    out = {}
+    probs = {"c1": configs.make_config("c1"),
+             "noisy": bal_io.perturb(synthetic.make_random_problem(4, 60, seed=5, pixel_noise=1.0), 0.01, seed=0)}
+    for tag, p in probs.items():
+        out[f"{tag}_fingerprint"] = np.array(
+            __import__("paper_2204_12834_b200.problem", fromlist=["Problem"]).Problem(**problem_arrays(p)).fingerprint())
+        lin = blocks.linearize(p)
+        for j, lam in enumerate([1e-4, 1.0]):
+            sys_ = lin.damp(lam)
+            pre = f"{tag}_l{j}_"
+            out[pre + "lam"] = np.array(lam)
+            out[pre + "schur_diag"] = solvers.schur_diagonal_blocks(sys_)
+            rels = []
+            rep = solvers.pcg_schur_jacobi(sys_, 1e-6, 500, callback=lambda it, x, rel: rels.append(rel))
+            out[pre + "jac_delta_p"], out[pre + "jac_iters"] = rep.delta_p, np.array(rep.iterations)
+            out[pre + "jac_rel"], out[pre + "jac_conv"] = np.array(rep.final_relative_residual), np.array(rep.converged)
+            out[pre + "jac_rels"] = np.array(rels)
+            for m in (0, 2):
+                rep = solvers.pcg_power_series_preconditioner(sys_, m, 1e-6, 500)
+                out[pre + f"pow{m}_delta_p"], out[pre + f"pow{m}_iters"] = rep.delta_p, np.array(rep.iterations)
+                out[pre + f"pow{m}_rel"] = np.array(rep.final_relative_residual)
+            rep = solvers.pcg_schur_jacobi(sys_, 1e-3, 3)
+            out[pre + "jac3_delta_p"], out[pre + "jac3_iters"] = rep.delta_p, np.array(rep.iterations)
+            out[pre + "jac3_conv"] = np.array(rep.converged)
+        for solver in ("pcg", "pcg-power"):
+            cfg = lm.LmConfig(solver=solver, max_outer_iterations=10, max_order=2)
+            tr = lm.run(p, cfg)
+            its = tr.iterations
+            t = f"{tag}_lm_{solver.replace('-', '_')}"
+            out[t + "_cost"] = np.array([i.cost for i in its])
+            out[t + "_lam"] = np.array([i.lam for i in its])
+            out[t + "_inner"] = np.array([i.inner_iterations for i in its])
+            out[t + "_order"] = np.array([i.order_m for i in its])
+            out[t + "_accepted"] = np.array([i.accepted for i in its])
+    np.savez_compressed(os.path.join(HERE, "pcg.npz"), **out)
+    print("wrote pcg.npz")
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[2] == "pcg":
+        return pcg_bundle()
     from paper_2204_12834_b200 import configs
     oracle = bal_io.perturb(synthetic.make_random_problem(3, 5, seed=1), 0.01, seed=0)
     bundle("rand3x5", oracle, lams=[1e-4, 1.0],
@@ -172,6 +215,7 @@ def main():
                                          epsilon=1e-6)},
            store=False, save_inputs=False)
     explicit_bundle()
+    pcg_bundle()
 
 
 if __name__ == "__main__":

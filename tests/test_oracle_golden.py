@@ -185,3 +185,48 @@ def test_pass_counts():
     s.passes = dict.fromkeys(s.passes, 0)
     O.series_solve(s, 1e-300, 6)
     assert (s.passes["w"], s.passes["wt"], s.passes["v_inv"], s.passes["u_inv"]) == (6, 6, 6, 7)
+
+
+# -- PCG baselines (reference solvers.py:30-118), pinned by tests/golden/pcg.npz ----------
+
+PCG_PROBLEMS = {"c1": "c1", "noisy": "noisy4x60"}
+
+
+@pytest.mark.parametrize("tag", sorted(PCG_PROBLEMS))
+def test_pcg_baselines_match_reference(tag):
+    p, _ = golden_problem(PCG_PROBLEMS[tag])
+    z = load_golden("pcg")
+    assert p.fingerprint() == str(z[f"{tag}_fingerprint"])
+    lin = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points)
+    for j in range(2):
+        pre = f"{tag}_l{j}_"
+        s = O.OracleSystem(lin, float(z[pre + "lam"]))
+        assert rel(O.schur_diagonal_blocks(s), z[pre + "schur_diag"]) < 1e-12
+        x, it, r, conv, rels = O.pcg(s, O.schur_jacobi(s), 1e-6, 500)
+        assert it == int(z[pre + "jac_iters"]) and conv == bool(z[pre + "jac_conv"])
+        assert rel(x, z[pre + "jac_delta_p"]) < 1e-10
+        np.testing.assert_allclose(rels, z[pre + "jac_rels"], rtol=1e-6)
+        for m in (0, 2):
+            x, it, r, conv, _ = O.pcg(s, lambda v: O.series_apply(s, v, m), 1e-6, 500)
+            assert it == int(z[pre + f"pow{m}_iters"])
+            assert rel(x, z[pre + f"pow{m}_delta_p"]) < 1e-10
+        x, it, r, conv, _ = O.pcg(s, O.schur_jacobi(s), 1e-3, 3)
+        assert it == int(z[pre + "jac3_iters"]) and conv == bool(z[pre + "jac3_conv"])
+        assert rel(x, z[pre + "jac3_delta_p"]) < 1e-10
+
+
+@pytest.mark.parametrize("tag", sorted(PCG_PROBLEMS))
+@pytest.mark.parametrize("solver", ["pcg", "pcg-power"])
+def test_pcg_lm_trace_matches_reference(tag, solver):
+    p, _ = golden_problem(PCG_PROBLEMS[tag])
+    z = load_golden("pcg")
+    t = f"{tag}_lm_{solver.replace('-', '_')}"
+    tr, _, _ = O.lm_run(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points,
+                        max_outer_iterations=10, max_order=2, solver=solver)
+    its = tr.iterations
+    assert len(its) == len(z[t + "_cost"])
+    np.testing.assert_allclose([i.cost for i in its], z[t + "_cost"], rtol=1e-10)
+    assert [i.inner for i in its][1:] == z[t + "_inner"].tolist()[1:]
+    assert [i.order_m for i in its][1:] == z[t + "_order"].tolist()[1:]
+    assert [i.accepted for i in its] == z[t + "_accepted"].tolist()
+    np.testing.assert_allclose([i.lam for i in its], z[t + "_lam"], rtol=0)

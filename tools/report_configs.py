@@ -1,0 +1,128 @@
+"""Per-config report: series throughput + roofline, and LM time-to-1%-cost.
+
+    python tools/report_configs.py --configs c1,c2,c3,c3m64,c4,c5 --ref c1,c2,c3 \
+        --out gpurun_out/configs.json
+
+For every config (seeded synthetic problem of BASELINE.json's shapes):
+  * terms/s and obs/s of the fused series term (device events, forced terms),
+    achieved algorithmic GB/s of the term kernel and its fraction of the
+    measured HBM peak (bench.kernel_bytes / term_bytes);
+  * a full LM run through paper_2204_12834_b200.lm.run (GPU path; wall clock
+    includes building the device store), and for the configs in --ref the
+    reference algorithm's LM (oracle.poba_oracle.lm_run, numpy, this host's
+    CPU) on the identical input;
+  * time to reach the 1% cost threshold f* + 0.01 (f0 - f*), with f* the
+    smallest final cost among the runs compared (evalkit.py:66-89).
+The oracle is used here only as the timed CPU baseline and cost checker.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+from bench import kernel_bytes, measured_peak, term_bytes  # noqa: E402
+
+
+def series_throughput(problem, lam, reps=20):
+    import paper_2204_12834_b200 as P
+    s = P.assemble(problem, lam=lam)
+    dev = s._dp.dev
+    info = dev.info()
+    P.power_series_solve(s, 1e-300, 4)
+    ms_term, ms_kernel, launches = dev.time_terms(reps)
+    n_o, n_l, n_c = problem.n_observations, problem.n_points, problem.n_cameras
+    peak, kind = measured_peak()
+    kb = kernel_bytes(n_o, n_l, n_c)
+    tb = term_bytes(n_o, n_l, n_c)
+    return {"terms_per_s": 1e3 / ms_term, "obs_per_s": n_o * 1e3 / ms_term, "ms_per_term": ms_term,
+            "ms_term_kernel": ms_kernel, "launches_per_term": launches,
+            "term_gbs": tb / (ms_term / 1e3) / 1e9, "term_frac": tb / (ms_term / 1e3) / 1e9 / peak,
+            "kernel_gbs": kb / (ms_kernel / 1e3) / 1e9, "kernel_frac": kb / (ms_kernel / 1e3) / 1e9 / peak,
+            "peak_gbs": peak, "peak_kind": kind, "n_chunks": info["n_chunks"], "n_partials": info["n_partials"],
+            "device_bytes": info["device_bytes"]}
+
+
+def gpu_lm(problem, st):
+    from paper_2204_12834_b200 import lm
+    cfg = lm.LmConfig(solver="poba", max_outer_iterations=st.max_outer_iterations, epsilon=st.epsilon,
+                      max_order=st.max_order, initial_lambda=st.initial_lambda)
+    t0 = time.perf_counter()
+    tr = lm.run(problem, cfg)
+    wall = time.perf_counter() - t0
+    return {"costs": [it.cost for it in tr.iterations], "times": [it.cumulative_time_s for it in tr.iterations],
+            "orders": [it.order_m for it in tr.iterations], "accepted": [it.accepted for it in tr.iterations],
+            "converged": tr.converged, "wall_s": wall}
+
+
+def ref_lm(problem, st):
+    from oracle import poba_oracle as O
+    t0 = time.perf_counter()
+    tr, _, _ = O.lm_run(problem.cam_indices, problem.pt_indices, problem.pixels, problem.camera_params, problem.points,
+                  initial_lambda=st.initial_lambda, max_outer_iterations=st.max_outer_iterations,
+                  epsilon=st.epsilon, max_order=st.max_order)
+    wall = time.perf_counter() - t0
+    return {"costs": [it.cost for it in tr.iterations], "times": list(tr.times),
+            "orders": [it.order_m for it in tr.iterations], "accepted": [it.accepted for it in tr.iterations],
+            "converged": tr.converged, "wall_s": wall}
+
+
+def time_to(run, thr):
+    for c, t in zip(run["costs"], run["times"]):
+        if c <= thr:
+            return t
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c1,c2,c3,c3m64,c4,c5")
+    ap.add_argument("--ref", default="c1,c2")
+    ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "configs.json"))
+    args = ap.parse_args()
+    from paper_2204_12834_b200 import configs
+    refs = set(x for x in args.ref.split(",") if x)
+    out = {"host_cpus": os.cpu_count(), "configs": {}}
+    for name in args.configs.split(","):
+        t = time.perf_counter()
+        problem = configs.make_config(name, 1.0, seed=0)
+        gen_s = time.perf_counter() - t
+        st = configs.LM_SETTINGS.get(name, configs.LmSettings())
+        rec = {"n_cameras": problem.n_cameras, "n_points": problem.n_points,
+               "n_observations": problem.n_observations, "gen_s": gen_s,
+               "lm_settings": {"max_outer_iterations": st.max_outer_iterations, "max_order": st.max_order,
+                               "epsilon": st.epsilon, "initial_lambda": st.initial_lambda}}
+        rec["series"] = series_throughput(problem, st.initial_lambda)
+        rec["gpu_lm"] = gpu_lm(problem, st)
+        runs = {"gpu": rec["gpu_lm"]}
+        if name in refs:
+            rec["ref_lm"] = ref_lm(problem, st)
+            runs["ref"] = rec["ref_lm"]
+            g, r = rec["gpu_lm"]["costs"], rec["ref_lm"]["costs"]
+            n = min(len(g), len(r))
+            rec["cost_rel_diff_per_iter"] = [abs(a - b) / abs(b) for a, b in zip(g[:n], r[:n])]
+        f0 = rec["gpu_lm"]["costs"][0]
+        f_star = min(r_["costs"][-1] for r_ in runs.values())
+        thr = f0 - 0.99 * (f0 - f_star)
+        rec["f0"], rec["f_star"], rec["threshold_1pct"] = f0, f_star, thr
+        rec["time_to_1pct_s"] = {k: time_to(v, thr) for k, v in runs.items()}
+        out["configs"][name] = rec
+        s = rec["series"]
+        print(f"{name}: obs {problem.n_observations} terms/s {s['terms_per_s']:.1f} kernel {s['kernel_gbs']:.0f} GB/s "
+              f"({100 * s['kernel_frac']:.1f}%) | LM gpu {rec['gpu_lm']['wall_s']:.2f}s final {rec['gpu_lm']['costs'][-1]:.6g}"
+              + (f" | ref {rec['ref_lm']['wall_s']:.1f}s final {rec['ref_lm']['costs'][-1]:.6g}" if name in refs else "")
+              + f" | t1% {rec['time_to_1pct_s']}", flush=True)
+        os.makedirs(os.path.dirname(args.out), exist_ok=True)
+        with open(args.out, "w") as fh:
+            json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
