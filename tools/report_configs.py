@@ -50,16 +50,16 @@ def series_throughput(problem, lam, reps=20):
             "device_bytes": info["device_bytes"]}
 
 
-def gpu_lm(problem, st):
+def gpu_lm(problem, st, solver="poba"):
     from paper_2204_12834_b200 import lm
-    cfg = lm.LmConfig(solver="poba", max_outer_iterations=st.max_outer_iterations, epsilon=st.epsilon,
+    cfg = lm.LmConfig(solver=solver, max_outer_iterations=st.max_outer_iterations, epsilon=st.epsilon,
                       max_order=st.max_order, initial_lambda=st.initial_lambda)
     t0 = time.perf_counter()
     tr = lm.run(problem, cfg)
     wall = time.perf_counter() - t0
     return {"costs": [it.cost for it in tr.iterations], "times": [it.cumulative_time_s for it in tr.iterations],
-            "orders": [it.order_m for it in tr.iterations], "accepted": [it.accepted for it in tr.iterations],
-            "converged": tr.converged, "wall_s": wall}
+            "orders": [it.order_m for it in tr.iterations], "inner": [it.inner_iterations for it in tr.iterations],
+            "accepted": [it.accepted for it in tr.iterations], "converged": tr.converged, "wall_s": wall}
 
 
 def ref_lm(problem, st):
@@ -85,6 +85,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1,c2,c3,c3m64,c4,c5")
     ap.add_argument("--ref", default="c1,c2")
+    ap.add_argument("--solvers", default="poba,pcg,pcg-power", help="GPU LM inner solvers to time")
     ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "configs.json"))
     args = ap.parse_args()
     from paper_2204_12834_b200 import configs
@@ -102,6 +103,11 @@ def main():
         rec["series"] = series_throughput(problem, st.initial_lambda)
         rec["gpu_lm"] = gpu_lm(problem, st)
         runs = {"gpu": rec["gpu_lm"]}
+        for solver in args.solvers.split(","):
+            if solver and solver != "poba":
+                key = "gpu_" + solver.replace("-", "_")
+                rec[key + "_lm"] = gpu_lm(problem, st, solver)
+                runs[key] = rec[key + "_lm"]
         if name in refs:
             rec["ref_lm"] = ref_lm(problem, st)
             runs["ref"] = rec["ref_lm"]
@@ -118,7 +124,8 @@ def main():
         print(f"{name}: obs {problem.n_observations} terms/s {s['terms_per_s']:.1f} kernel {s['kernel_gbs']:.0f} GB/s "
               f"({100 * s['kernel_frac']:.1f}%) | LM gpu {rec['gpu_lm']['wall_s']:.2f}s final {rec['gpu_lm']['costs'][-1]:.6g}"
               + (f" | ref {rec['ref_lm']['wall_s']:.1f}s final {rec['ref_lm']['costs'][-1]:.6g}" if name in refs else "")
-              + f" | t1% {rec['time_to_1pct_s']}", flush=True)
+              + f" | t1% {rec['time_to_1pct_s']} | finals "
+              + str({k: v["costs"][-1] for k, v in runs.items()}), flush=True)
         os.makedirs(os.path.dirname(args.out), exist_ok=True)
         with open(args.out, "w") as fh:
             json.dump(out, fh, indent=1)
