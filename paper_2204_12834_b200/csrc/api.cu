@@ -87,15 +87,44 @@ void unpack3(const double* p6, double* out9) {
   for (int q = 0; q < 9; ++q) out9[q] = p6[idx[q]];
 }
 
-// landmark arrays: this rank owns points [lm_lo, lm_hi); host arrays are full (n_pt rows)
+// landmark arrays: this rank owns file landmarks [lm_lo, lm_hi); host arrays are
+// full (n_pt rows, file order); the device keeps them in store order
+// (store j <-> file lm_lo + lm_perm[j]), permuted on the device.
+__global__ void k_lm_gather(const double* __restrict__ src, const int* __restrict__ perm, int64_t n, int width,
+                            double* __restrict__ dst) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n * width) return;
+  const int64_t j = q / width;
+  dst[q] = src[(int64_t)perm[j] * width + (q - j * width)];
+}
+__global__ void k_lm_scatter(const double* __restrict__ src, const int* __restrict__ perm, int64_t n, int width,
+                             double* __restrict__ dst) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n * width) return;
+  const int64_t j = q / width;
+  dst[(int64_t)perm[j] * width + (q - j * width)] = src[q];
+}
+
 int lm_upload(Ctx& c, const double* host_full, int width, double* d_local) {
   if (c.n_lm_l == 0) return POBA_OK;
-  PCK(cudaMemcpyAsync(d_local, host_full + c.lm_lo * width, c.n_lm_l * width * 8, cudaMemcpyHostToDevice, c.stream));
+  PTRY(c.lm_stage.alloc(c.n_lm_l * width * 8));
+  PCK(cudaMemcpyAsync(c.lm_stage.p, host_full + c.lm_lo * width, c.n_lm_l * width * 8, cudaMemcpyHostToDevice,
+                      c.stream));
+  k_lm_gather<<<grid_for(c.n_lm_l * width, 256), 256, 0, c.stream>>>(c.lm_stage.as<double>(), c.lm_perm.as<int>(),
+                                                                     c.n_lm_l, width, d_local);
+  c.launches++;
+  PCK(cudaGetLastError());
   return POBA_OK;
 }
 int lm_download(Ctx& c, const double* d_local, int width, double* host_full) {
   if (c.n_lm_l == 0) return POBA_OK;
-  PCK(cudaMemcpyAsync(host_full + c.lm_lo * width, d_local, c.n_lm_l * width * 8, cudaMemcpyDeviceToHost, c.stream));
+  PTRY(c.lm_stage.alloc(c.n_lm_l * width * 8));
+  k_lm_scatter<<<grid_for(c.n_lm_l * width, 256), 256, 0, c.stream>>>(d_local, c.lm_perm.as<int>(), c.n_lm_l, width,
+                                                                      c.lm_stage.as<double>());
+  c.launches++;
+  PCK(cudaGetLastError());
+  PCK(cudaMemcpyAsync(host_full + c.lm_lo * width, c.lm_stage.p, c.n_lm_l * width * 8, cudaMemcpyDeviceToHost,
+                      c.stream));
   PCK(cudaStreamSynchronize(c.stream));
   return POBA_OK;
 }
@@ -465,8 +494,9 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
   NEED(c.have_lin, "no linearization");
   std::vector<double> h;
   const int64_t nc = c.n_cam, nl = c.n_lm_l;
-  auto scatter_lm = [&](const std::vector<double>& src, int width) {
-    std::memcpy(dst + c.lm_lo * width, src.data(), nl * width * 8);
+  auto scatter_lm = [&](const std::vector<double>& src, int width) {  // store order -> file rows
+    for (int64_t j = 0; j < nl; ++j)
+      std::memcpy(dst + (c.lm_lo + c.lm_order_host[j]) * width, src.data() + j * width, width * 8);
   };
   auto lm_sym = [&](const DBuf& b) -> int {
     PTRY(poba::copy_down(c, b, nl * 6 * 8, h));

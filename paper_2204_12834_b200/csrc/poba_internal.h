@@ -30,6 +30,7 @@ constexpr int kBlockTiles = 8;    // warp-tiles per CTA in the streaming kernels
 constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
 constexpr int kJPlanes = 12;      // Jacobian column pairs per row
 constexpr int kTermWarps = 8;     // warps per CTA of the term kernel (one CTA per SM)
+constexpr int kPackWindow = 64;   // landmark lookahead of the tile packer
 constexpr int kTStride = 10;      // doubles per camera record of the term vector / partials (80 B, 16-B aligned)
 // Term-kernel shared memory: per warp one bulk-copy stage (32 rows, the tile
 // descriptor, the V^-1 slice of its <= kTileLm landmarks) and the gathered
@@ -212,6 +213,9 @@ struct Ctx {
   DBuf lidx_s;       // uint8 [n_slots] landmark index within its tile
   DBuf lm_slot0;     // int32 [n_lm_l] first slot of each local landmark
   DBuf lm_k;         // int32 [n_lm_l]
+  DBuf lm_perm;      // int32 [n_lm_l] store landmark j -> file-local landmark (lm_lo + lm_perm[j])
+  std::vector<int> lm_order_host;
+  DBuf lm_stage;     // double staging for landmark uploads/downloads (file order)
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
   DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
@@ -292,6 +296,7 @@ struct TilePlan {
   std::vector<int> lm_tile, lm_off_in_tile;
 };
 void plan_tiles(const int* k_per_point, int64_t n_pt, TilePlan& plan);
+void pack_landmarks(const int* k, int64_t n, int window, std::vector<Tile>& tiles, std::vector<int>& order);
 size_t shard_cut(const TilePlan& plan, int64_t n_obs, int r, int nranks);
 
 // ---- host-side orchestration entry points ---------------------------------------

@@ -268,6 +268,78 @@ size_t shard_cut(const TilePlan& plan, int64_t n_obs, int r, int nranks) {
   return lo;
 }
 
+// Host-only: pack one rank's landmarks (file-local 0..n-1) into warp-tiles with a
+// bounded lookahead.  Landmarks are taken in index order (spatial locality);
+// when the next one does not fit the open tile, the largest landmarks of the
+// next `window` that still fit are pulled forward first.  Returns the tiles
+// (lm0 in the new STORE numbering) and order[j] = file-local landmark at store
+// position j.  Long landmarks (k > kTile) span consecutive full sub-tiles.
+void pack_landmarks(const int* k, int64_t n, int window, std::vector<Tile>& tiles, std::vector<int>& order) {
+  tiles.clear();
+  order.clear();
+  order.reserve(n);
+  std::vector<char> used(n, 0);
+  int64_t obs = 0;
+  Tile cur{};
+  bool open = false;
+  auto place = [&](int64_t l) {
+    if (!open) {
+      cur = Tile{};
+      cur.obs0 = (int)obs;
+      cur.lm0 = (int)order.size();
+      open = true;
+    }
+    order.push_back((int)l);
+    used[l] = 1;
+    cur.n += k[l];
+    cur.nlm += 1;
+    obs += k[l];
+  };
+  auto close = [&]() {
+    if (open) tiles.push_back(cur);
+    open = false;
+  };
+  auto fill = [&](int64_t from) {  // best fit from the lookahead window
+    if (!open) return;
+    const int64_t to = std::min<int64_t>(n, from + window);
+    while (cur.n < kTile && cur.nlm < kTileLm) {
+      int64_t best = -1;
+      for (int64_t l = from; l < to; ++l)
+        if (!used[l] && k[l] <= kTile - cur.n && (best < 0 || k[l] > k[best])) best = l;
+      if (best < 0) break;
+      place(best);
+    }
+  };
+  for (int64_t l = 0; l < n; ++l) {
+    if (used[l]) continue;
+    const int kk = k[l];
+    if (kk > kTile) {
+      fill(l + 1);
+      close();
+      const int j = (int)order.size();
+      order.push_back((int)l);
+      used[l] = 1;
+      for (int sub = 0; sub < kk; sub += kTile) {
+        Tile t{};
+        t.obs0 = (int)(obs + sub);
+        t.n = std::min(kTile, kk - sub);
+        t.lm0 = j;
+        t.nlm = 1;
+        t.flags = kTileLong;
+        tiles.push_back(t);
+      }
+      obs += kk;
+      continue;
+    }
+    if (open && (cur.n + kk > kTile || cur.nlm >= kTileLm)) {
+      fill(l + 1);
+      close();
+    }
+    place(l);
+  }
+  close();
+}
+
 // Canonical (reference) order and k-groups, built on first export request.
 int build_canonical_order(Ctx& c) {
   if (c.have_order) return POBA_OK;
@@ -376,8 +448,6 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   plan_tiles(hk.data(), n_pt, plan);
   std::vector<int64_t>& lm_first = plan.lm_first;
   std::vector<Tile>& gt = plan.tiles;
-  std::vector<int>& lm_tile = plan.lm_tile;
-  std::vector<int>& lm_off_in_tile = plan.lm_off_in_tile;
   size_t t_lo = 0, t_hi = gt.size();
   if (c.nranks > 1) {
     t_lo = shard_cut(plan, n, c.rank, c.nranks);
@@ -389,34 +459,44 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   c.n_lm_l = c.lm_hi - c.lm_lo;
   const int64_t obs_lo = lm_first[c.lm_lo];
   c.n_obs_l = lm_first[c.lm_hi] - obs_lo;
-  std::vector<Tile> tiles(gt.begin() + t_lo, gt.begin() + t_hi);
+  // this rank's landmarks re-packed with lookahead; the device works in the
+  // resulting STORE landmark order (lm_order: store j -> file landmark lm_lo + lm_order[j])
+  std::vector<Tile> tiles;
+  pack_landmarks(hk.data() + c.lm_lo, c.n_lm_l, kPackWindow, tiles, c.lm_order_host);
   c.long_host.clear();
-  for (auto& t : tiles) {
-    t.obs0 -= (int)obs_lo;
-    t.lm0 -= (int)c.lm_lo;
+  for (auto& t : tiles)
     if ((t.flags & kTileLong) && (c.long_host.empty() || c.long_host.back() != t.lm0)) c.long_host.push_back(t.lm0);
-  }
   c.n_tiles = (int)tiles.size();
   c.n_long = (int)c.long_host.size();
   c.n_slots = (int64_t)c.n_tiles * kTile;
   const int64_t ns = c.n_slots, nl = c.n_obs_l, nlm = c.n_lm_l;
 
-  // --- per-landmark slot map ------------------------------------------------------------------
-  std::vector<int> h_slot0(nlm), h_first(nlm + 1), h_k(nlm);
-  std::vector<uint8_t> h_tidx(nlm);
-  for (int64_t j = 0; j < nlm; ++j) {
-    const int64_t g = c.lm_lo + j;
-    h_slot0[j] = (lm_tile[g] - (int)t_lo) * kTile + lm_off_in_tile[g];
-    h_first[j] = (int)(lm_first[g] - obs_lo);
-    h_k[j] = hk[g];
-    const Tile& t = tiles[lm_tile[g] - t_lo];
-    h_tidx[j] = (t.flags & kTileLong) ? 0 : (uint8_t)(j - t.lm0);
-  }
+  // --- per-landmark slot maps ------------------------------------------------------------------
+  // file-local (for placing the (pt, cam)-sorted observations) and store-local (kernels)
+  std::vector<int> f_slot0(nlm), h_first(nlm + 1), s_slot0(nlm), s_k(nlm);
+  std::vector<uint8_t> f_tidx(nlm);
+  for (int64_t j = 0; j < nlm; ++j) h_first[j] = (int)(lm_first[c.lm_lo + j] - obs_lo);
   h_first[nlm] = (int)nl;
+  for (int ti = 0; ti < c.n_tiles; ++ti) {
+    const Tile& t = tiles[ti];
+    if ((t.flags & kTileLong) && ti > 0 && (tiles[ti - 1].flags & kTileLong) && tiles[ti - 1].lm0 == t.lm0) continue;
+    int off = 0;
+    for (int q = 0; q < t.nlm; ++q) {
+      const int j = t.lm0 + q;
+      const int l = c.lm_order_host[j];
+      f_slot0[l] = ti * kTile + off;
+      f_tidx[l] = (t.flags & kTileLong) ? 0 : (uint8_t)q;
+      s_slot0[j] = f_slot0[l];
+      s_k[j] = hk[c.lm_lo + l];
+      off += s_k[j];
+    }
+  }
   PTRY(c.lm_slot0.alloc(std::max<int64_t>(nlm, 1) * 4));
   PTRY(c.lm_k.alloc(std::max<int64_t>(nlm, 1) * 4));
-  PCK(cudaMemcpyAsync(c.lm_slot0.p, h_slot0.data(), nlm * 4, cudaMemcpyHostToDevice, s));
-  PCK(cudaMemcpyAsync(c.lm_k.p, h_k.data(), nlm * 4, cudaMemcpyHostToDevice, s));
+  PTRY(c.lm_perm.alloc(std::max<int64_t>(nlm, 1) * 4));
+  PCK(cudaMemcpyAsync(c.lm_slot0.p, s_slot0.data(), nlm * 4, cudaMemcpyHostToDevice, s));
+  PCK(cudaMemcpyAsync(c.lm_k.p, s_k.data(), nlm * 4, cudaMemcpyHostToDevice, s));
+  PCK(cudaMemcpyAsync(c.lm_perm.p, c.lm_order_host.data(), nlm * 4, cudaMemcpyHostToDevice, s));
   if (c.n_long) {
     PTRY(c.long_lm.alloc(c.n_long * 4));
     PCK(cudaMemcpyAsync(c.long_lm.p, c.long_host.data(), c.n_long * 4, cudaMemcpyHostToDevice, s));
@@ -433,7 +513,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PCK(cudaMemsetAsync(c.lidx_s.p, 0, ns, s));
   c.launches++;
   {
-    DBuf ka, kb, va, vb, pixf, dfirst, dtidx;
+    DBuf ka, kb, va, vb, pixf, dfirst, dtidx, dslot0;
     PTRY(ka.alloc(n * 8));
     PTRY(kb.alloc(n * 8));
     PTRY(va.alloc(n * 4));
@@ -449,9 +529,11 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PTRY(dfirst.alloc((nlm + 1) * 4));
     PTRY(dtidx.alloc(std::max<int64_t>(nlm, 1)));
     PCK(cudaMemcpyAsync(dfirst.p, h_first.data(), (nlm + 1) * 4, cudaMemcpyHostToDevice, s));
-    PCK(cudaMemcpyAsync(dtidx.p, h_tidx.data(), nlm, cudaMemcpyHostToDevice, s));
+    PTRY(dslot0.alloc(std::max<int64_t>(nlm, 1) * 4));
+    PCK(cudaMemcpyAsync(dtidx.p, f_tidx.data(), nlm, cudaMemcpyHostToDevice, s));
+    PCK(cudaMemcpyAsync(dslot0.p, f_slot0.data(), nlm * 4, cudaMemcpyHostToDevice, s));
     k_fill_slots<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), vb.as<int>(), obs_lo, nl, bc, c.lm_lo,
-                                              dfirst.as<int>(), c.lm_slot0.as<int>(), dtidx.as<uint8_t>(),
+                                              dfirst.as<int>(), dslot0.as<int>(), dtidx.as<uint8_t>(),
                                               h_pix ? pixf.as<double2>() : nullptr, c.cam_s.as<int>(),
                                               c.file_s.as<int>(), c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>());
     c.launches++;
