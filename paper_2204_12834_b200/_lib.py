@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpoba.so")
+LIB_PATH = os.environ.get("POBA_LIB") or os.path.join(_HERE, "lib", "libpoba.so")  # POBA_LIB: A/B builds
 
 POBA_OK, POBA_EINVAL, POBA_ENOTSPD, POBA_ENONFINITE, POBA_ECUDA, POBA_ENCCL, POBA_EVANISH = range(7)
 OP_W, OP_WT, OP_U_INV, OP_V_INV, OP_U, OP_SCHUR = range(6)

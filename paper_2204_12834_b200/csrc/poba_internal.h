@@ -41,7 +41,7 @@ constexpr int kStDesc = kStRows;                                 // 32-B tile de
 constexpr int kStVinv = kStDesc + 32;                            // V^-1 slice
 constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7456
 constexpr int kTRecBytes = kTStride * 8;                         // 80
-constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera records = 10016
+constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera-record table = 10016
 constexpr int kTermSmemMax = 227 * 1024;
 constexpr int kTermCtl = kTermWarps * 8 + 16;                    // stage barriers + turn word
 constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kTRecBytes) / 32 * 32;
@@ -144,6 +144,7 @@ struct Tile {
 constexpr int kTileLong = 1;      // sub-tile of a landmark with k > kTile
 constexpr int kTileDupCam = 2;    // some camera appears twice in the tile
 constexpr int kTileChunkLast = 4; // last tile of its chunk: write the partials after applying it
+constexpr int kTileScanShift = 8; // bits 8-10: segmented-scan steps, ceil(log2(longest landmark run))
 
 // Compact per-tile descriptor streamed into the term kernel's stage (32 B).
 struct TileK {

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   if (t_first >= range.y) return;
   const int nq = (range.y - t_first + kTermWarps - 1) / kTermWarps;
   uint8_t* stg = smraw + wid * kWarpSmem;
-  double2* ttab = reinterpret_cast<double2*>(stg + kStageBytes);  // [32 observations][5]
+  double2* ttab = reinterpret_cast<double2*>(stg + kStageBytes);  // [32 observations][5] camera records
   uint64_t* sbar = &stage_bar[wid];
   const uint64_t pol = policy_evict_first();
 
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     const int4 d = *reinterpret_cast<const int4*>(a.tk + t_first);
     issue(t_first, d.x, d.z, d.y);
   }
-  double2 tp[5];
+  double2 tp[5];  // camera-record pieces of the next tile, in flight (five lanes per 80-B record)
   int cam_next = 0;
   if (MODE == kModeTerm) {
     gather(a.cam_s[(int64_t)t_first * kTile + lane], tp);
@@ -361,17 +361,19 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     if (lane == 0 && q + 1 < nq) {
       issue(ti + kTermWarps, t.nx_n & 0xff, t.nx_n >> 8, t.nx_lm0);
     }
-    // phase 1
-    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
-    if (MODE == kModeTerm && valid && !is_long) {
-      const double2* tr = ttab + lane * 5;
-      double tc[10];
+    // phase 1: this lane's camera record from the warp's record table (filled
+    // at the end of the previous tile)
+    double tc[10];
+    if (MODE == kModeTerm) {
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
-        const double2 v = tr[p];
+        const double2 v = ttab[lane * 5 + p];
         tc[2 * p] = v.x;
         tc[2 * p + 1] = v.y;
       }
+    }
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+    if (MODE == kModeTerm && valid && !is_long) {
       double u0 = 0.0, u1 = 0.0;
 #pragma unroll
       for (int j = 0; j < 9; ++j) {
@@ -383,8 +385,10 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
       w2 = fma(jr[11].x, u0, jr[11].y * u1);
     }
     if (MODE == kModeTerm) {
+      const int steps = (t.flags >> kTileScanShift) & 7;  // ceil(log2(longest landmark run of the tile))
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
+      for (int i = 0, d = 1; i < 5; ++i, d <<= 1) {
+        if (i >= steps) break;
         const double o0 = __shfl_up_sync(0xffffffffu, w0, d);
         const double o1 = __shfl_up_sync(0xffffffffu, w1, d);
         const double o2 = __shfl_up_sync(0xffffffffu, w2, d);

@@ -464,8 +464,16 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   std::vector<Tile> tiles;
   pack_landmarks(hk.data() + c.lm_lo, c.n_lm_l, kPackWindow, tiles, c.lm_order_host);
   c.long_host.clear();
-  for (auto& t : tiles)
+  for (auto& t : tiles) {
     if ((t.flags & kTileLong) && (c.long_host.empty() || c.long_host.back() != t.lm0)) c.long_host.push_back(t.lm0);
+    if (!(t.flags & kTileLong)) {  // segmented-scan depth for the tile's longest landmark
+      int kmax = 1;
+      for (int q = 0; q < t.nlm; ++q) kmax = std::max(kmax, hk[c.lm_lo + c.lm_order_host[t.lm0 + q]]);
+      int steps = 0;
+      while ((1 << steps) < kmax) ++steps;
+      t.flags |= steps << kTileScanShift;
+    }
+  }
   c.n_tiles = (int)tiles.size();
   c.n_long = (int)c.long_host.size();
   c.n_slots = (int64_t)c.n_tiles * kTile;
