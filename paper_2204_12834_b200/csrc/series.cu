@@ -700,21 +700,24 @@ k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ c
   }
 }
 
-constexpr int kLongThreads = 256;
+// Landmarks with k > kTile: one warp per landmark, lanes stride its
+// observations, fixed-shape butterfly for the landmark sum.
+constexpr int kLongWarps = 8;
+constexpr int kLongThreads = kLongWarps * 32;
 
 template <int OUT>
 __global__ void __launch_bounds__(kLongThreads)
-k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, const int* __restrict__ lm_k,
+k_wt_long(const int* __restrict__ long_lm, int n_long, const int* __restrict__ lm_slot0, const int* __restrict__ lm_k,
           const int* __restrict__ cam_s, const double2* __restrict__ J, int ts, const double* __restrict__ tin,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag, const SeriesState* __restrict__ st, int check_stop) {
-  __shared__ double red[kLongThreads][3];
   if (check_stop && st->stopped) return;
-  const int lm = long_lm[blockIdx.x];
+  const int w = blockIdx.x * kLongWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= n_long) return;
+  const int lm = long_lm[w];
   const int o0 = lm_slot0[lm], o1 = o0 + lm_k[lm];
-  const int tid = threadIdx.x;
   double y0 = 0.0, y1 = 0.0, y2 = 0.0;
-  for (int o = o0 + tid; o < o1; o += kLongThreads) {
+  for (int o = o0 + lane; o < o1; o += 32) {
     const double* tv = tin + (int64_t)cam_s[o] * ts;
     const double2* row = J + (int64_t)o * kRow;
     double u0 = 0.0, u1 = 0.0;
@@ -729,17 +732,14 @@ k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, con
     y1 += fma(b.x, u0, b.y * u1);
     y2 += fma(c.x, u0, c.y * u1);
   }
-  red[tid][0] = y0;
-  red[tid][1] = y1;
-  red[tid][2] = y2;
-  __syncthreads();
-  for (int s = kLongThreads / 2; s; s >>= 1) {
-    if (tid < s)
-      for (int k = 0; k < 3; ++k) red[tid][k] += red[tid + s][k];
-    __syncthreads();
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    y0 += __shfl_xor_sync(0xffffffffu, y0, d);
+    y1 += __shfl_xor_sync(0xffffffffu, y1, d);
+    y2 += __shfl_xor_sync(0xffffffffu, y2, d);
   }
-  if (tid == 0) {
-    double y[3] = {red[0][0], red[0][1], red[0][2]}, z[3];
+  if (lane == 0) {
+    double y[3] = {y0, y1, y2}, z[3];
     if (OUT == kOutWt) {
       z[0] = y[0]; z[1] = y[1]; z[2] = y[2];
     } else if (OUT == kOutZ) {
@@ -755,7 +755,6 @@ k_wt_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0, con
     out[lm * 3 + 2] = z[2];
   }
 }
-
 
 // elementwise block-diagonal products
 __global__ void k_cam_mv(const double* __restrict__ M45, const double* __restrict__ v, int64_t n_cam,
@@ -857,8 +856,8 @@ int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool ch
   const unsigned grid = (unsigned)c.n_cta;
   if (mode == kModeTerm) {
     if (c.n_long) {
-      k_wt_long<kOutZ><<<c.n_long, kLongThreads, 0, c.stream>>>(
-          c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.as<double2>(),
+      k_wt_long<kOutZ><<<grid_for(c.n_long, kLongWarps), kLongThreads, 0, c.stream>>>(
+          c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.as<double2>(),
           kTStride, tin, nullptr, c.Vinv.as<double>(), c.ltmp.as<double>(), nullptr, c.state.as<SeriesState>(),
           check_stop ? 1 : 0);
       c.launches++;
@@ -1080,7 +1079,7 @@ int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero) {
       c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl);
   c.launches++;
   if (c.n_long) {
-    k_wt_long<kOutBack><<<c.n_long, kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
+    k_wt_long<kOutBack><<<grid_for(c.n_long, kLongWarps), kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(), c.lm_k.as<int>(),
                                                    c.cam_s.as<int>(), c.J.as<double2>(), 9, d_dp,
                                                    c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl,
                                                    c.state.as<SeriesState>(), 0);
@@ -1118,7 +1117,7 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
           nullptr, d_out, nullptr);
       c.launches++;
       if (c.n_long) {
-        k_wt_long<kOutWt><<<c.n_long, kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
+        k_wt_long<kOutWt><<<grid_for(c.n_long, kLongWarps), kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(), c.lm_k.as<int>(),
                                                      c.cam_s.as<int>(), c.J.as<double2>(), 9, d_in, nullptr,
                                                      nullptr, d_out, nullptr, c.state.as<SeriesState>(), 0);
         c.launches++;
