@@ -192,7 +192,10 @@ class Device:
         _check(self._lib.poba_set_points(self._h, _d(_f64(points, (self.n_pt, 3)))))
 
     def get_points(self, base=None):
-        out = np.zeros((self.n_pt, 3)) if base is None else np.array(base, dtype=np.float64, copy=True)
+        if base is not None:
+            out = np.array(base, dtype=np.float64, copy=True)
+        else:  # a shard fills only its own rows
+            out = np.zeros((self.n_pt, 3)) if self.nranks > 1 else np.empty((self.n_pt, 3))
         _check(self._lib.poba_get_points(self._h, _d(out)))
         return out
 
@@ -244,7 +247,9 @@ class Device:
 
     def back_substitute(self, delta_p=None, want_delta_l=True):
         nz = ctypes.c_int(0)
-        dl = np.zeros(3 * self.n_pt) if want_delta_l else None
+        dl = None
+        if want_delta_l:  # a shard fills only its own rows
+            dl = np.zeros(3 * self.n_pt) if self.nranks > 1 else np.empty(3 * self.n_pt)
         dp = None if delta_p is None else _f64(delta_p)
         _check(self._lib.poba_back_substitute(self._h, _d(dp), _d(dl), ctypes.byref(nz)))
         return dl, bool(nz.value)

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <dlfcn.h>
@@ -105,11 +106,75 @@ __global__ void k_lm_scatter(const double* __restrict__ src, const int* __restri
   dst[(int64_t)perm[j] * width + (q - j * width)] = src[q];
 }
 
+// Large host<->device copies of pageable memory go through a pinned staging
+// buffer owned by the context and a few host threads (CUDA's own pageable path
+// runs at a few GB/s); pinned user memory is copied directly.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kChunk = 8u << 20;
+  const int nt = (int)std::min<size_t>(8, (bytes + kChunk - 1) / kChunk);
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const size_t o = (size_t)t * per;
+    if (o >= bytes) break;
+    th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, std::min(per, bytes - o)); });
+  }
+  for (auto& x : th) x.join();
+}
+
+int pinned_stage(Ctx& c, size_t bytes) {
+  if (c.host_stage_bytes >= bytes) return POBA_OK;
+  if (c.host_stage) cudaFreeHost(c.host_stage);
+  c.host_stage = nullptr;
+  c.host_stage_bytes = 0;
+  PCK(cudaHostAlloc(&c.host_stage, bytes, cudaHostAllocDefault));
+  c.host_stage_bytes = bytes;
+  return POBA_OK;
+}
+
+int host_to_device(Ctx& c, void* d_dst, const void* h_src, size_t bytes) {
+  if (bytes < (4u << 20) || is_pinned(h_src)) {
+    PCK(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, c.stream));
+    return POBA_OK;
+  }
+  PCK(cudaStreamSynchronize(c.stream));  // the staging buffer may still feed an earlier copy
+  PTRY(pinned_stage(c, bytes));
+  par_memcpy(c.host_stage, h_src, bytes);
+  PCK(cudaMemcpyAsync(d_dst, c.host_stage, bytes, cudaMemcpyHostToDevice, c.stream));
+  PCK(cudaStreamSynchronize(c.stream));
+  return POBA_OK;
+}
+
+int device_to_host(Ctx& c, void* h_dst, const void* d_src, size_t bytes) {
+  if (bytes < (4u << 20) || is_pinned(h_dst)) {
+    PCK(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, c.stream));
+    PCK(cudaStreamSynchronize(c.stream));
+    return POBA_OK;
+  }
+  PTRY(pinned_stage(c, bytes));
+  PCK(cudaMemcpyAsync(c.host_stage, d_src, bytes, cudaMemcpyDeviceToHost, c.stream));
+  PCK(cudaStreamSynchronize(c.stream));
+  par_memcpy(h_dst, c.host_stage, bytes);
+  return POBA_OK;
+}
+
 int lm_upload(Ctx& c, const double* host_full, int width, double* d_local) {
   if (c.n_lm_l == 0) return POBA_OK;
   PTRY(c.lm_stage.alloc(c.n_lm_l * width * 8));
-  PCK(cudaMemcpyAsync(c.lm_stage.p, host_full + c.lm_lo * width, c.n_lm_l * width * 8, cudaMemcpyHostToDevice,
-                      c.stream));
+  PTRY(host_to_device(c, c.lm_stage.p, host_full + c.lm_lo * width, c.n_lm_l * width * 8));
   k_lm_gather<<<grid_for(c.n_lm_l * width, 256), 256, 0, c.stream>>>(c.lm_stage.as<double>(), c.lm_perm.as<int>(),
                                                                      c.n_lm_l, width, d_local);
   c.launches++;
@@ -123,10 +188,7 @@ int lm_download(Ctx& c, const double* d_local, int width, double* host_full) {
                                                                       c.lm_stage.as<double>());
   c.launches++;
   PCK(cudaGetLastError());
-  PCK(cudaMemcpyAsync(host_full + c.lm_lo * width, c.lm_stage.p, c.n_lm_l * width * 8, cudaMemcpyDeviceToHost,
-                      c.stream));
-  PCK(cudaStreamSynchronize(c.stream));
-  return POBA_OK;
+  return device_to_host(c, host_full + c.lm_lo * width, c.lm_stage.p, c.n_lm_l * width * 8);
 }
 
 int copy_down(Ctx& c, const DBuf& src, size_t bytes, std::vector<double>& out) {

@@ -217,6 +217,8 @@ struct Ctx {
   DBuf lm_perm;      // int32 [n_lm_l] store landmark j -> file-local landmark (lm_lo + lm_perm[j])
   std::vector<int> lm_order_host;
   DBuf lm_stage;     // double staging for landmark uploads/downloads (file order)
+  void* host_stage = nullptr;  // pinned host staging for large pageable copies
+  size_t host_stage_bytes = 0;
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
   DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
@@ -286,7 +288,10 @@ struct Ctx {
       if (g.exec) cudaGraphExecDestroy(g.exec);
     graphs.clear();
   }
-  ~Ctx() { drop_graphs(); }
+  ~Ctx() {
+    drop_graphs();
+    if (host_stage) cudaFreeHost(host_stage);
+  }
 };
 
 // ---- host-only planning (no GPU needed) ------------------------------------------
