@@ -274,6 +274,34 @@ def make_corridor(n_cameras=1200, n_points=160_000, seed=0, window=30, extra_tra
 # C4: camera clusters on a sphere, heavy-tailed tracks, outliers
 # ---------------------------------------------------------------------------
 
+def make_mixed_tracks(n_cameras=72, n_points=400, seed=0, radius=10.0, name="mixed"):
+    """Test problem with every track-length regime of the store: k = 1 (single
+    observation), short tracks packed many to a warp-tile, and long tracks
+    (k > 32) that span several sub-tiles.  Ring of cameras looking at the
+    origin, points ~ N(0, 0.5^2 I), 1 px noise, the usual perturbation."""
+    rng = np.random.default_rng(seed)
+    ang = 2.0 * np.pi * np.arange(n_cameras) / n_cameras
+    centers = np.stack([radius * np.cos(ang), radius * np.sin(ang), rng.uniform(-1, 1, n_cameras)], axis=1)
+    R = _frames(centers, -centers)
+    cams = _cameras(centers, R, rng)
+    X = rng.normal(0.0, 0.5, (n_points, 3))
+    P = np.einsum("cij,pj->pci", Rotation.from_rotvec(cams[:, 0:3]).as_matrix(), X) + cams[None, :, 3:6]
+    vis = _visible(P)
+    nvis = vis.sum(axis=1)
+    kind = rng.random(n_points)
+    k = np.where(kind < 0.2, 1, np.where(kind < 0.7, rng.integers(2, 13, n_points),
+                                         rng.integers(33, n_cameras + 1, n_points)))
+    k = np.minimum(k, nvis)
+    if (k < 1).any():
+        raise RuntimeError("a point is visible from no camera")
+    keys = np.where(vis, rng.random((n_points, n_cameras)), 2.0)
+    order = np.argsort(keys, axis=1)
+    rows = np.repeat(np.arange(n_points), k)
+    cols = order[rows, np.concatenate([np.arange(m) for m in k])]
+    cam_idx, pt_idx = _cover_cameras(cams, X, cols.astype(np.int64), rows.astype(np.int64), n_cameras, rng)
+    return _finish(name, cams, X, cam_idx, pt_idx, rng)
+
+
 def make_clusters(n_cameras=1100, n_points=1_000_000, seed=0, n_clusters=8, radius=20.0,
                   p_geom=0.12, k_cap=200, outlier_frac=0.05, batch=25_000, name=None):
     """configs[3]: 1100 cams in 8 clusters on a radius-20 sphere, 1M points ~ N(0, 4 I).

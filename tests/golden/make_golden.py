@@ -190,9 +190,20 @@ def pcg_bundle():
     print("wrote pcg.npz")
 
 
+def mixed_bundle():
+    """Track lengths 1 .. 72 (single-observation points, packed short tracks, long tracks)."""
+    from paper_2204_12834_b200 import configs
+    mixed = configs.make_mixed_tracks()
+    p = bal_io.BalProblem(mixed.camera_params, mixed.points, mixed.cam_indices, mixed.pt_indices, mixed.pixels)
+    bundle("mixed", p, lams=[1e-4, 1.0], solves=[(0.01, 20), (1e-300, 12)],
+           lm_cfgs={"lm_mixed": lm.LmConfig(solver="poba", max_outer_iterations=15, max_order=20)})
+
+
 def main():
     if len(sys.argv) > 2 and sys.argv[2] == "pcg":
         return pcg_bundle()
+    if len(sys.argv) > 2 and sys.argv[2] == "mixed":
+        return mixed_bundle()
     from paper_2204_12834_b200 import configs
     oracle = bal_io.perturb(synthetic.make_random_problem(3, 5, seed=1), 0.01, seed=0)
     bundle("rand3x5", oracle, lams=[1e-4, 1.0],
@@ -216,6 +227,7 @@ def main():
            store=False, save_inputs=False)
     explicit_bundle()
     pcg_bundle()
+    mixed_bundle()
 
 
 if __name__ == "__main__":

@@ -13,7 +13,7 @@ from conftest import golden_problem, load_golden
 
 pytestmark = pytest.mark.gpu
 
-FIXTURES = ["rand3x5", "noisy4x60", "rig49", "c1", "c2"]
+FIXTURES = ["rand3x5", "noisy4x60", "rig49", "c1", "c2", "mixed"]
 INC_TOL = 1e-9     # increments, relative (north star)
 COST_TOL = 1e-8    # per-LM cost, relative (north star)
 
@@ -95,6 +95,7 @@ def test_cost(P, name):
     ("rig49", "lm_poba", dict(max_outer_iterations=50)),
     ("c1", "lm_c1", dict(max_outer_iterations=10, max_order=32)),
     ("c2", "lm_c2", dict(max_outer_iterations=20, max_order=32, epsilon=1e-6)),
+    ("mixed", "lm_mixed", dict(max_outer_iterations=15, max_order=20)),
 ])
 def test_lm_trace(P, name, tag, kw):
     p, z = golden_problem(name)

@@ -14,7 +14,7 @@ import pytest
 from conftest import golden_problem, load_golden
 from oracle import poba_oracle as O
 
-FIXTURES = ["rand3x5", "noisy4x60", "rig49", "c1", "c2"]
+FIXTURES = ["rand3x5", "noisy4x60", "rig49", "c1", "c2", "mixed"]
 
 
 def rel(a, b):
@@ -78,6 +78,7 @@ def test_cost_matches_reference(name):
     ("noisy4x60", "lm_poba", {}),
     ("c1", "lm_c1", dict(max_outer_iterations=10, max_order=32)),
     ("c2", "lm_c2", dict(max_outer_iterations=20, max_order=32, epsilon=1e-6)),
+    ("mixed", "lm_mixed", dict(max_outer_iterations=15, max_order=20)),
 ])
 def test_lm_trace_matches_reference(name, tag, kw):
     p, z = golden_problem(name)
