@@ -62,6 +62,11 @@ int poba_destroy(poba_ctx* ctx);
  * this rank's landmark range.  pixels may be NULL (explicit-Jacobian use).   */
 int poba_set_problem(poba_ctx* ctx, int64_t n_cam, int64_t n_pt, int64_t n_obs,
                      const int64_t* cam_idx, const int64_t* pt_idx, const double* pixels);
+/* Block-storage precision (PoBA-32 / PoBA-64, blocks.py:42-47 `precision`):
+ * 32 keeps the Jacobian rows and residuals rounded to fp32 (half the bytes per
+ * series term) while every sum stays fp64, as the reference's float32 storage
+ * with float64 einsums.  Invalidates the linearization; default 64.          */
+int poba_set_precision(poba_ctx* ctx, int bits);
 /* info[0..15]: n_groups, n_tiles, n_chunks, n_partials, obs_lo, obs_hi, lm_lo,
  * lm_hi, max_slots, n_long, device_bytes, k_max, n_cam, n_pt, n_obs, rank   */
 int poba_problem_info(poba_ctx* ctx, int64_t* info);

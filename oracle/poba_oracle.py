@@ -210,8 +210,9 @@ def _reduce(store, cam_sorted, pt_sorted, order, n_cam, n_pt, n_invalid):
                      U0, V0, bp.ravel(), bl.ravel(), D_p, D_l, n_invalid)
 
 
-def linearize(cam_idx, pt_idx, pixels, cams, pts):
-    """blocks.py:293-324 (float64 storage)."""
+def linearize(cam_idx, pt_idx, pixels, cams, pts, precision=64):
+    """blocks.py:293-324; precision=32 stores the blocks as float32 (PoBA-32) and every
+    later sum reads the rounded values in float64 (blocks.py:42-47)."""
     cams = np.asarray(cams, dtype=np.float64)
     pts = np.asarray(pts, dtype=np.float64)
     n_cam, n_pt = cams.shape[0], pts.shape[0]
@@ -226,11 +227,13 @@ def linearize(cam_idx, pt_idx, pixels, cams, pts):
         store[s, :, 0:9] = jp
         store[s, :, 9:12] = jl
         store[s, :, 12] = res
+    if precision == 32:
+        store = store.astype(np.float32).astype(np.float64)
     return _reduce(store, cs, ps, order, n_cam, n_pt, bad)
 
 
-def linearize_explicit(cam_idx, pt_idx, jp, jl, res, n_cam, n_pt):
-    """blocks.py:333-352 (assemble_from_observations, float64 storage)."""
+def linearize_explicit(cam_idx, pt_idx, jp, jl, res, n_cam, n_pt, precision=64):
+    """blocks.py:333-352 (assemble_from_observations)."""
     cam_idx = np.asarray(cam_idx, dtype=np.int64)
     pt_idx = np.asarray(pt_idx, dtype=np.int64)
     order, cs, ps = canonical_order(cam_idx, pt_idx, n_pt)
@@ -238,6 +241,8 @@ def linearize_explicit(cam_idx, pt_idx, jp, jl, res, n_cam, n_pt):
     store[:, :, 0:9] = np.asarray(jp)[order]
     store[:, :, 9:12] = np.asarray(jl)[order]
     store[:, :, 12] = np.asarray(res)[order]
+    if precision == 32:
+        store = store.astype(np.float32).astype(np.float64)
     return _reduce(store, cs, ps, order, n_cam, n_pt, 0)
 
 
@@ -507,7 +512,8 @@ class OracleTrace:
 def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
            max_outer_iterations=50, relative_function_tolerance=1e-6,
            epsilon=0.01, max_order=20, lambda_decrease=2.0, lambda_increase=4.0,
-           damping="marquardt", clock=None, solver="poba", cg_tolerance=1e-6, cg_max_iterations=500):
+           damping="marquardt", clock=None, solver="poba", cg_tolerance=1e-6, cg_max_iterations=500,
+           precision=64):
     """lm.py:167-232 for solver in {'poba', 'pcg', 'pcg-power'} (dispatch lm.py:147-164), precision=64."""
     import time
     clock = clock or time.perf_counter
@@ -524,7 +530,7 @@ def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
     lin = None
     for it in range(1, max_outer_iterations + 1):
         if lin is None:
-            lin = linearize(cam_idx, pt_idx, pixels, cams, pts)
+            lin = linearize(cam_idx, pt_idx, pixels, cams, pts, precision)
         sys_ = OracleSystem(lin, lam, damping)
         if solver == "poba":
             dp, order, _ = series_solve(sys_, epsilon, max_order)

@@ -57,6 +57,7 @@ _SIGS = {
     "poba_debug_counters": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "poba_shard_bounds": (ctypes.c_int, [ctypes.c_int64, _I64P, ctypes.c_int, _I64P]),
     "poba_schur_diagonal": (ctypes.c_int, [_P, _DP]),
+    "poba_set_precision": (ctypes.c_int, [_P, ctypes.c_int]),
     "poba_pcg": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, _DP,
                                 _IP, _DP, _IP, _DP]),
 }
@@ -141,6 +142,7 @@ class Device:
         self._h = h
         self._lib = lib
         self.rank, self.nranks = rank, nranks
+        self.precision = 64
         self.n_cam = self.n_pt = self.n_obs = 0
 
     def close(self):
@@ -229,6 +231,11 @@ class Device:
         out = np.empty(9 * self.n_cam)
         _check(self._lib.poba_series_apply(self._h, _d(_f64(v)), int(order), _d(out)))
         return out
+
+    def set_precision(self, bits):
+        """Block storage precision 64 or 32 (PoBA-32); invalidates the linearization."""
+        _check(self._lib.poba_set_precision(self._h, int(bits)))
+        self.precision = int(bits)
 
     def schur_diagonal(self):
         out = np.empty((self.n_cam, 9, 9))

@@ -29,13 +29,15 @@ DIAG_CLAMP_MIN = 1e-6
 DIAG_CLAMP_MAX = 1e6
 
 
+_PRECISION_DTYPES = {32: np.float32, 64: np.float64}
+
+
 def _parse_precision(precision: int):
-    if precision not in (32, 64):
-        raise ValueError(f"precision must be 32 or 64, got {precision}")
-    if precision == 32:
-        raise NotImplementedError("PoBA-32 (fp32 block storage) is not implemented on the GPU path yet; "
-                                  "use precision=64")
-    return np.float64
+    """Block storage dtype (blocks.py:355-359); 32 = PoBA-32: fp32 blocks, fp64 reductions."""
+    try:
+        return _PRECISION_DTYPES[precision]
+    except (KeyError, TypeError):
+        raise ValueError(f"precision must be 32 or 64, got {precision}") from None
 
 
 # ---------------------------------------------------------------------------
@@ -151,7 +153,7 @@ class LandmarkBlockStore:
 
     @property
     def dtype(self):
-        return np.dtype(np.float64)
+        return np.dtype(_PRECISION_DTYPES[self._lin.precision])
 
     @property
     def n_observations(self):
@@ -160,13 +162,13 @@ class LandmarkBlockStore:
     @property
     def block_bytes(self) -> int:
         """sum over landmarks of 2k * 13 * itemsize, as the reference accounts it (blocks.py:97-100)."""
-        return self.n_observations * 2 * BLOCK_COLS * 8
+        return self.n_observations * 2 * BLOCK_COLS * self.dtype.itemsize
 
     @property
     def storage_obs(self):
         if self._storage is None:
             self._lin._activate()
-            self._storage = self._dp.dev.read(_lib.READ_STORAGE)
+            self._storage = self._dp.dev.read(_lib.READ_STORAGE).astype(self.dtype, copy=False)
         return self._storage
 
     @property
@@ -198,9 +200,10 @@ class LandmarkBlockStore:
 class Linearization:
     """Device linearization (reference blocks.py:115-137); arrays read back lazily."""
 
-    def __init__(self, dp: DeviceProblem, source, n_invalid: int):
+    def __init__(self, dp: DeviceProblem, source, n_invalid: int, precision: int = 64):
         self._dp = dp
         self._source = source
+        self.precision = int(precision)
         self.n_invalid = int(n_invalid)
         dp.generation += 1
         self._gen = dp.generation
@@ -215,6 +218,7 @@ class Linearization:
         if dp.generation == self._gen:
             return
         kind = self._source[0]
+        dp.dev.set_precision(self.precision)
         if kind == "state":
             dp.dev.linearize(self._source[1], self._source[2])
         else:
@@ -421,8 +425,7 @@ class DampedSystem:
 def memory_account(system: DampedSystem) -> int:
     """The reference's analytic byte count of one damped system (blocks.py:263-274)."""
     n_p, n_l = system.n_cameras, system.n_points
-    n_obs = system.store.n_observations
-    return (n_obs * 2 * BLOCK_COLS * 8 + 3 * n_p * 81 * 8 + 3 * n_l * 9 * 8
+    return (system.store.block_bytes + 3 * n_p * 81 * 8 + 3 * n_l * 9 * 8
             + 2 * (9 * n_p + 3 * n_l) * 8)
 
 
@@ -438,12 +441,13 @@ def linearize(problem, state=None, precision: int = 64, device: int = 0) -> Line
     cams = np.ascontiguousarray(state.camera_params, dtype=np.float64)
     pts = np.ascontiguousarray(state.points, dtype=np.float64)
     dp = device_problem(problem, device)
+    dp.dev.set_precision(precision)
     n_invalid = dp.dev.linearize(cams, pts)
     if n_invalid:
         log.warning("%d observation(s) had zero projected depth and were zeroed", n_invalid)
     # the source arrays are kept by reference (no copy), like the reference keeps
     # no copy at all; callers must not mutate them while the Linearization lives
-    return Linearization(dp, ("state", cams, pts), n_invalid)
+    return Linearization(dp, ("state", cams, pts), n_invalid, precision)
 
 
 def assemble(problem, state=None, lam: float = 1e-4, precision: int = 64,
@@ -463,5 +467,6 @@ def assemble_from_observations(cam_indices, pt_indices, j_pose, j_point, residua
     jp = np.ascontiguousarray(j_pose, dtype=np.float64)
     jl = np.ascontiguousarray(j_point, dtype=np.float64)
     r = np.ascontiguousarray(residuals, dtype=np.float64)
+    dp.dev.set_precision(precision)
     dp.dev.linearize_explicit(jp, jl, r)
-    return Linearization(dp, ("explicit", jp, jl, r), 0)
+    return Linearization(dp, ("explicit", jp, jl, r), 0, precision)

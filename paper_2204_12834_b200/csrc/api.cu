@@ -294,6 +294,11 @@ int poba_set_problem(poba_ctx* ctx, int64_t n_cam, int64_t n_pt, int64_t n_obs, 
   return POBA_OK;
 }
 
+int poba_set_precision(poba_ctx* ctx, int bits) {
+  CTX_CHECK(ctx);
+  return poba::set_precision_device(ctx->c, bits);
+}
+
 int poba_problem_info(poba_ctx* ctx, int64_t* info) {
   CTX_CHECK(ctx);
   NEED(info, "null output");
@@ -612,7 +617,13 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
       const int64_t ns = c.n_slots, n = c.n_obs;
       std::vector<double> J((size_t)poba::kRow * ns * 2), R(ns * 2);
       std::vector<int> file(ns), order(n), slot_of_file(n, -1);
-      PTRY(poba::copy_sync(c, J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
+      if (c.precision == 32) {  // fp32 store: widen (exact) for the float64 caller
+        std::vector<float> Jf((size_t)poba::kRow * ns * 2);
+        PTRY(poba::copy_sync(c, Jf.data(), c.J.p, Jf.size() * 4, cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < Jf.size(); ++q) J[q] = (double)Jf[q];
+      } else {
+        PTRY(poba::copy_sync(c, J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
+      }
       PTRY(poba::copy_sync(c, R.data(), c.Rz.p, R.size() * 8, cudaMemcpyDeviceToHost));
       PTRY(poba::copy_sync(c, file.data(), c.file_s.p, ns * 4, cudaMemcpyDeviceToHost));
       PTRY(poba::copy_sync(c, order.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));

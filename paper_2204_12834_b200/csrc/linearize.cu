@@ -129,12 +129,12 @@ __device__ __forceinline__ void evaluate_obs(const double* __restrict__ cp, doub
 // warp per warp-tile, each landmark's observations in camera order (np.add.at's
 // sequential fold of blocks.py:394,396 runs over the same observations in the
 // same order).
-template <bool kExplicit>
+template <bool kExplicit, bool F32>
 __global__ void __launch_bounds__(kBlockTiles * kTile)
 k_lin_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
            const int* __restrict__ file_s, const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s,
            const double* __restrict__ prep, const double* __restrict__ points, const double* __restrict__ ejp,
-           const double* __restrict__ ejl, const double* __restrict__ eres, double2* __restrict__ J,
+           const double* __restrict__ ejl, const double* __restrict__ eres, void* __restrict__ J,
            double2* __restrict__ Rz, double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
            unsigned long long* __restrict__ n_invalid) {
   __shared__ double contrib_all[kBlockTiles][kTile * 9];
@@ -171,11 +171,23 @@ k_lin_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ 
       evaluate_obs<true>(prep + (int64_t)cam_s[o] * 16, X[0], X[1], X[2], pix_s[o], m);
       bad = !m.valid;
     }
-    double2* row = J + o * kRow;
+    // at precision 32 every stored value is rounded to fp32 first and all
+    // sums below use the rounded values, as the reference's float32 storage
+    // feeds its float64 einsums (blocks.py:316-320, 387-396)
 #pragma unroll
-    for (int j = 0; j < 9; ++j) row[j] = make_double2(m.jp0[j], m.jp1[j]);
+    for (int j = 0; j < 9; ++j) {
+      m.jp0[j] = stored<F32>(m.jp0[j]);
+      m.jp1[j] = stored<F32>(m.jp1[j]);
+      jstore<F32>(J, o, j, m.jp0[j], m.jp1[j]);
+    }
 #pragma unroll
-    for (int b = 0; b < 3; ++b) row[9 + b] = make_double2(m.jl0[b], m.jl1[b]);
+    for (int b = 0; b < 3; ++b) {
+      m.jl0[b] = stored<F32>(m.jl0[b]);
+      m.jl1[b] = stored<F32>(m.jl1[b]);
+      jstore<F32>(J, o, 9 + b, m.jl0[b], m.jl1[b]);
+    }
+    m.r0 = stored<F32>(m.r0);
+    m.r1 = stored<F32>(m.r1);
     Rz[o] = make_double2(m.r0, m.r1);
     double* cc = contrib + lane * 9;
     cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
@@ -211,8 +223,9 @@ k_lin_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ 
 }
 
 // V0/b_l of landmarks longer than a tile, straight from the stored rows
+template <bool F32>
 __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0,
-                           const int* __restrict__ lm_k, const double2* __restrict__ J,
+                           const int* __restrict__ lm_k, const void* __restrict__ J,
                            const double2* __restrict__ Rz, int64_t pad, double* __restrict__ V0,
                            double* __restrict__ bl, double* __restrict__ Dl) {
   const int lm = long_lm[blockIdx.x];
@@ -221,8 +234,7 @@ __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restric
   if (comp >= 9) return;
   double acc = 0.0;
   for (int o = o0; o < o1; ++o) {
-    const double2* row = J + (int64_t)o * kRow;
-    const double2 a = row[9], b = row[10], c = row[11];
+    const double2 a = jload<F32>(J, o, 9), b = jload<F32>(J, o, 10), c = jload<F32>(J, o, 11);
     const double2 r = Rz[o];
     double v;
     switch (comp) {
@@ -256,9 +268,10 @@ __device__ __forceinline__ int find_camera(const int* __restrict__ off, int n_ca
 
 // U0 (packed upper 45) and b_p (9) partial sums over chunks of <= 128 observations
 // of one camera, walked in camera-major order; fixed warp-butterfly reduction.
+template <bool F32>
 __global__ void __launch_bounds__(256)
 k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cam_start,
-                   const int* __restrict__ cperm, const double2* __restrict__ J,
+                   const int* __restrict__ cperm, const void* __restrict__ J,
                    const double2* __restrict__ Rz, int64_t pad, int n_cam, int n_cc,
                    double* __restrict__ out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -273,10 +286,9 @@ k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ c
   for (int p = p0 + lane; p < p1; p += 32) {
     const int o = cperm[p];
     double a[9], b[9];
-    const double2* row = J + (int64_t)o * kRow;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = row[j];
+      const double2 v = jload<F32>(J, o, j);
       a[j] = v.x;
       b[j] = v.y;
     }
@@ -411,29 +423,45 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 32);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
   const unsigned nb = grid_for(c.n_tiles, kBlockTiles);
-  if (expl)
-    k_lin_tile<true><<<nb, kBlockTiles * kTile, 0, s>>>(
-        c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
-        c.lidx_s.as<uint8_t>(), nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>(),
-        c.J.as<double2>(), c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(), c.Dl.as<double>(), d_bad);
-  else
-    k_lin_tile<false><<<nb, kBlockTiles * kTile, 0, s>>>(
-        c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
-        c.lidx_s.as<uint8_t>(), c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr,
-        c.J.as<double2>(), c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(), c.Dl.as<double>(), d_bad);
+  const bool f32 = c.precision == 32;
+  auto lin = [&](auto kern, const double* prep, const double* pts, const double* a, const double* b,
+                 const double* r) {
+    kern<<<nb, kBlockTiles * kTile, 0, s>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.file_s.as<int>(),
+                                            c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(), prep, pts, a, b, r,
+                                            c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
+                                            c.Dl.as<double>(), d_bad);
+  };
+  if (expl) {
+    if (f32) lin(k_lin_tile<true, true>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>());
+    else lin(k_lin_tile<true, false>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>());
+  } else {
+    if (f32) lin(k_lin_tile<false, true>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr);
+    else lin(k_lin_tile<false, false>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr);
+  }
   c.launches++;
   PCK(cudaGetLastError());
   if (c.n_long) {
-    k_lin_long<<<c.n_long, 32, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(),
-                                       c.J.as<double2>(), c.Rz.as<double2>(), ns, c.V0.as<double>(),
-                                       c.bl.as<double>(), c.Dl.as<double>());
+    if (f32)
+      k_lin_long<true><<<c.n_long, 32, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.J.p,
+                                               c.Rz.as<double2>(), ns, c.V0.as<double>(), c.bl.as<double>(),
+                                               c.Dl.as<double>());
+    else
+      k_lin_long<false><<<c.n_long, 32, 0, s>>>(c.long_lm.as<int>(), c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.J.p,
+                                                c.Rz.as<double2>(), ns, c.V0.as<double>(), c.bl.as<double>(),
+                                                c.Dl.as<double>());
     c.launches++;
   }
   // camera side: U0 / b_p via camera-major chunks, then a fixed-order merge
   if (c.n_cchunks) {
-    k_cam_chunk_reduce<<<grid_for((int64_t)c.n_cchunks * 32, 256), 256, 0, s>>>(
-        c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(), c.J.as<double2>(), c.Rz.as<double2>(),
-        ns, (int)c.n_cam, c.n_cchunks, c.cc_part.as<double>());
+    const unsigned g = grid_for((int64_t)c.n_cchunks * 32, 256);
+    if (f32)
+      k_cam_chunk_reduce<true><<<g, 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
+                                                 c.J.p, c.Rz.as<double2>(), ns, (int)c.n_cam, c.n_cchunks,
+                                                 c.cc_part.as<double>());
+    else
+      k_cam_chunk_reduce<false><<<g, 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
+                                                  c.J.p, c.Rz.as<double2>(), ns, (int)c.n_cam, c.n_cchunks,
+                                                  c.cc_part.as<double>());
     c.launches++;
   }
   k_cam_merge54<<<grid_for(c.n_cam * 32, 256), 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_part.as<double>(),

@@ -33,9 +33,10 @@ __device__ __forceinline__ int find_cam(const int* __restrict__ off, int n_cam, 
 
 // per camera-major chunk (<= kCamChunk observations of one camera):
 // sum of W_o V_l^-1 W_o^T, W_o = J_p^T J_l (9x3), packed upper 45
+template <bool F32>
 __global__ void __launch_bounds__(128)
 k_schur_diag_chunk(const int* __restrict__ cc_cam_off, const int* __restrict__ cam_start,
-                   const int* __restrict__ cperm, const double2* __restrict__ J, const Tile* __restrict__ tiles,
+                   const int* __restrict__ cperm, const void* __restrict__ J, const Tile* __restrict__ tiles,
                    const uint8_t* __restrict__ lidx_s, const double* __restrict__ Vinv, int n_cam, int n_cc,
                    double* __restrict__ out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -49,16 +50,15 @@ k_schur_diag_chunk(const int* __restrict__ cc_cam_off, const int* __restrict__ c
   for (int q = 0; q < 45; ++q) acc[q] = 0.0;
   for (int p = p0 + lane; p < p1; p += 32) {
     const int o = cperm[p];
-    const double2* row = J + (int64_t)o * kRow;
     const Tile t = tiles[o >> 5];
     const int lm = t.lm0 + ((t.flags & kTileLong) ? 0 : lidx_s[o]);
     const double* V = Vinv + (int64_t)lm * 6;
     const double v00 = V[0], v01 = V[1], v02 = V[2], v11 = V[3], v12 = V[4], v22 = V[5];
-    const double2 l0 = row[9], l1 = row[10], l2 = row[11];
+    const double2 l0 = jload<F32>(J, o, 9), l1 = jload<F32>(J, o, 10), l2 = jload<F32>(J, o, 11);
     double w[9][3], tm[9][3];
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
-      const double2 a = row[i];
+      const double2 a = jload<F32>(J, o, i);
       w[i][0] = fma(a.x, l0.x, a.y * l0.y);
       w[i][1] = fma(a.x, l1.x, a.y * l1.y);
       w[i][2] = fma(a.x, l2.x, a.y * l2.y);
@@ -150,9 +150,17 @@ int schur_diag_device(Ctx& c, double* d_out45 /* nullable */) {
   PTRY(c.scratch_c.alloc(n_cam * 45 * 8));
   if (c.n_cchunks) {
     const int threads = 128;
-    k_schur_diag_chunk<<<grid_for((int64_t)c.n_cchunks * 32, threads), threads, 0, s>>>(
-        c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(), c.J.as<double2>(), c.tiles.as<Tile>(),
-        c.lidx_s.as<uint8_t>(), c.Vinv.as<double>(), (int)n_cam, c.n_cchunks, c.cc_part.as<double>());
+    const unsigned g = grid_for((int64_t)c.n_cchunks * 32, threads);
+    if (c.precision == 32)
+      k_schur_diag_chunk<true><<<g, threads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
+                                                     c.J.p, c.tiles.as<Tile>(), c.lidx_s.as<uint8_t>(),
+                                                     c.Vinv.as<double>(), (int)n_cam, c.n_cchunks,
+                                                     c.cc_part.as<double>());
+    else
+      k_schur_diag_chunk<false><<<g, threads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(),
+                                                      c.cperm.as<int>(), c.J.p, c.tiles.as<Tile>(),
+                                                      c.lidx_s.as<uint8_t>(), c.Vinv.as<double>(), (int)n_cam,
+                                                      c.n_cchunks, c.cc_part.as<double>());
     c.launches++;
   }
   k_schur_diag_merge<<<grid_for(n_cam * 32, 256), 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_part.as<double>(),

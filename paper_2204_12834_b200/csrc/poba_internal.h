@@ -49,6 +49,11 @@ constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kTRecB
 static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
 static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 
+// PoBA-32 (blocks.py:42-47): block storage may be fp32 (rows of 13 float2 =
+// 104 B, metadata as int2 {slot, run}); every value read from it is widened to
+// fp64 and all arithmetic and reductions stay fp64.
+constexpr int kRowBytesF32 = kRow * 8;
+
 // metadata word (row entry 12, as int4)
 struct RowMeta {
   int slot;      // slot of the camera in the chunk accumulator table
@@ -180,6 +185,7 @@ struct PcgState {
 
 struct Ctx {
   int device = 0;
+  int precision = 64;  // block storage: 64 (double2 rows) or 32 (float2 rows)
   cudaStream_t stream = nullptr;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
@@ -231,7 +237,8 @@ struct Ctx {
   DBuf cc_cam_off;   // int32 [n_cam+1] camera -> cchunk range
 
   // store (K1), slot space
-  DBuf J;            // double2 [n_slots][kRow] rows (J_p pairs, J_l pairs, metadata)
+  DBuf J;            // [n_slots][kRow] rows (J_p pairs, J_l pairs, metadata): double2, or float2 at precision 32
+  DBuf slot_s;       // int32 [n_slots] chunk slot of each observation's camera (metadata source)
   DBuf Rz;           // double2 [n_slots] residuals
 
   // camera arrays
@@ -318,6 +325,7 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out);
 int cameras_prep(Ctx& c, const double* d_cams, double* d_prep);
 int allreduce_sum(Ctx& c, double* d_buf, size_t n);
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches);
+int set_precision_device(Ctx& c, int bits);
 int b_tilde_device(Ctx& c);
 int schur_diag_device(Ctx& c, double* d_out45);
 int pcg_device(Ctx& c, int precond, int order, double tol, int max_iter, bool resume, double* h_delta_p,
@@ -338,6 +346,26 @@ inline int copy_sync(Ctx& c, void* dst, const void* src, size_t bytes, cudaMemcp
 
 // ---- device helpers shared by the tile kernels -----------------------------------
 #ifdef __CUDACC__
+// Jacobian column pair p (0..11) of slot o, widened to fp64
+template <bool F32>
+__device__ __forceinline__ double2 jload(const void* __restrict__ J, int64_t o, int p) {
+  if (F32) {
+    const float2 v = reinterpret_cast<const float2*>(J)[o * kRow + p];
+    return make_double2((double)v.x, (double)v.y);
+  }
+  return reinterpret_cast<const double2*>(J)[o * kRow + p];
+}
+template <bool F32>
+__device__ __forceinline__ void jstore(void* __restrict__ J, int64_t o, int p, double a, double b) {
+  if (F32) reinterpret_cast<float2*>(J)[o * kRow + p] = make_float2((float)a, (float)b);
+  else reinterpret_cast<double2*>(J)[o * kRow + p] = make_double2(a, b);
+}
+// the value fp32 storage keeps (round to nearest, as numpy's astype(float32))
+template <bool F32>
+__device__ __forceinline__ double stored(double v) {
+  return F32 ? (double)__double2float_rn(v) : v;
+}
+
 // landmark starts inside a tile from the per-slot landmark index (lstart has nlm+1 entries)
 __device__ __forceinline__ void tile_landmark_starts(const uint8_t* __restrict__ lidx_tile, int n, int nlm,
                                                      int* lstart) {

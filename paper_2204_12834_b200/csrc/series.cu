@@ -215,7 +215,7 @@ struct TermArgs {
   const TileK* tk;         // per warp-tile kernel descriptors
   const int2* cta_tiles;   // tile range of each CTA
   const int* cam_s;        // camera of each slot (gathered two tiles ahead)
-  const double2* J;        // slot rows
+  const void* J;           // slot rows (double2, or float2 at precision 32)
   const double* tin;       // camera vector (kModeTerm)
   const double* lvec;      // b_l (kModeBt) or landmark input (kModeW)
   const double* Vinv;
@@ -245,7 +245,7 @@ struct TermArgs {
 //            pre-summed in lane order.
 // After the last tile of a chunk its warp writes the table out once (one 80-B
 // partial per (chunk, camera)) and clears it before passing the turn on.
-template <int MODE>
+template <int MODE, bool F32>
 __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -270,8 +270,11 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
 
   auto issue = [&](int ti, int n, int nlm, int lm0) {  // lane 0
     const uint32_t vbytes = (MODE != kModeW) ? (uint32_t)(nlm * 48) : 0u;
-    mbar_expect_tx(sbar, (uint32_t)(n * kRowBytes + 32) + vbytes);
-    bulk_g2s_stream(stg, a.J + (int64_t)ti * kTile * kRow, (uint32_t)(n * kRowBytes), sbar, pol);
+    // fp32 rows are 104 B: copy an even number of them (bulk copies move multiples of 16 B)
+    const uint32_t rbytes = F32 ? (uint32_t)(((n + 1) & ~1) * kRowBytesF32) : (uint32_t)(n * kRowBytes);
+    const char* src = static_cast<const char*>(a.J) + (int64_t)ti * kTile * (F32 ? kRowBytesF32 : kRowBytes);
+    mbar_expect_tx(sbar, rbytes + 32u + vbytes);
+    bulk_g2s_stream(stg, src, rbytes, sbar, pol);
     bulk_g2s(stg + kStDesc, a.tk + ti, 32, sbar);
     if (vbytes) bulk_g2s(stg + kStVinv, a.Vinv + (int64_t)lm0 * 6, vbytes, sbar);
   };
@@ -334,10 +337,15 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
     const bool valid = lane < t.n;
     const bool is_long = t.flags & kTileLong;
-    const double2* row = reinterpret_cast<const double2*>(stg) + lane * kRow;
     int slot = 0, li = 0, first = lane, last = lane;
-    if (valid) {  // one 16-B shared load: slot, landmark run
-      const int4 mv = *reinterpret_cast<const int4*>(row + 12);
+    if (valid) {  // slot, landmark run (16-B load; 8-B at precision 32)
+      int2 mv;
+      if (F32) {
+        mv = reinterpret_cast<const int2*>(stg)[lane * kRow + 12];
+      } else {
+        const int4 m4 = reinterpret_cast<const int4*>(stg)[lane * kRow + 12];
+        mv = make_int2(m4.x, m4.y);
+      }
       slot = mv.x;
       li = mv.y & 0xff;
       first = (mv.y >> 8) & 0xff;
@@ -356,7 +364,14 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     }
     double2 jr[kJPlanes];
 #pragma unroll
-    for (int p = 0; p < kJPlanes; ++p) jr[p] = valid ? row[p] : make_double2(0.0, 0.0);
+    for (int p = 0; p < kJPlanes; ++p) {
+      if (F32) {
+        const float2 v = valid ? reinterpret_cast<const float2*>(stg)[lane * kRow + p] : make_float2(0.f, 0.f);
+        jr[p] = make_double2((double)v.x, (double)v.y);
+      } else {
+        jr[p] = valid ? reinterpret_cast<const double2*>(stg)[lane * kRow + p] : make_double2(0.0, 0.0);
+      }
+    }
     __syncwarp();  // every lane is done with the stage: refill it with this warp's next tile
     if (lane == 0 && q + 1 < nq) {
       issue(ti + kTermWarps, t.nx_n & 0xff, t.nx_n >> 8, t.nx_lm0);
@@ -640,10 +655,10 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
 // W^T-type passes with landmark output (apply_wt, back-substitution, long z)
 // ---------------------------------------------------------------------------
 
-template <int OUT>
+template <int OUT, bool F32>
 __global__ void __launch_bounds__(kBlockTiles * kTile)
 k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
-          const uint8_t* __restrict__ lidx_s, const double2* __restrict__ J, const double* __restrict__ tin, int ts,
+          const uint8_t* __restrict__ lidx_s, const void* __restrict__ J, const double* __restrict__ tin, int ts,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag) {
   __shared__ double wbuf_all[kBlockTiles][kTile * 3];
@@ -658,17 +673,16 @@ k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ c
   const int64_t o = (int64_t)ti * kTile + lane;
   if (lane < t.n) {
     const double* tv = tin + (int64_t)cam_s[o] * ts;
-    const double2* row = J + o * kRow;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = row[j];
+      const double2 v = jload<F32>(J, o, j);
       u0 = fma(v.x, tv[j], u0);
       u1 = fma(v.y, tv[j], u1);
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const double2 v = row[9 + b];
+      const double2 v = jload<F32>(J, o, 9 + b);
       wbuf[lane * 3 + b] = fma(v.x, u0, v.y * u1);
     }
     const int li = lidx_s[o];
@@ -705,10 +719,10 @@ k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ c
 constexpr int kLongWarps = 8;
 constexpr int kLongThreads = kLongWarps * 32;
 
-template <int OUT>
+template <int OUT, bool F32>
 __global__ void __launch_bounds__(kLongThreads)
 k_wt_long(const int* __restrict__ long_lm, int n_long, const int* __restrict__ lm_slot0, const int* __restrict__ lm_k,
-          const int* __restrict__ cam_s, const double2* __restrict__ J, int ts, const double* __restrict__ tin,
+          const int* __restrict__ cam_s, const void* __restrict__ J, int ts, const double* __restrict__ tin,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag, const SeriesState* __restrict__ st, int check_stop) {
   if (check_stop && st->stopped) return;
@@ -719,15 +733,14 @@ k_wt_long(const int* __restrict__ long_lm, int n_long, const int* __restrict__ l
   double y0 = 0.0, y1 = 0.0, y2 = 0.0;
   for (int o = o0 + lane; o < o1; o += 32) {
     const double* tv = tin + (int64_t)cam_s[o] * ts;
-    const double2* row = J + (int64_t)o * kRow;
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = row[j];
+      const double2 v = jload<F32>(J, o, j);
       u0 = fma(v.x, tv[j], u0);
       u1 = fma(v.y, tv[j], u1);
     }
-    const double2 a = row[9], b = row[10], c = row[11];
+    const double2 a = jload<F32>(J, o, 9), b = jload<F32>(J, o, 10), c = jload<F32>(J, o, 11);
     y0 += fma(a.x, u0, a.y * u1);
     y1 += fma(b.x, u0, b.y * u1);
     y2 += fma(c.x, u0, c.y * u1);
@@ -798,14 +811,48 @@ __global__ void k_add_inplace(double* __restrict__ a, const double* __restrict__
   if (q < n) a[q] += b[q];
 }
 
+template <int OUT>
+void launch_wt_tile(Ctx& c, const double* tin, int ts, const double* bl, double* out, int* flag) {
+  const unsigned g = grid_for(c.n_tiles, kBlockTiles);
+  if (c.precision == 32)
+    k_wt_tile<OUT, true><<<g, kBlockTiles * kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(),
+                                                                  c.lidx_s.as<uint8_t>(), c.J.p, tin, ts, bl,
+                                                                  c.Vinv.as<double>(), out, flag);
+  else
+    k_wt_tile<OUT, false><<<g, kBlockTiles * kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(),
+                                                                   c.lidx_s.as<uint8_t>(), c.J.p, tin, ts, bl,
+                                                                   c.Vinv.as<double>(), out, flag);
+  c.launches++;
+}
+
+template <int OUT>
+void launch_wt_long(Ctx& c, const double* tin, int ts, const double* bl, double* out, int* flag, bool check_stop) {
+  if (!c.n_long) return;
+  const unsigned g = grid_for(c.n_long, kLongWarps);
+  if (c.precision == 32)
+    k_wt_long<OUT, true><<<g, kLongThreads, 0, c.stream>>>(c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(),
+                                                           c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.p, ts, tin, bl,
+                                                           c.Vinv.as<double>(), out, flag, c.state.as<SeriesState>(),
+                                                           check_stop ? 1 : 0);
+  else
+    k_wt_long<OUT, false><<<g, kLongThreads, 0, c.stream>>>(c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(),
+                                                            c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.p, ts, tin, bl,
+                                                            c.Vinv.as<double>(), out, flag,
+                                                            c.state.as<SeriesState>(), check_stop ? 1 : 0);
+  c.launches++;
+}
+
 int configure_term(Ctx& c) {
   static thread_local int done_dev = -1;
   int dev = 0;
   PCK(cudaGetDevice(&dev));
   if (done_dev != dev) {
-    PCK(cudaFuncSetAttribute(k_term<kModeTerm>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
-    PCK(cudaFuncSetAttribute(k_term<kModeBt>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
-    PCK(cudaFuncSetAttribute(k_term<kModeW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeTerm, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeBt, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeTerm, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeBt, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    PCK(cudaFuncSetAttribute(k_term<kModeW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
     done_dev = dev;
   }
   return POBA_OK;
@@ -816,7 +863,7 @@ TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_sto
   a.tk = c.tilek.as<TileK>();
   a.cta_tiles = c.cta_tiles.as<int2>();
   a.cam_s = c.cam_s.as<int>();
-  a.J = c.J.as<double2>();
+  a.J = c.J.p;
   a.tin = tin;
   a.lvec = lvec;
   a.Vinv = c.Vinv.as<double>();
@@ -854,19 +901,17 @@ int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool ch
   const TermArgs a = term_args(c, tin, lvec, check_stop);
   const size_t smem = kTermSmem;
   const unsigned grid = (unsigned)c.n_cta;
+  const bool f32 = c.precision == 32;
   if (mode == kModeTerm) {
-    if (c.n_long) {
-      k_wt_long<kOutZ><<<grid_for(c.n_long, kLongWarps), kLongThreads, 0, c.stream>>>(
-          c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(), c.lm_k.as<int>(), c.cam_s.as<int>(), c.J.as<double2>(),
-          kTStride, tin, nullptr, c.Vinv.as<double>(), c.ltmp.as<double>(), nullptr, c.state.as<SeriesState>(),
-          check_stop ? 1 : 0);
-      c.launches++;
-    }
-    k_term<kModeTerm><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    launch_wt_long<kOutZ>(c, tin, kTStride, nullptr, c.ltmp.as<double>(), nullptr, check_stop);
+    if (f32) k_term<kModeTerm, true><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeTerm, false><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   } else if (mode == kModeBt) {
-    k_term<kModeBt><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeBt, true><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeBt, false><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   } else {
-    k_term<kModeW><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeW, true><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeW, false><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   }
   c.launches++;
   PCK(cudaGetLastError());
@@ -1074,17 +1119,8 @@ int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero) {
   cudaStream_t s = c.stream;
   int* fl = c.flag.as<int>() + 1;
   PCK(cudaMemsetAsync(fl, 0, 4, s));
-  k_wt_tile<kOutBack><<<grid_for(c.n_tiles, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
-      c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_dp, 9,
-      c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl);
-  c.launches++;
-  if (c.n_long) {
-    k_wt_long<kOutBack><<<grid_for(c.n_long, kLongWarps), kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(), c.lm_k.as<int>(),
-                                                   c.cam_s.as<int>(), c.J.as<double2>(), 9, d_dp,
-                                                   c.bl.as<double>(), c.Vinv.as<double>(), c.dl.as<double>(), fl,
-                                                   c.state.as<SeriesState>(), 0);
-    c.launches++;
-  }
+  launch_wt_tile<kOutBack>(c, d_dp, 9, c.bl.as<double>(), c.dl.as<double>(), fl);
+  launch_wt_long<kOutBack>(c, d_dp, 9, c.bl.as<double>(), c.dl.as<double>(), fl, false);
   PCK(cudaGetLastError());
   int h = 0;
   PCK(cudaMemcpyAsync(&h, fl, 4, cudaMemcpyDeviceToHost, s));
@@ -1112,16 +1148,8 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
       PCK(cudaMemcpyAsync(d_out, c.rvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, s));
       break;
     case POBA_OP_WT:
-      k_wt_tile<kOutWt><<<grid_for(c.n_tiles, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
-          c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.lidx_s.as<uint8_t>(), c.J.as<double2>(), d_in, 9, nullptr,
-          nullptr, d_out, nullptr);
-      c.launches++;
-      if (c.n_long) {
-        k_wt_long<kOutWt><<<grid_for(c.n_long, kLongWarps), kLongThreads, 0, s>>>(c.long_lm.as<int>(), c.n_long, c.lm_slot0.as<int>(), c.lm_k.as<int>(),
-                                                     c.cam_s.as<int>(), c.J.as<double2>(), 9, d_in, nullptr,
-                                                     nullptr, d_out, nullptr, c.state.as<SeriesState>(), 0);
-        c.launches++;
-      }
+      launch_wt_tile<kOutWt>(c, d_in, 9, nullptr, d_out, nullptr);
+      launch_wt_long<kOutWt>(c, d_in, 9, nullptr, d_out, nullptr, false);
       break;
     case POBA_OP_U_INV:
       k_cam_mv<<<grid_for(c.n_cam * 9, 256), 256, 0, s>>>(c.Uinv.as<double>(), d_in, c.n_cam, d_out);

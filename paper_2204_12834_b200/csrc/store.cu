@@ -117,9 +117,10 @@ __global__ void k_fill_i32(int* __restrict__ a, int64_t n, int v) {
 }
 
 // metadata column (row entry 12) of every slot; one warp per tile
+template <bool F32>
 __global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
                             const int* __restrict__ slot_s, const uint8_t* __restrict__ lidx_s,
-                            double2* __restrict__ J) {
+                            void* __restrict__ J) {
   const Tile t = tiles[blockIdx.x];
   const int lane = threadIdx.x;
   const int64_t s = (int64_t)blockIdx.x * kTile + lane;
@@ -136,7 +137,8 @@ __global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restric
   m.pad = 0;
   m.run = valid ? (li | (first << 8) | (last << 16)) : 0;
   m.cam = cam_s[s];
-  *reinterpret_cast<RowMeta*>(J + s * kRow + 12) = m;
+  if (F32) reinterpret_cast<int2*>(J)[s * kRow + 12] = make_int2(m.slot, m.run);  // 8-B metadata
+  else *reinterpret_cast<RowMeta*>(reinterpret_cast<double2*>(J) + s * kRow + 12) = m;
 }
 
 __global__ void k_cam_slot_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
@@ -389,6 +391,36 @@ int build_canonical_order(Ctx& c) {
     j = e;
   }
   c.have_order = true;
+  return POBA_OK;
+}
+
+// (re)allocate the row store for the context's precision and write the metadata
+int alloc_store(Ctx& c) {
+  const size_t row = c.precision == 32 ? (size_t)kRowBytesF32 : (size_t)kRowBytes;
+  const size_t bytes = row * (size_t)c.n_slots;
+  c.J.release();
+  PTRY(c.J.alloc(bytes));
+  PCK(cudaMemsetAsync(c.J.p, 0, bytes, c.stream));
+  if (c.precision == 32)
+    k_pack_meta<true><<<c.n_tiles, kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.slot_s.as<int>(),
+                                                         c.lidx_s.as<uint8_t>(), c.J.p);
+  else
+    k_pack_meta<false><<<c.n_tiles, kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.slot_s.as<int>(),
+                                                          c.lidx_s.as<uint8_t>(), c.J.p);
+  c.launches++;
+  PCK(cudaGetLastError());
+  PCK(cudaStreamSynchronize(c.stream));
+  return POBA_OK;
+}
+
+// switch the block-storage precision (PoBA-32 / PoBA-64); the store must be re-linearized
+int set_precision_device(Ctx& c, int bits) {
+  if (bits != 32 && bits != 64) return fail(POBA_EINVAL, "precision must be 32 or 64, got " + std::to_string(bits));
+  if (bits == c.precision) return POBA_OK;
+  c.precision = bits;
+  c.drop_graphs();
+  c.have_lin = c.have_damp = c.have_solution = c.have_delta_l = false;
+  if (c.have_problem) PTRY(alloc_store(c));
   return POBA_OK;
 }
 
@@ -688,19 +720,12 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   }
 
   // --- store rows (J + metadata) and work buffers ------------------------------------------------------------
-  PTRY(c.J.alloc((size_t)kRow * ns * 16));
   PTRY(c.Rz.alloc((size_t)ns * 16));
-  PCK(cudaMemsetAsync(c.J.p, 0, (size_t)kRow * ns * 16, s));
   PCK(cudaMemsetAsync(c.Rz.p, 0, (size_t)ns * 16, s));
-  {
-    DBuf dslot;
-    PTRY(dslot.alloc(ns * 4));
-    PCK(cudaMemcpyAsync(dslot.p, obs_slot.data(), ns * 4, cudaMemcpyHostToDevice, s));
-    k_pack_meta<<<c.n_tiles, kTile, 0, s>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), dslot.as<int>(),
-                                            c.lidx_s.as<uint8_t>(), c.J.as<double2>());
-    PCK(cudaStreamSynchronize(s));
-  }
-  c.launches++;
+  PTRY(c.slot_s.alloc(ns * 4));
+  PCK(cudaMemcpyAsync(c.slot_s.p, obs_slot.data(), ns * 4, cudaMemcpyHostToDevice, s));
+  PCK(cudaStreamSynchronize(s));  // obs_slot is a local vector
+  PTRY(alloc_store(c));
   const int64_t nc = n_cam, nlm1 = std::max<int64_t>(nlm, 1);
   for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.bt, &c.xvec, &c.rvec})
     PTRY(b->alloc(nc * 9 * 8));

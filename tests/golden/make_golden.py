@@ -199,7 +199,28 @@ def mixed_bundle():
            lm_cfgs={"lm_mixed": lm.LmConfig(solver="poba", max_outer_iterations=15, max_order=20)})
 
 
+def p32_bundle():
+    """PoBA-32 (precision=32: float32 block storage, float64 reductions) on c1 and mixed."""
+    from paper_2204_12834_b200 import configs
+    out = {}
+    mixed = configs.make_mixed_tracks()
+    probs = {"c1": configs.make_config("c1"),
+             "mixed": bal_io.BalProblem(mixed.camera_params, mixed.points, mixed.cam_indices, mixed.pt_indices,
+                                        mixed.pixels)}
+    for tag, p in probs.items():
+        lin = blocks.linearize(p, precision=32)
+        assert lin.store.storage_obs.dtype == np.float32
+        out.update(lin_outputs(lin, f"{tag}_"))
+        out.update(system_outputs(lin.damp(1e-4), f"{tag}_sys", [(0.01, 20), (1e-300, 12)]))
+        out.update(trace_outputs(lm.run(p, lm.LmConfig(solver="poba", precision=32, max_outer_iterations=12,
+                                                       max_order=20)), f"{tag}_lm32"))
+    np.savez_compressed(os.path.join(HERE, "p32.npz"), **out)
+    print("wrote p32.npz")
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[2] == "p32":
+        return p32_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "pcg":
         return pcg_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "mixed":
@@ -228,6 +249,7 @@ def main():
     explicit_bundle()
     pcg_bundle()
     mixed_bundle()
+    p32_bundle()
 
 
 if __name__ == "__main__":

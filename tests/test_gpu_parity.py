@@ -271,3 +271,35 @@ def test_zero_rhs_and_zero_update(P):
     assert r.converged and r.order_used == 0 and not r.delta_p.any()
     assert not P.back_substitute(s, r.delta_p).any()
     del configs
+
+
+@pytest.mark.parametrize("tag", ["c1", "mixed"])
+def test_poba32(P, tag):
+    """precision=32 (PoBA-32): fp32 block storage, fp64 sums; reference golden p32.npz."""
+    p, _ = golden_problem(tag)
+    z = load_golden("p32")
+    lin = P.linearize(p, precision=32)
+    st = lin.store.storage_obs
+    assert st.dtype == np.float32
+    assert lin.store.block_bytes == p.n_observations * 2 * 13 * 4
+    for key in ("U0", "V0", "b_p", "b_l", "D_p", "D_l"):
+        assert rel(getattr(lin, key), z[f"{tag}_{key}"]) < 1e-11, key
+    s = lin.damp(1e-4)
+    assert rel(s.b_tilde(), z[f"{tag}_sys_b_tilde"]) < INC_TOL
+    for j in range(2):
+        pre = f"{tag}_sys_solve{j}_"
+        r = P.power_series_solve(s, float(z[pre + "eps"]), int(z[pre + "m"]))
+        assert r.order_used == int(z[pre + "order"]) and r.converged == bool(z[pre + "converged"])
+        assert rel(r.delta_p, z[pre + "delta_p"]) < INC_TOL
+        assert rel(P.back_substitute(s, r.delta_p), z[pre + "delta_l"]) < INC_TOL
+    # a float64 linearization of the same problem is still exact after the switch
+    lin64 = P.linearize(p)
+    assert lin64.store.storage_obs.dtype == np.float64
+    assert rel(lin.U0, z[f"{tag}_U0"]) < 1e-11  # cached
+    tr = P.run(p, P.LmConfig(precision=32, max_outer_iterations=12, max_order=20))
+    costs = np.array([i.cost for i in tr.iterations])
+    want = z[f"{tag}_lm32_cost"]
+    assert len(costs) == len(want)
+    assert np.all(np.abs(costs - want) <= COST_TOL * want)
+    assert [i.accepted for i in tr.iterations] == z[f"{tag}_lm32_accepted"].tolist()
+    assert [i.peak_bytes for i in tr.iterations] == z[f"{tag}_lm32_peak_bytes"].tolist()

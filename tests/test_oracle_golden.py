@@ -231,3 +231,27 @@ def test_pcg_lm_trace_matches_reference(tag, solver):
     assert [i.order_m for i in its][1:] == z[t + "_order"].tolist()[1:]
     assert [i.accepted for i in its] == z[t + "_accepted"].tolist()
     np.testing.assert_allclose([i.lam for i in its], z[t + "_lam"], rtol=0)
+
+
+# -- PoBA-32 (precision=32), pinned by tests/golden/p32.npz --------------------------------
+
+@pytest.mark.parametrize("tag", ["c1", "mixed"])
+def test_poba32_matches_reference(tag):
+    p, _ = golden_problem(tag)
+    z = load_golden("p32")
+    lin = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points, precision=32)
+    assert np.array_equal(lin.store.astype(np.float32).astype(np.float64), lin.store)
+    for key in ("U0", "V0", "b_p", "b_l", "D_p", "D_l"):
+        assert rel(getattr(lin, key), z[f"{tag}_{key}"]) < 1e-13, key
+    s = O.OracleSystem(lin, 1e-4)
+    assert rel(s.b_tilde(), z[f"{tag}_sys_b_tilde"]) < 1e-11
+    for j in range(2):
+        pre = f"{tag}_sys_solve{j}_"
+        dp, order, conv = O.series_solve(s, float(z[pre + "eps"]), int(z[pre + "m"]))
+        assert order == int(z[pre + "order"]) and conv == bool(z[pre + "converged"])
+        assert rel(dp, z[pre + "delta_p"]) < 1e-10
+        assert rel(O.back_sub(s, dp), z[pre + "delta_l"]) < 1e-10
+    tr, _, _ = O.lm_run(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points,
+                        max_outer_iterations=12, max_order=20, precision=32)
+    np.testing.assert_allclose([i.cost for i in tr.iterations], z[f"{tag}_lm32_cost"], rtol=1e-10)
+    assert [i.accepted for i in tr.iterations] == z[f"{tag}_lm32_accepted"].tolist()
