@@ -29,7 +29,10 @@ constexpr int kRowBytes = kRow * 16;
 constexpr int kBlockTiles = 8;    // warp-tiles per CTA in the streaming kernels (256 threads)
 constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
 constexpr int kJPlanes = 12;      // Jacobian column pairs per row
-constexpr int kTermWarps = 8;     // warps per CTA of the term kernel (one CTA per SM)
+#ifndef POBA_TERM_WARPS
+#define POBA_TERM_WARPS 12
+#endif
+constexpr int kTermWarps = POBA_TERM_WARPS;  // warps per CTA of the term kernel (one CTA per SM)
 constexpr int kPackWindow = 64;   // landmark lookahead of the tile packer
 constexpr int kTStride = 10;      // doubles per camera record of the term vector / partials (80 B, 16-B aligned)
 // Term-kernel shared memory: per warp one bulk-copy stage (32 rows, the tile
