@@ -119,7 +119,7 @@ bool is_pinned(const void* p) {
 }
 
 void par_memcpy(void* dst, const void* src, size_t bytes) {
-  constexpr size_t kChunk = 8u << 20;
+  constexpr size_t kChunk = 1u << 20;
   const int nt = (int)std::min<size_t>(8, (bytes + kChunk - 1) / kChunk);
   if (nt <= 1) {
     std::memcpy(dst, src, bytes);
@@ -164,11 +164,27 @@ int device_to_host(Ctx& c, void* h_dst, const void* d_src, size_t bytes) {
     PCK(cudaStreamSynchronize(c.stream));
     return POBA_OK;
   }
+  // pipelined: the DMA of piece i+1 overlaps the host copy of piece i
   PTRY(pinned_stage(c, bytes));
-  PCK(cudaMemcpyAsync(c.host_stage, d_src, bytes, cudaMemcpyDeviceToHost, c.stream));
-  PCK(cudaStreamSynchronize(c.stream));
-  par_memcpy(h_dst, c.host_stage, bytes);
-  return POBA_OK;
+  constexpr int kPieces = 8;
+  const size_t piece = ((bytes + kPieces - 1) / kPieces + 4095) & ~(size_t)4095;
+  std::vector<cudaEvent_t> ev;
+  for (size_t o = 0; o < bytes; o += piece) {
+    cudaEvent_t e;
+    PCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    PCK(cudaMemcpyAsync((char*)c.host_stage + o, (const char*)d_src + o, std::min(piece, bytes - o),
+                        cudaMemcpyDeviceToHost, c.stream));
+    PCK(cudaEventRecord(e, c.stream));
+    ev.push_back(e);
+  }
+  int st = POBA_OK;
+  for (size_t k = 0; k < ev.size(); ++k) {
+    const size_t o = k * piece;
+    if (st == POBA_OK && cudaEventSynchronize(ev[k]) != cudaSuccess) st = fail(POBA_ECUDA, "device_to_host");
+    if (st == POBA_OK) par_memcpy((char*)h_dst + o, (const char*)c.host_stage + o, std::min(piece, bytes - o));
+    cudaEventDestroy(ev[k]);
+  }
+  return st;
 }
 
 int lm_upload(Ctx& c, const double* host_full, int width, double* d_local) {
