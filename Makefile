@@ -3,7 +3,10 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 SRC := $(wildcard paper_2204_12834_b200/csrc/*.cu)
-OBJ := $(patsubst paper_2204_12834_b200/csrc/%.cu,build/%.o,$(SRC))
+CPPSRC := $(wildcard paper_2204_12834_b200/csrc/*.cpp)
+OBJ := $(patsubst paper_2204_12834_b200/csrc/%.cu,build/%.o,$(SRC)) $(patsubst paper_2204_12834_b200/csrc/%.cpp,build/%.o,$(CPPSRC))
+CXX ?= g++
+CXXFLAGS := -O3 -std=c++17 -fPIC -Wall
 LIB := paper_2204_12834_b200/lib/libpoba.so
 
 all: $(LIB)
@@ -11,6 +14,10 @@ all: $(LIB)
 build/%.o: paper_2204_12834_b200/csrc/%.cu paper_2204_12834_b200/csrc/poba_internal.h include/poba.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+build/%.o: paper_2204_12834_b200/csrc/%.cpp include/poba.h
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(OBJ)
 	@mkdir -p paper_2204_12834_b200/lib

@@ -36,6 +36,7 @@ extern "C" {
 #define POBA_ECUDA 4      /* CUDA runtime error                            */
 #define POBA_ENCCL 5      /* NCCL error                                    */
 #define POBA_EVANISH 6    /* vanishing iterate norm with nonzero rhs       */
+#define POBA_EPARSE 7     /* malformed BAL text (message as BalParseError) */
 
 typedef struct poba_ctx poba_ctx;
 
@@ -187,6 +188,19 @@ int poba_stream(poba_ctx* ctx, void** stream);
 int poba_shard_bounds(int64_t n_pt, const int64_t* k_per_point, int nranks, int64_t* lm_bounds);
 /* instrumentation counters of POBA_PHASE_TIMING builds (8 x uint64, reset on read) */
 int poba_debug_counters(poba_ctx* ctx, uint64_t* out);
+
+/* ---- native BAL ingest (bal_io.parse_bal / _parse_lines, bal_io.py:180-260) --
+ * Parses BAL text from a path (text-mode line endings) or from an in-memory
+ * buffer (lines end at '\n'), with the reference's token grammar (Python int()
+ * / float()), validation order, pruning of unreferenced cameras and points, and
+ * line-numbered messages (POBA_EPARSE).  Host only; no GPU needed.
+ * info: n_cam, n_pt, n_obs (after pruning), n_pruned_cameras, n_pruned_points.  */
+typedef struct poba_bal poba_bal;
+int poba_bal_parse(const char* path, const char* text, int64_t text_len, poba_bal** out);
+int poba_bal_info(const poba_bal* bal, int64_t* info5);
+int poba_bal_copy(const poba_bal* bal, double* cams, double* points, int64_t* cam_idx, int64_t* pt_idx,
+                  double* pixels);
+int poba_bal_free(poba_bal* bal);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("POBA_LIB") or os.path.join(_HERE, "lib", "libpoba.so")  # POBA_LIB: A/B builds
 
-POBA_OK, POBA_EINVAL, POBA_ENOTSPD, POBA_ENONFINITE, POBA_ECUDA, POBA_ENCCL, POBA_EVANISH = range(7)
+POBA_OK, POBA_EINVAL, POBA_ENOTSPD, POBA_ENONFINITE, POBA_ECUDA, POBA_ENCCL, POBA_EVANISH, POBA_EPARSE = range(8)
 OP_W, OP_WT, OP_U_INV, OP_V_INV, OP_U, OP_SCHUR = range(6)
 (READ_U0, READ_V0, READ_B_P, READ_B_L, READ_D_P, READ_D_L, READ_U, READ_V, READ_U_INV, READ_V_INV,
  READ_B_TILDE, READ_STORAGE) = range(12)
@@ -58,6 +58,10 @@ _SIGS = {
     "poba_shard_bounds": (ctypes.c_int, [ctypes.c_int64, _I64P, ctypes.c_int, _I64P]),
     "poba_schur_diagonal": (ctypes.c_int, [_P, _DP]),
     "poba_set_precision": (ctypes.c_int, [_P, ctypes.c_int]),
+    "poba_bal_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(_P)]),
+    "poba_bal_info": (ctypes.c_int, [_P, _I64P]),
+    "poba_bal_copy": (ctypes.c_int, [_P, _DP, _DP, _I64P, _I64P, _DP]),
+    "poba_bal_free": (ctypes.c_int, [_P]),
     "poba_pcg": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int, _DP,
                                 _IP, _DP, _IP, _DP]),
 }

@@ -24,6 +24,8 @@ class Problem:
     pt_indices: np.ndarray
     pixels: np.ndarray
     name: str = ""
+    n_pruned_cameras: int = 0
+    n_pruned_points: int = 0
 
     def __post_init__(self) -> None:
         # same validation, same messages as bal_io.py:79-98

@@ -218,7 +218,65 @@ def p32_bundle():
     print("wrote p32.npz")
 
 
+BAL_CASES = {
+    # name: text (the reference's own parser decides what each one means)
+    "minimal": "1 1 1\n0 0 1.5 -2.25\n" + " ".join(["0.1"] * 9) + "\n1 2 3\n",
+    "layout_free": "1 1\n1 0 0\n1.5 -2.25 " + " ".join(["0.1"] * 9) + " 1\n2\n\n3",
+    "tabs_crlf": "1\t1\t1\r\n0 0 1.5 -2.25\r\n" + " ".join(["0.1"] * 9) + "\r\n1 2 3\r\n",
+    "numbers": "1 2 2\n0 0 +1_0.5e-1_0 .5\n0_0 1 1 2\n" + " ".join(["0.1"] * 9) + "\n1 2 3 4 5 6\n",
+    "number_forms": "2 2 2\n0 0 1e400 -inf\n1 1 NaN 5.\n" + " ".join(["1E-320"] * 9) + " "
+                    + " ".join(["-0.0"] * 9) + "\n1 2 3 4 5 6\n",
+    "plus_index": "1 1 1\n+0 00 1 2\n" + " ".join(["0.1"] * 9) + "\n1 2 3\n",
+    "prune": "3 3 2\n0 0 1 2\n2 2 3 4\n" + " ".join(["0.1"] * 27) + "\n" + " ".join(["1"] * 9) + "\n",
+    "point_range": "1 1 1\n0 1 1 2\n",
+    "camera_range": "1 1 1\n-1 0 1 2\n",
+    "duplicate": "1 1 2\n0 0 1 2\n0 0 3 4\n",
+    "truncated_obs": "1 1 2\n0 0 1 2\n0\n",
+    "truncated_cam": "1 1 1\n0 0 1 2\n0.1 0.2\n\n\n",
+    "truncated_pt": "1 1 1\n0 0 1 2\n" + " ".join(["0.1"] * 9) + "\n1 2",
+    "non_numeric": "1 1 1\n0 0 abc 2\n",
+    "hex_float": "1 1 1\n0 0 0x1p3 2\n",
+    "underscore_bad": "1 1 1\n0 0 1__0 2\n",
+    "non_integer_index": "1 1 1\n0.0 0 1 2\n",
+    "quote_token": "1 1 1\n0 0 it's 2\n",
+    "trailing": "1 1 1\n0 0 1 2\n" + " ".join(["0.1"] * 9) + "\n1 2 3\n\n4\n",
+    "zero_count": "0 1 1\n",
+    "negative_count": "1 -2 1\n",
+    "empty": "",
+    "header_only": "1 1 1\n",
+    "bad_header": "x 1 1\n",
+    "huge_index": "1 1 1\n123456789012345678901234567890 0 1 2\n",
+}
+
+
+def bal_bundle():
+    """The reference's own parse_bal on a corpus of BAL texts: arrays or error messages."""
+    import io
+    out = {}
+    for name, text in BAL_CASES.items():
+        out[f"{name}_text"] = np.frombuffer(text.encode(), dtype=np.uint8)
+        try:
+            p = bal_io.parse_bal(io.StringIO(text))
+            out[f"{name}_ok"] = np.array(True)
+            for k in ("camera_params", "points", "cam_indices", "pt_indices", "pixels"):
+                out[f"{name}_{k}"] = getattr(p, k)
+            out[f"{name}_pruned"] = np.array([p.n_pruned_cameras, p.n_pruned_points])
+        except Exception as e:  # noqa: BLE001 -- record exactly what the reference raises
+            out[f"{name}_ok"] = np.array(False)
+            out[f"{name}_error"] = np.array(f"{type(e).__name__}: {e}")
+    rig = synthetic.make_rig_problem(pixel_noise=1.0)
+    text = bal_io.serialize_bal(bal_io.perturb(rig, 0.01, seed=0))
+    out["rig_text"] = np.frombuffer(text.encode(), dtype=np.uint8)
+    p = bal_io.parse_bal(io.StringIO(text))
+    for k in ("camera_params", "points", "cam_indices", "pt_indices", "pixels"):
+        out[f"rig_{k}"] = getattr(p, k)
+    np.savez_compressed(os.path.join(HERE, "bal.npz"), **out)
+    print("wrote bal.npz")
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[2] == "bal":
+        return bal_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "p32":
         return p32_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "pcg":
@@ -250,6 +308,7 @@ def main():
     pcg_bundle()
     mixed_bundle()
     p32_bundle()
+    bal_bundle()
 
 
 if __name__ == "__main__":
