@@ -156,6 +156,7 @@ int poba_get_points(poba_ctx* ctx, double* points);
 #define POBA_OP_V_INV 3  /* (3 n_pt) -> (3 n_pt)    */
 #define POBA_OP_U 4      /* (9 n_cam) -> (9 n_cam)  */
 #define POBA_OP_SCHUR 5  /* (9 n_cam) -> (9 n_cam)  */
+#define POBA_OP_WVW 6    /* (9 n_cam) -> (9 n_cam): W V^-1 W^T, one fused pass (spectral.py power iteration) */
 int poba_apply(poba_ctx* ctx, int op, const double* in, double* out);
 
 /* ---- read-back of assembled quantities (parity tests, attributes) ----------- */

@@ -466,6 +466,70 @@ def pcg(system, apply_preconditioner, tol=1e-6, max_iter=500):
 
 
 # ---------------------------------------------------------------------------
+# spectral diagnostics (spectral.py:54-143)
+# ---------------------------------------------------------------------------
+
+def u_inv_sqrt_blocks(system):
+    """spectral.py:46-51: blockwise symmetric inverse square roots of the damped U."""
+    w, Q = np.linalg.eigh(system.U)
+    if w.min() <= 0:
+        raise ValueError("damped pose blocks must be positive definite")
+    return _f64sum("pik,pk,pjk->pij", Q, 1.0 / np.sqrt(w), Q)
+
+
+def estimate_spectral_radius(system, tol=1e-9, max_iter=10000, seed=0):
+    """spectral.py:54-86: power iteration on U^-1/2 W V^-1 W^T U^-1/2; (value, iterations, converged)."""
+    uis = u_inv_sqrt_blocks(system)
+
+    def apply_sym(v):
+        y = _f64sum("pij,pj->pi", uis, v.reshape(system.n_cameras, POSE)).ravel()
+        y = system.apply_w(system.apply_v_inv(system.apply_wt(y)))
+        return _f64sum("pij,pj->pi", uis, y.reshape(system.n_cameras, POSE)).ravel()
+
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(system.n_cameras * POSE)
+    v /= np.linalg.norm(v)
+    est = 0.0
+    for it in range(1, max_iter + 1):
+        w = apply_sym(v)
+        nw = np.linalg.norm(w)
+        if nw == 0.0:
+            return 0.0, it, True
+        new = float(v @ w)
+        v = w / nw
+        if abs(new - est) <= tol * max(abs(new), 1e-300):
+            return new, it, True
+        est = new
+    return est, max_iter, False
+
+
+def _dense(apply, dim):
+    out = np.empty((dim, dim))
+    e = np.zeros(dim)
+    for j in range(dim):
+        e[j] = 1.0
+        out[:, j] = apply(e)
+        e[j] = 0.0
+    return out
+
+
+def verify_error_bound(system, orders):
+    """spectral.py:98-143: (rho, orders, bound, measured, ||U^-1||, ||b_tilde||) from dense factorizations."""
+    orders = np.asarray(sorted(int(m) for m in orders))
+    dim = system.n_cameras * POSE
+    S = _dense(system.apply_schur, dim)
+    bt = system.b_tilde()
+    exact = np.linalg.solve(S, -bt)
+    P = _dense(lambda v: system.apply_u_inv(system.apply_w(system.apply_v_inv(system.apply_wt(v)))), dim)
+    rho = float(np.max(np.abs(np.linalg.eigvals(P))))
+    u_inv_norm = float(np.linalg.norm(_dense(system.apply_u_inv, dim), 2))
+    b_norm = float(np.linalg.norm(bt))
+    bound = rho ** (orders + 1.0) / (1.0 - rho) * u_inv_norm * b_norm
+    measured = np.array([np.linalg.norm(series_apply(system, -bt, int(m)) - exact) for m in orders])
+    return rho, orders, bound, measured, u_inv_norm, b_norm
+
+
+# ---------------------------------------------------------------------------
 # cost, retraction, LM loop (lm.py:107-144, 167-232)
 # ---------------------------------------------------------------------------
 

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("POBA_LIB") or os.path.join(_HERE, "lib", "libpoba.so")  # POBA_LIB: A/B builds
 
 POBA_OK, POBA_EINVAL, POBA_ENOTSPD, POBA_ENONFINITE, POBA_ECUDA, POBA_ENCCL, POBA_EVANISH, POBA_EPARSE = range(8)
-OP_W, OP_WT, OP_U_INV, OP_V_INV, OP_U, OP_SCHUR = range(6)
+OP_W, OP_WT, OP_U_INV, OP_V_INV, OP_U, OP_SCHUR, OP_WVW = range(7)
 (READ_U0, READ_V0, READ_B_P, READ_B_L, READ_D_P, READ_D_L, READ_U, READ_V, READ_U_INV, READ_V_INV,
  READ_B_TILDE, READ_STORAGE) = range(12)
 

@@ -405,6 +405,13 @@ class DampedSystem:
     def apply_u(self, v_p):
         return self._op(_lib.OP_U, np.asarray(v_p, dtype=np.float64).ravel())
 
+    def apply_w_vinv_wt(self, v_p):
+        """W V^-1 W^T v_p in one pass of the fused series-term kernel (pose space to pose space)."""
+        self.counters.w += 1
+        self.counters.wt += 1
+        self.counters.v_inv += 1
+        return self._op(_lib.OP_WVW, np.asarray(v_p, dtype=np.float64).ravel())
+
     def apply_schur(self, v_p):
         """S v = (U - W V^-1 W^T) v, never forming S (blocks.py:252-254)."""
         return self._op(_lib.OP_SCHUR, np.asarray(v_p, dtype=np.float64).ravel())

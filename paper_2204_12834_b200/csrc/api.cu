@@ -560,7 +560,7 @@ int poba_apply(poba_ctx* ctx, int op, const double* in, double* out) {
   if (in_lm) PTRY(poba::lm_upload(c, in, 3, din.as<double>()));
   else PCK(cudaMemcpyAsync(din.p, in, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
   PTRY(poba::apply_op_device(c, op, din.as<double>(), dout.as<double>()));
-  if (op == POBA_OP_W && c.nranks > 1) PTRY(poba::allreduce_sum(c, dout.as<double>(), c.n_cam * 9));
+  // (the camera merge of OP_W / OP_WVW already all-reduces across ranks)
   if (out_lm) {
     PTRY(poba::lm_download(c, dout.as<double>(), 3, out));
   } else {

@@ -1163,6 +1163,14 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
       k_lm_mv<<<grid_for(c.n_lm_l, 256), 256, 0, s>>>(c.Vinv.as<double>(), d_in, c.n_lm_l, d_out);
       c.launches++;
       break;
+    case POBA_OP_WVW: {  // W V^-1 W^T v with one pass of the fused term kernel
+      k_restride<<<grid_for(c.n_cam * 9, 256), 256, 0, s>>>(d_in, 9, c.n_cam, c.tvec.as<double>(), kTStride);
+      c.launches++;
+      PTRY(launch_term(c, kModeTerm, c.tvec.as<double>(), nullptr, false));
+      PTRY(launch_cam(c, kCamMerge, 0, 0.0, false));
+      PCK(cudaMemcpyAsync(d_out, c.rvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, s));
+      break;
+    }
     case POBA_OP_SCHUR: {
       // S v = U v - W V^-1 W^T v
       PTRY(apply_op_device(c, POBA_OP_WT, d_in, c.ltmp.as<double>()));

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["PowerSeriesResult", "stop_criterion", "power_series_solve",
+__all__ = ["PowerSeriesResult", "stop_criterion", "series_terms", "power_series_solve",
            "apply_series_inverse", "back_substitute"]
 
 
@@ -49,6 +49,16 @@ def _device_system(system):
         raise NotImplementedError("series solve with an overridden b_l is not supported on the device")
     system._activate()
     return system
+
+
+def series_terms(system, rhs: np.ndarray):
+    """Yield t_0 = U^-1 rhs, then t_i = (U^-1 W V^-1 W^T) t_{i-1} forever (power_series.py:45-50);
+    each term is one fused device pass."""
+    sys_ = _device_system(system)
+    t = sys_.apply_u_inv(np.asarray(rhs, dtype=np.float64))
+    while True:
+        yield t
+        t = sys_.apply_u_inv(sys_.apply_w_vinv_wt(t))
 
 
 def power_series_solve(system, epsilon: float = 0.01, max_order: int = 20,

@@ -23,7 +23,7 @@ from . import _lib
 from .power_series import _device_system, apply_series_inverse
 
 __all__ = ["CgReport", "pcg", "schur_diagonal_blocks", "make_schur_jacobi_preconditioner",
-           "pcg_schur_jacobi", "pcg_power_series_preconditioner"]
+           "pcg_schur_jacobi", "pcg_power_series_preconditioner", "materialize_schur"]
 
 log = logging.getLogger(__name__)
 
@@ -135,3 +135,16 @@ def pcg_power_series_preconditioner(system, order: int, tol: float = 1e-6, max_i
         raise ValueError("order must be non-negative")
     sys_ = _device_system(system)
     return _pcg_device(sys_, _DevicePreconditioner(sys_, _lib.PRECOND_SERIES, order), tol, max_iter, callback)
+
+
+def materialize_schur(system) -> np.ndarray:
+    """Form S densely by pushing basis vectors through the device Schur operator (solvers.py:124-133)."""
+    sys_ = _device_system(system)
+    dim = sys_.n_pose_params
+    S = np.empty((dim, dim))
+    e = np.zeros(dim)
+    for j in range(dim):
+        e[j] = 1.0
+        S[:, j] = sys_.apply_schur(e)
+        e[j] = 0.0
+    return S

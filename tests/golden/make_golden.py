@@ -274,7 +274,36 @@ def bal_bundle():
     print("wrote bal.npz")
 
 
+def spectral_bundle():
+    """The reference's spectral diagnostics (spectral.py:54-143) on small systems."""
+    from paper_2204_12834_b200 import configs
+    from powerba import spectral
+    out = {}
+    mixed = configs.make_mixed_tracks()
+    probs = {"c1": configs.make_config("c1"),
+             "noisy": bal_io.perturb(synthetic.make_random_problem(4, 60, seed=5, pixel_noise=1.0), 0.01, seed=0),
+             "mixed": bal_io.BalProblem(mixed.camera_params, mixed.points, mixed.cam_indices, mixed.pt_indices,
+                                        mixed.pixels)}
+    for tag, p in probs.items():
+        lin = blocks.linearize(p)
+        for j, lam in enumerate([1e-4, 1.0]):
+            sys_ = lin.damp(lam)
+            pre = f"{tag}_l{j}_"
+            out[pre + "lam"] = np.array(lam)
+            for tol_tag, tol in (("tight", 1e-9), ("loose", 1e-4)):
+                est = spectral.estimate_spectral_radius(sys_, tol=tol, max_iter=20000, seed=0)
+                out[pre + f"rho_{tol_tag}"] = np.array([est.value, est.iterations, est.converged])
+            rep = spectral.verify_error_bound(sys_, [0, 1, 2, 4, 8])
+            out[pre + "rho_dense"] = np.array(rep.rho)
+            out[pre + "bound"], out[pre + "measured"] = rep.bound, rep.measured_error
+            out[pre + "norms"] = np.array([rep.u_inv_norm, rep.b_tilde_norm])
+    np.savez_compressed(os.path.join(HERE, "spectral.npz"), **out)
+    print("wrote spectral.npz")
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[2] == "spectral":
+        return spectral_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "bal":
         return bal_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "p32":
@@ -309,6 +338,7 @@ def main():
     mixed_bundle()
     p32_bundle()
     bal_bundle()
+    spectral_bundle()
 
 
 if __name__ == "__main__":

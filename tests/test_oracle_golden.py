@@ -255,3 +255,26 @@ def test_poba32_matches_reference(tag):
                         max_outer_iterations=12, max_order=20, precision=32)
     np.testing.assert_allclose([i.cost for i in tr.iterations], z[f"{tag}_lm32_cost"], rtol=1e-10)
     assert [i.accepted for i in tr.iterations] == z[f"{tag}_lm32_accepted"].tolist()
+
+
+# -- spectral diagnostics (reference spectral.py), pinned by tests/golden/spectral.npz ------
+
+SPECTRAL = {"c1": "c1", "noisy": "noisy4x60", "mixed": "mixed"}
+
+
+@pytest.mark.parametrize("tag", sorted(SPECTRAL))
+def test_spectral_matches_reference(tag):
+    p, _ = golden_problem(SPECTRAL[tag])
+    z = load_golden("spectral")
+    lin = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points)
+    for j in range(2):
+        pre = f"{tag}_l{j}_"
+        s = O.OracleSystem(lin, float(z[pre + "lam"]))
+        val, it, conv = O.estimate_spectral_radius(s, tol=1e-4, max_iter=20000, seed=0)
+        want = z[pre + "rho_loose"]
+        assert abs(val - want[0]) <= 1e-10 * want[0] and it == int(want[1]) and conv == bool(want[2])
+        rho, orders, bound, measured, un, bn = O.verify_error_bound(s, [0, 1, 2, 4, 8])
+        assert abs(rho - float(z[pre + "rho_dense"])) <= 1e-9
+        np.testing.assert_allclose(measured, z[pre + "measured"], rtol=1e-6)
+        np.testing.assert_allclose(bound, z[pre + "bound"], rtol=1e-6)
+        np.testing.assert_allclose([un, bn], z[pre + "norms"], rtol=1e-12)
