@@ -190,6 +190,22 @@ int poba_shard_bounds(int64_t n_pt, const int64_t* k_per_point, int nranks, int6
 /* instrumentation counters of POBA_PHASE_TIMING builds (8 x uint64, reset on read) */
 int poba_debug_counters(poba_ctx* ctx, uint64_t* out);
 
+/* ---- PoST clustered solve (clustering.py:49-148) ------------------------------
+ * poba_cluster_cameras: host-only greedy covisibility clustering
+ * (cluster_cameras): assignment[n_cam], cluster count, cut observations.
+ * The clustered pose solve runs on a context whose store holds one virtual
+ * landmark per (landmark, cluster) pair: poba_set_dl installs the global
+ * landmark damping diagonal (restrict_system keeps it), and
+ * poba_series_solve_clustered runs every cluster's truncated series at once
+ * with per-cluster stop tests (solve_clustered): order_used = max, converged
+ * = all.                                                                      */
+int poba_cluster_cameras(int64_t n_cam, int64_t n_pt, int64_t n_obs, const int64_t* cam_idx, const int64_t* pt_idx,
+                         int64_t max_cluster_size, int64_t* assignment, int64_t* n_clusters,
+                         int64_t* cut_observations);
+int poba_set_dl(poba_ctx* ctx, const double* d_l);
+int poba_series_solve_clustered(poba_ctx* ctx, const int64_t* cluster_of_cam, int n_clusters, double epsilon,
+                                int max_order, double* delta_p, int* order_used, int* converged);
+
 /* ---- native BAL ingest (bal_io.parse_bal / _parse_lines, bal_io.py:180-260) --
  * Parses BAL text from a path (text-mode line endings) or from an in-memory
  * buffer (lines end at '\n'), with the reference's token grammar (Python int()

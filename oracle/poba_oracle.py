@@ -530,6 +530,68 @@ def verify_error_bound(system, orders):
 
 
 # ---------------------------------------------------------------------------
+# PoST clustering (clustering.py:49-148)
+# ---------------------------------------------------------------------------
+
+def cluster_cameras(cam_idx, pt_idx, n_cam, max_cluster_size):
+    """clustering.py:49-101: (assignment, n_clusters, sizes, cut_observations)."""
+    from collections import Counter
+    order = np.lexsort((cam_idx, pt_idx))
+    ps, cs = np.asarray(pt_idx)[order], np.asarray(cam_idx)[order]
+    bnd = np.flatnonzero(np.diff(ps)) + 1
+    weights = Counter()
+    for cams in np.split(cs, bnd):
+        for i in range(len(cams)):
+            for j in range(i + 1, len(cams)):
+                weights[(int(cams[i]), int(cams[j]))] += 1
+    parent = np.arange(n_cam)
+    size = np.ones(n_cam, dtype=np.int64)
+
+    def find(a):
+        while parent[a] != a:
+            parent[a] = parent[parent[a]]
+            a = parent[a]
+        return a
+    for (ci, cj), _ in sorted(weights.items(), key=lambda kv: (-kv[1], kv[0])):
+        ra, rb = find(ci), find(cj)
+        if ra == rb or size[ra] + size[rb] > max_cluster_size:
+            continue
+        keep, drop = min(ra, rb), max(ra, rb)
+        parent[drop] = keep
+        size[keep] += size[drop]
+    roots = np.array([find(c) for c in range(n_cam)])
+    ur = np.unique(roots)
+    assignment = np.searchsorted(ur, roots)
+    cut = sum(len(c) for c in np.split(assignment[cs], bnd) if np.unique(c).size > 1)
+    return assignment, len(ur), np.bincount(assignment), int(cut)
+
+
+def solve_clustered(lin, lam, assignment, n_clusters, eps, max_order):
+    """clustering.py:104-148: per-cluster restricted systems (global D kept), series solved per cluster."""
+    delta = np.zeros((lin.n_cameras, POSE))
+    order_used, converged = 0, True
+    cs, ps = lin.cam_sorted, lin.pt_sorted
+    for c in range(n_clusters):
+        cams = np.flatnonzero(assignment == c)
+        cam_map = np.full(lin.n_cameras, -1)
+        cam_map[cams] = np.arange(len(cams))
+        mask = np.isin(cs, cams)
+        kept = np.unique(ps[mask])
+        lm_map = np.full(lin.n_points, -1)
+        lm_map[kept] = np.arange(len(kept))
+        rows = lin.store[mask]
+        sub = linearize_explicit(cam_map[cs[mask]], lm_map[ps[mask]], rows[:, :, 0:9], rows[:, :, 9:12],
+                                 rows[:, :, 12], len(cams), len(kept))
+        sub.D_p = lin.D_p[cams]
+        sub.D_l = lin.D_l[kept]
+        dp, order, conv = series_solve(OracleSystem(sub, lam), eps, max_order)
+        delta[cams] = dp.reshape(len(cams), POSE)
+        order_used = max(order_used, order)
+        converged = converged and conv
+    return delta.ravel(), order_used, converged
+
+
+# ---------------------------------------------------------------------------
 # cost, retraction, LM loop (lm.py:107-144, 167-232)
 # ---------------------------------------------------------------------------
 

@@ -58,6 +58,11 @@ _SIGS = {
     "poba_shard_bounds": (ctypes.c_int, [ctypes.c_int64, _I64P, ctypes.c_int, _I64P]),
     "poba_schur_diagonal": (ctypes.c_int, [_P, _DP]),
     "poba_set_precision": (ctypes.c_int, [_P, ctypes.c_int]),
+    "poba_cluster_cameras": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I64P, _I64P,
+                                            ctypes.c_int64, _I64P, _I64P, _I64P]),
+    "poba_set_dl": (ctypes.c_int, [_P, _DP]),
+    "poba_series_solve_clustered": (ctypes.c_int, [_P, _I64P, ctypes.c_int, ctypes.c_double, ctypes.c_int, _DP,
+                                                   _IP, _IP]),
     "poba_bal_parse": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(_P)]),
     "poba_bal_info": (ctypes.c_int, [_P, _I64P]),
     "poba_bal_copy": (ctypes.c_int, [_P, _DP, _DP, _I64P, _I64P, _DP]),
@@ -126,6 +131,17 @@ def shard_bounds(k_per_point, nranks: int) -> np.ndarray:
     return out
 
 
+def cluster_cameras(n_cam, n_pt, cam_idx, pt_idx, max_cluster_size):
+    """Host-only covisibility clustering (clustering.py:49-101): (assignment, n_clusters, cut)."""
+    ci = np.ascontiguousarray(cam_idx, dtype=np.int64)
+    pi = np.ascontiguousarray(pt_idx, dtype=np.int64)
+    out = np.empty(int(n_cam), dtype=np.int64)
+    nc, cut = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(load().poba_cluster_cameras(int(n_cam), int(n_pt), len(ci), _i64(ci), _i64(pi), int(max_cluster_size),
+                                       _i64(out), ctypes.byref(nc), ctypes.byref(cut)))
+    return out, int(nc.value), int(cut.value)
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(load().poba_nccl_unique_id(ctypes.cast(buf, _P)))
@@ -146,6 +162,7 @@ class Device:
         self._h = h
         self._lib = lib
         self.rank, self.nranks = rank, nranks
+        self.device = device
         self.precision = 64
         self.n_cam = self.n_pt = self.n_obs = 0
 
@@ -240,6 +257,18 @@ class Device:
         """Block storage precision 64 or 32 (PoBA-32); invalidates the linearization."""
         _check(self._lib.poba_set_precision(self._h, int(bits)))
         self.precision = int(bits)
+
+    def set_dl(self, d_l):
+        """Override the landmark damping diagonal D_l (n_pt, 3) of the current linearization."""
+        _check(self._lib.poba_set_dl(self._h, _d(_f64(d_l, (self.n_pt, 3)))))
+
+    def series_solve_clustered(self, cluster_of_cam, n_clusters, epsilon, max_order):
+        dp = np.empty(9 * self.n_cam)
+        order, conv = ctypes.c_int(0), ctypes.c_int(0)
+        cl = np.ascontiguousarray(cluster_of_cam, dtype=np.int64)
+        _check(self._lib.poba_series_solve_clustered(self._h, _i64(cl), int(n_clusters), float(epsilon),
+                                                     int(max_order), _d(dp), ctypes.byref(order), ctypes.byref(conv)))
+        return dp, int(order.value), bool(conv.value)
 
     def schur_diagonal(self):
         out = np.empty((self.n_cam, 9, 9))

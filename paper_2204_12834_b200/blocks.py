@@ -53,6 +53,7 @@ class DeviceProblem:
         self.n_cameras, self.n_points = int(n_cameras), int(n_points)
         self.n_observations = len(cam_indices)
         self.dev.set_problem(n_cameras, n_points, cam_indices, pt_indices, pixels)
+        self.cam_indices, self.pt_indices, self.pixels = cam_indices, pt_indices, pixels  # by reference
         self.generation = 0          # bumped by every (re)linearization
         self.active_system = None    # DampedSystem whose damping is on the device
         self.source = None           # what produced the current linearization

@@ -461,6 +461,32 @@ int poba_series_apply(poba_ctx* ctx, const double* v, int order, double* out) {
   return POBA_OK;
 }
 
+// PoST: landmark damping diagonal override (restrict_system keeps the global D_l,
+// clustering.py:118-119) and the clustered series with per-cluster stop tests
+int poba_set_dl(poba_ctx* ctx, const double* d_l) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_lin, "no linearization");
+  NEED(d_l, "null D_l");
+  PTRY(poba::lm_upload(c, d_l, 3, c.Dl.as<double>()));
+  PCK(cudaStreamSynchronize(c.stream));
+  c.have_damp = c.have_solution = c.have_delta_l = false;
+  return POBA_OK;
+}
+
+int poba_series_solve_clustered(poba_ctx* ctx, const int64_t* cluster_of_cam, int n_clusters, double epsilon,
+                                int max_order, double* delta_p, int* order_used, int* converged) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  NEED(cluster_of_cam && n_clusters >= 1, "no clustering");
+  NEED(order_used && converged, "null outputs");
+  if (max_order < 0) return poba::fail(POBA_EINVAL, "max_order must be non-negative");
+  if (!(epsilon > 0)) return poba::fail(POBA_EINVAL, "epsilon must be positive");
+  return poba::series_clustered_device(c, cluster_of_cam, n_clusters, epsilon, max_order, delta_p, order_used,
+                                       converged);
+}
+
 int poba_schur_diagonal(poba_ctx* ctx, double* blocks_81) {
   CTX_CHECK(ctx);
   Ctx& c = ctx->c;

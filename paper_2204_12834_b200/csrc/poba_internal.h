@@ -329,6 +329,8 @@ int cameras_prep(Ctx& c, const double* d_cams, double* d_prep);
 int allreduce_sum(Ctx& c, double* d_buf, size_t n);
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches);
 int set_precision_device(Ctx& c, int bits);
+int series_clustered_device(Ctx& c, const int64_t* h_cluster_of_cam, int n_clusters, double eps, int max_order,
+                            double* h_delta_p, int* order_used, int* converged);
 int b_tilde_device(Ctx& c);
 int schur_diag_device(Ctx& c, double* d_out45);
 int pcg_device(Ctx& c, int precond, int order, double tol, int max_iter, bool resume, double* h_delta_p,

@@ -990,6 +990,13 @@ int damp_device(Ctx& c, double lam, int identity) {
   return POBA_OK;
 }
 
+// entry points for the clustered (PoST) series in clustered.cu
+int launch_term_mode(Ctx& c, int mode, const double* tin, const double* lvec, bool check_stop) {
+  PTRY(configure_term(c));
+  return launch_term(c, mode, tin, lvec, check_stop);
+}
+int launch_merge(Ctx& c) { return launch_cam(c, kCamMerge, 0, 0.0, false); }
+
 // the launches of one series solve (b_tilde, t0, then max_order terms; every
 // kernel checks the device-side stop flag, so the sequence is fixed)
 int enqueue_series(Ctx& c, double eps, int max_order, bool forced) {

@@ -301,7 +301,42 @@ def spectral_bundle():
     print("wrote spectral.npz")
 
 
+def post_bundle():
+    """The reference's PoST pieces (clustering.py): covisibility clusters, clustered solves, LM(post)."""
+    from paper_2204_12834_b200 import configs
+    from powerba import clustering
+    out = {}
+    mixed = configs.make_mixed_tracks()
+    probs = {"c1": configs.make_config("c1"),
+             "mixed": bal_io.BalProblem(mixed.camera_params, mixed.points, mixed.cam_indices, mixed.pt_indices,
+                                        mixed.pixels),
+             "c2": configs.make_config("c2")}
+    for tag, p in probs.items():
+        lin = blocks.linearize(p)
+        for size in (1, 5, 16, 1000):
+            part = clustering.cluster_cameras(p, size)
+            pre = f"{tag}_s{size}_"
+            out[pre + "assignment"] = part.assignment
+            out[pre + "meta"] = np.array([part.n_clusters, part.cut_observations])
+            out[pre + "sizes"] = part.sizes
+            if tag != "c2":
+                for j, lam in enumerate([1e-4, 1.0]):
+                    sys_ = lin.damp(lam)
+                    for k, (eps, m) in enumerate([(0.01, 20), (1e-300, 6)]):
+                        r = clustering.solve_clustered(sys_, part, eps, m)
+                        q = pre + f"l{j}_e{k}_"
+                        out[q + "delta_p"] = r.delta_p
+                        out[q + "order_conv"] = np.array([r.order_used, r.converged])
+        if tag != "c2":
+            tr = lm.run(p, lm.LmConfig(solver="post", max_cluster_size=5, max_outer_iterations=10, max_order=20))
+            out.update(trace_outputs(tr, f"{tag}_lm_post"))
+    np.savez_compressed(os.path.join(HERE, "post.npz"), **out)
+    print("wrote post.npz")
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[2] == "post":
+        return post_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "spectral":
         return spectral_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "bal":
@@ -339,6 +374,7 @@ def main():
     p32_bundle()
     bal_bundle()
     spectral_bundle()
+    post_bundle()
 
 
 if __name__ == "__main__":

@@ -278,3 +278,28 @@ def test_spectral_matches_reference(tag):
         np.testing.assert_allclose(measured, z[pre + "measured"], rtol=1e-6)
         np.testing.assert_allclose(bound, z[pre + "bound"], rtol=1e-6)
         np.testing.assert_allclose([un, bn], z[pre + "norms"], rtol=1e-12)
+
+
+# -- PoST clustering (reference clustering.py), pinned by tests/golden/post.npz -------------
+
+POST = {"c1": "c1", "mixed": "mixed", "c2": "c2"}
+
+
+@pytest.mark.parametrize("tag", sorted(POST))
+def test_post_clustering_matches_reference(tag):
+    p, _ = golden_problem(POST[tag])
+    z = load_golden("post")
+    lin = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points) if tag != "c2" else None
+    for size in (1, 5, 16, 1000):
+        pre = f"{tag}_s{size}_"
+        a, n, sizes, cut = O.cluster_cameras(p.cam_indices, p.pt_indices, p.n_cameras, size)
+        assert np.array_equal(a, z[pre + "assignment"]) and [n, cut] == z[pre + "meta"].tolist()
+        assert np.array_equal(sizes, z[pre + "sizes"])
+        if lin is None:
+            continue
+        for j, lam in enumerate([1e-4, 1.0]):
+            for k, (eps, m) in enumerate([(0.01, 20), (1e-300, 6)]):
+                q = pre + f"l{j}_e{k}_"
+                dp, order, conv = O.solve_clustered(lin, lam, a, n, eps, m)
+                assert [order, conv] == z[q + "order_conv"].tolist()
+                assert rel(dp, z[q + "delta_p"]) < 1e-10
