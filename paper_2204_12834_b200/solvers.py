@@ -23,7 +23,11 @@ from . import _lib
 from .power_series import _device_system, apply_series_inverse
 
 __all__ = ["CgReport", "pcg", "schur_diagonal_blocks", "make_schur_jacobi_preconditioner",
-           "pcg_schur_jacobi", "pcg_power_series_preconditioner", "materialize_schur"]
+           "pcg_schur_jacobi", "pcg_power_series_preconditioner", "materialize_schur", "dense_direct",
+           "DENSE_DIM_LIMIT"]
+
+# dense_direct refuses anything larger than this many pose parameters (solvers.py:17)
+DENSE_DIM_LIMIT = 2000
 
 log = logging.getLogger(__name__)
 
@@ -148,3 +152,22 @@ def materialize_schur(system) -> np.ndarray:
         S[:, j] = sys_.apply_schur(e)
         e[j] = 0.0
     return S
+
+
+def dense_direct(system) -> np.ndarray:
+    """Solve S dx_p = -b_tilde by dense Cholesky; oracle-scale only (solvers.py:136-151).
+
+    The columns of S come from the device Schur operator; the <= 2000 x 2000
+    factorization itself is host LAPACK, as in the reference.
+    """
+    import scipy.linalg
+    sys_ = _device_system(system)
+    dim = sys_.n_pose_params
+    if dim > DENSE_DIM_LIMIT:
+        raise ValueError(f"dense solve refused: {dim} pose parameters exceeds limit {DENSE_DIM_LIMIT}")
+    S = materialize_schur(sys_)
+    try:
+        factor = scipy.linalg.cho_factor(S)
+    except np.linalg.LinAlgError as exc:
+        raise ValueError(f"materialized reduced system is not SPD: {exc}") from None
+    return scipy.linalg.cho_solve(factor, -sys_.b_tilde())

@@ -334,7 +334,24 @@ def post_bundle():
     print("wrote post.npz")
 
 
+def direct_bundle():
+    """The reference's dense_direct (solvers.py:136-151) and lm.run(solver="direct")."""
+    from paper_2204_12834_b200 import configs
+    out = {}
+    probs = {"c1": configs.make_config("c1"),
+             "noisy": bal_io.perturb(synthetic.make_random_problem(4, 60, seed=5, pixel_noise=1.0), 0.01, seed=0)}
+    for tag, p in probs.items():
+        lin = blocks.linearize(p)
+        for j, lam in enumerate([1e-4, 1.0]):
+            out[f"{tag}_l{j}_delta_p"] = solvers.dense_direct(lin.damp(lam))
+        out.update(trace_outputs(lm.run(p, lm.LmConfig(solver="direct", max_outer_iterations=10)), f"{tag}_lm_direct"))
+    np.savez_compressed(os.path.join(HERE, "direct.npz"), **out)
+    print("wrote direct.npz")
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[2] == "direct":
+        return direct_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "post":
         return post_bundle()
     if len(sys.argv) > 2 and sys.argv[2] == "spectral":
@@ -375,6 +392,7 @@ def main():
     bal_bundle()
     spectral_bundle()
     post_bundle()
+    direct_bundle()
 
 
 if __name__ == "__main__":
