@@ -34,7 +34,7 @@ def test_dense_direct_and_lm(tag):
 def test_dense_direct_refuses_large():
     import paper_2204_12834_b200 as P
     from paper_2204_12834_b200 import configs, solvers
-    p = configs.make_config("c3", 0.02)  # 1200 cameras -> 10800 pose parameters
+    p = configs.make_config("c3", 0.25)  # 300 cameras -> 2700 pose parameters
     assert 9 * p.n_cameras > solvers.DENSE_DIM_LIMIT
     with pytest.raises(ValueError, match="dense solve refused"):
         solvers.dense_direct(P.assemble(p, lam=1e-4))
