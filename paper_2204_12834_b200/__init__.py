@@ -14,4 +14,6 @@ from .problem import Problem  # noqa: F401
 from .solvers import (CgReport, make_schur_jacobi_preconditioner, pcg, pcg_power_series_preconditioner,  # noqa: F401
                       pcg_schur_jacobi, schur_diagonal_blocks)
 
+from . import bal_io, clustering, solvers, spectral  # noqa: F401,E402
+
 __version__ = "0.1.0"

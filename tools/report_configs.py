@@ -31,17 +31,17 @@ sys.path.insert(0, REPO)
 from bench import kernel_bytes, measured_peak, term_bytes  # noqa: E402
 
 
-def series_throughput(problem, lam, reps=20):
+def series_throughput(problem, lam, reps=20, precision=64):
     import paper_2204_12834_b200 as P
-    s = P.assemble(problem, lam=lam)
+    s = P.assemble(problem, lam=lam, precision=precision)
     dev = s._dp.dev
     info = dev.info()
     P.power_series_solve(s, 1e-300, 4)
     ms_term, ms_kernel, launches = dev.time_terms(reps)
     n_o, n_l, n_c = problem.n_observations, problem.n_points, problem.n_cameras
     peak, kind = measured_peak()
-    kb = kernel_bytes(n_o, n_l, n_c)
-    tb = term_bytes(n_o, n_l, n_c)
+    kb = kernel_bytes(n_o, n_l, n_c) - (96 * n_o if precision == 32 else 0)
+    tb = term_bytes(n_o, n_l, n_c) - (96 * n_o if precision == 32 else 0)
     return {"terms_per_s": 1e3 / ms_term, "obs_per_s": n_o * 1e3 / ms_term, "ms_per_term": ms_term,
             "ms_term_kernel": ms_kernel, "launches_per_term": launches,
             "term_gbs": tb / (ms_term / 1e3) / 1e9, "term_frac": tb / (ms_term / 1e3) / 1e9 / peak,
@@ -50,10 +50,10 @@ def series_throughput(problem, lam, reps=20):
             "device_bytes": info["device_bytes"]}
 
 
-def gpu_lm(problem, st, solver="poba"):
+def gpu_lm(problem, st, solver="poba", precision=64):
     from paper_2204_12834_b200 import lm
     cfg = lm.LmConfig(solver=solver, max_outer_iterations=st.max_outer_iterations, epsilon=st.epsilon,
-                      max_order=st.max_order, initial_lambda=st.initial_lambda)
+                      max_order=st.max_order, initial_lambda=st.initial_lambda, precision=precision)
     t0 = time.perf_counter()
     tr = lm.run(problem, cfg)
     wall = time.perf_counter() - t0
@@ -85,7 +85,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1,c2,c3,c3m64,c4,c5")
     ap.add_argument("--ref", default="c1,c2")
-    ap.add_argument("--solvers", default="poba,pcg,pcg-power", help="GPU LM inner solvers to time")
+    ap.add_argument("--solvers", default="poba,pcg,pcg-power,post,poba32", help="GPU LM inner solvers to time")
     ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "configs.json"))
     args = ap.parse_args()
     from paper_2204_12834_b200 import configs
@@ -101,12 +101,16 @@ def main():
                "lm_settings": {"max_outer_iterations": st.max_outer_iterations, "max_order": st.max_order,
                                "epsilon": st.epsilon, "initial_lambda": st.initial_lambda}}
         rec["series"] = series_throughput(problem, st.initial_lambda)
+        rec["series_poba32"] = series_throughput(problem, st.initial_lambda, precision=32)
         rec["gpu_lm"] = gpu_lm(problem, st)
         runs = {"gpu": rec["gpu_lm"]}
         for solver in args.solvers.split(","):
             if solver and solver != "poba":
                 key = "gpu_" + solver.replace("-", "_")
-                rec[key + "_lm"] = gpu_lm(problem, st, solver)
+                if solver == "poba32":
+                    rec[key + "_lm"] = gpu_lm(problem, st, "poba", precision=32)
+                else:
+                    rec[key + "_lm"] = gpu_lm(problem, st, solver)
                 runs[key] = rec[key + "_lm"]
         if name in refs:
             rec["ref_lm"] = ref_lm(problem, st)
