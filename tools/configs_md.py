@@ -1,0 +1,51 @@
+"""Render a tools/report_configs.py JSON as the markdown summary kept under profiles/."""
+import json
+import sys
+
+d = json.load(open(sys.argv[1]))
+title = sys.argv[2] if len(sys.argv) > 2 else "per-config report"
+out = [f"# {title}", "",
+       f"One B200; host CPUs on the GPU box: {d['host_cpus']}. Series throughput: device events over 20 forced "
+       "terms (`time_terms`), algorithmic bytes per SURVEY §8(d) (PoBA-32: 100 instead of 196 B per observation). "
+       "LM: full `lm.run` on the GPU (device store already built) for each inner solver, and the reference "
+       "algorithm's LM (`oracle.poba_oracle.lm_run`, numpy, one core) on the same input where feasible. Time to "
+       "1%: first trace time with cost ≤ f* + 0.01 (f0 − f*), f* = smallest final cost over the runs compared "
+       "(evalkit.py:66-89).", "", "## Series term throughput", "",
+       "| config | N_cam | N_pt | N_obs | terms/s | obs/s | term-kernel GB/s | frac of measured peak | PoBA-32 terms/s | chunks | partials |",
+       "|---|---|---|---|---|---|---|---|---|---|---|"]
+for k, r in d["configs"].items():
+    s = r["series"]
+    s32 = r.get("series_poba32", {})
+    out.append(f"| {k} | {r['n_cameras']:,} | {r['n_points']:,} | {r['n_observations']:,} | {s['terms_per_s']:,.0f} | "
+               f"{s['obs_per_s']:.3g} | {s['kernel_gbs']:,.0f} | {s['kernel_frac']:.2f} | "
+               f"{s32.get('terms_per_s', float('nan')):,.0f} | {s['n_chunks']} | {s['n_partials']:,} |")
+out += ["", "## Time to 1% cost (seconds) and final cost", ""]
+cols = [("gpu", "PoBA GPU"), ("gpu_poba32", "PoBA-32 GPU"), ("gpu_pcg", "PCG Schur-Jacobi GPU"),
+        ("gpu_pcg_power", "PCG power GPU"), ("gpu_post", "PoST GPU"), ("ref", "PoBA reference CPU")]
+out.append("| config | LM settings | " + " | ".join(c[1] for c in cols) + " | final cost PoBA GPU | final cost reference | max per-iteration cost rel diff GPU vs reference |")
+out.append("|---|---|" + "---|" * len(cols) + "---|---|---|")
+
+
+def cell(r, key):
+    lm_key = {"gpu": "gpu_lm", "ref": "ref_lm"}.get(key, key + "_lm")
+    run = r.get(lm_key)
+    if run is None:
+        return "not run"
+    if "error" in run:
+        return "failed: " + run["error"].split(":")[-1].strip()
+    t = r["time_to_1pct_s"].get(key)
+    return "not reached" if t is None else f"{t:.4g}"
+
+
+for k, r in d["configs"].items():
+    st = r["lm_settings"]
+    ref_final = f"{r['ref_lm']['costs'][-1]:.10g}" if "ref_lm" in r else "not run"
+    diff = f"{max(r['cost_rel_diff_per_iter']):.1e}" if "cost_rel_diff_per_iter" in r else "—"
+    out.append(f"| {k} | m={st['max_order']}, ε={st['epsilon']}, ≤{st['max_outer_iterations']} its | "
+               + " | ".join(cell(r, c[0]) for c in cols)
+               + f" | {r['gpu_lm']['costs'][-1]:.10g} | {ref_final} | {diff} |")
+out += ["", "C4/C5 reference LM runs are estimated at hours (SURVEY §8(d)) and were not run; their f* comes from "
+        "the GPU runs. PCG at C5 breaks down (p·Sp ≤ 0 in fp64 on the ill-conditioned λ = 1e-4 system), which "
+        "the reference's own `pcg` asserts on as well. PoST uses `max_cluster_size` = 100 (LmConfig default); its "
+        "time includes the host covisibility clustering."]
+print("\n".join(out))

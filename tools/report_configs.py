@@ -87,10 +87,13 @@ def main():
     ap.add_argument("--ref", default="c1,c2")
     ap.add_argument("--solvers", default="poba,pcg,pcg-power,post,poba32", help="GPU LM inner solvers to time")
     ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "configs.json"))
+    ap.add_argument("--merge", default=None, help="existing report to add these configs to")
     args = ap.parse_args()
     from paper_2204_12834_b200 import configs
     refs = set(x for x in args.ref.split(",") if x)
     out = {"host_cpus": os.cpu_count(), "configs": {}}
+    if args.merge and os.path.exists(args.merge):
+        out = json.load(open(args.merge))
     for name in args.configs.split(","):
         t = time.perf_counter()
         problem = configs.make_config(name, 1.0, seed=0)
@@ -107,11 +110,14 @@ def main():
         for solver in args.solvers.split(","):
             if solver and solver != "poba":
                 key = "gpu_" + solver.replace("-", "_")
-                if solver == "poba32":
-                    rec[key + "_lm"] = gpu_lm(problem, st, "poba", precision=32)
-                else:
-                    rec[key + "_lm"] = gpu_lm(problem, st, solver)
-                runs[key] = rec[key + "_lm"]
+                try:
+                    if solver == "poba32":
+                        rec[key + "_lm"] = gpu_lm(problem, st, "poba", precision=32)
+                    else:
+                        rec[key + "_lm"] = gpu_lm(problem, st, solver)
+                    runs[key] = rec[key + "_lm"]
+                except (AssertionError, ValueError) as e:  # e.g. PCG breakdown (the reference asserts too)
+                    rec[key + "_lm"] = {"error": f"{type(e).__name__}: {e}"}
         if name in refs:
             rec["ref_lm"] = ref_lm(problem, st)
             runs["ref"] = rec["ref_lm"]
