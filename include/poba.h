@@ -187,8 +187,6 @@ int poba_stream(poba_ctx* ctx, void** stream);
 /* landmark bounds [lm_bounds[r], lm_bounds[r+1]) of each rank's shard, as
  * poba_create_sharded contexts choose them (host-only, callable without a GPU) */
 int poba_shard_bounds(int64_t n_pt, const int64_t* k_per_point, int nranks, int64_t* lm_bounds);
-/* instrumentation counters of POBA_PHASE_TIMING builds (8 x uint64, reset on read) */
-int poba_debug_counters(poba_ctx* ctx, uint64_t* out);
 
 /* ---- PoST clustered solve (clustering.py:49-148) ------------------------------
  * poba_cluster_cameras: host-only greedy covisibility clustering

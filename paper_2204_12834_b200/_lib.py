@@ -54,7 +54,6 @@ _SIGS = {
     "poba_time_terms": (ctypes.c_int, [_P, ctypes.c_int, _DP, _DP, _IP]),
     "poba_launch_count": (ctypes.c_int64, [_P]),
     "poba_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
-    "poba_debug_counters": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "poba_shard_bounds": (ctypes.c_int, [ctypes.c_int64, _I64P, ctypes.c_int, _I64P]),
     "poba_schur_diagonal": (ctypes.c_int, [_P, _DP]),
     "poba_set_precision": (ctypes.c_int, [_P, ctypes.c_int]),
@@ -331,11 +330,6 @@ class Device:
 
     def launch_count(self) -> int:
         return int(self._lib.poba_launch_count(self._h))
-
-    def debug_counters(self):
-        out = (ctypes.c_uint64 * 8)()
-        _check(self._lib.poba_debug_counters(self._h, out))
-        return list(out)
 
     def stream_ptr(self) -> int:
         s = _P()

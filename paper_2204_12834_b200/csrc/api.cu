@@ -715,19 +715,6 @@ int poba_shard_bounds(int64_t n_pt, const int64_t* k_per_point, int nranks, int6
   return POBA_OK;
 }
 
-// instrumentation (POBA_PHASE_TIMING builds): read and reset 8 counters
-int poba_debug_counters(poba_ctx* ctx, uint64_t* out) {
-  CTX_CHECK(ctx);
-  Ctx& c = ctx->c;
-  PTRY(c.dbg.alloc(64));
-  if (out) {
-    PTRY(poba::copy_sync(c, out, c.dbg.p, 64, cudaMemcpyDeviceToHost));
-  }
-  PCK(cudaMemsetAsync(c.dbg.p, 0, 64, c.stream));
-  PCK(cudaStreamSynchronize(c.stream));
-  return POBA_OK;
-}
-
 int poba_stream(poba_ctx* ctx, void** stream) {
   NEED(ctx && stream, "null argument");
   *stream = (void*)ctx->c.stream;

@@ -278,7 +278,6 @@ struct Ctx {
   DBuf ctmp;         // double [n_cam*kTStride] scratch
   DBuf ctmp2;        // double [n_cam*kTStride]
   DBuf flag;         // int [16]
-  DBuf dbg;          // instrumentation counters (POBA_PHASE_TIMING builds)
   DBuf red;          // double scratch for reductions
   DBuf cub_tmp;      // CUB temp storage
 
