@@ -303,3 +303,40 @@ def test_poba32(P, tag):
     assert np.all(np.abs(costs - want) <= COST_TOL * want)
     assert [i.accepted for i in tr.iterations] == z[f"{tag}_lm32_accepted"].tolist()
     assert [i.peak_bytes for i in tr.iterations] == z[f"{tag}_lm32_peak_bytes"].tolist()
+
+
+def test_nccl_context_single_rank(P):
+    """A sharded context of world size 1 (NCCL communicator initialised through the
+    dlopen'ed libnccl) gives the same solve as a plain context."""
+    import ctypes
+    from paper_2204_12834_b200 import _lib
+    import torch  # noqa: F401  -- bind the process's libnccl first, as bench.py does
+    p, z = golden_problem("c1")
+    lib = _lib.load()
+    uid = _lib.nccl_unique_id()
+    h = _lib._P()
+    idbuf = ctypes.create_string_buffer(uid, 128)
+    _lib._check(lib.poba_create_sharded(0, 0, 1, ctypes.cast(idbuf, _lib._P), ctypes.byref(h)))
+    dev = _lib.Device.__new__(_lib.Device)
+    dev._h, dev._lib, dev.rank, dev.nranks, dev.device, dev.precision = h, lib, 0, 1, 0, 64
+    dev.n_cam = dev.n_pt = dev.n_obs = 0
+    dev.set_problem(p.n_cameras, p.n_points, p.cam_indices, p.pt_indices, p.pixels)
+    dev.linearize(p.camera_params, p.points)
+    dev.damp(float(z["lam0"]))
+    dp, order, conv, _ = dev.series_solve(float(z["sys0_solve0_eps"]), int(z["sys0_solve0_m"]))
+    assert order == int(z["sys0_solve0_order"])
+    assert rel(dp, z["sys0_solve0_delta_p"]) < INC_TOL
+    dev.close()
+
+
+def test_series_bitwise_reproducible_at_scale(P):
+    """C3-shaped problem (many chunks, CTA ranges, long runs of the apply chain): two solves agree bitwise."""
+    from paper_2204_12834_b200 import configs
+    p = configs.make_config("c3", 0.1)
+    s = P.assemble(p, lam=1e-4)
+    a = P.power_series_solve(s, 1e-300, 12)
+    b = P.power_series_solve(s, 1e-300, 12)
+    assert np.array_equal(a.delta_p, b.delta_p)
+    s32 = P.assemble(p, lam=1e-4, precision=32)
+    c = P.power_series_solve(s32, 1e-300, 12)
+    assert rel(c.delta_p, a.delta_p) < 1e-3  # PoBA-32 rounds the blocks, not the arithmetic
