@@ -340,3 +340,30 @@ def test_series_bitwise_reproducible_at_scale(P):
     s32 = P.assemble(p, lam=1e-4, precision=32)
     c = P.power_series_solve(s32, 1e-300, 12)
     assert rel(c.delta_p, a.delta_p) < 1e-3  # PoBA-32 rounds the blocks, not the arithmetic
+
+
+def test_concurrent_contexts_match_sequential(P):
+    """Independent problems solved from two host threads at once (one context each, the
+    reference's threaded benchmark pattern, evalkit.py:189-191) equal the sequential runs bitwise."""
+    import threading
+    probs = [golden_problem("c1")[0], golden_problem("noisy4x60")[0]]
+    cfg = P.LmConfig(max_outer_iterations=6, max_order=20)
+
+    def run(p):
+        tr = P.run(p, cfg, return_state=True)
+        return [i.cost for i in tr.iterations], tr.state.camera_params.copy()
+
+    seq = [run(p) for p in probs]
+    probs2 = [golden_problem("c1")[0], golden_problem("noisy4x60")[0]]  # fresh objects -> fresh contexts
+    out = [None, None]
+
+    def worker(i):
+        out[i] = run(probs2[i])
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for (c0, s0), (c1, s1) in zip(seq, out):
+        assert c0 == c1
+        assert np.array_equal(s0, s1)
