@@ -7,18 +7,19 @@
 //     the k-groups of blocks._build_groups (blocks.py:405-417).  libpoba
 //     reproduces it bit-exactly with a stable device radix sort of the packed
 //     key (k, pt, cam) and exports it (order / cam_sorted / pt_sorted / groups);
-//   * the STORE order the kernels stream: landmarks in index order, each
-//     landmark's observations sorted by camera (the within-block order of the
-//     reference), packed into landmark-aligned tiles of <= 256 slots.  Dropping
-//     the k-grouping keeps spatially adjacent landmarks (and therefore the
-//     cameras that see them) in the same tiles and chunks, which is what makes
-//     the shared-memory camera reduction of the series kernel effective.  The
-//     store order changes only fp64 summation order, never which terms are
-//     summed.
-// On top of the tiles it builds chunks (contiguous tile ranges whose distinct
-// cameras fit the shared-memory slot accumulators), the per-tile camera
-// segments and permutation (fixed-order reduction, no fp64 atomics), the
-// camera -> partial CSR, and the camera-major permutation used by U0/b_p.
+//   * the STORE order the kernels stream: each rank's landmarks packed into
+//     warp-tiles of <= 32 observation slots and <= kTileLm landmarks, in index
+//     order with a bounded lookahead (pack_landmarks), each landmark's
+//     observations sorted by camera (the reference's within-block order); the
+//     device numbers landmarks in this packed order.  Dropping the k-grouping
+//     keeps spatially adjacent landmarks (and the cameras that see them)
+//     together.  The store order changes only fp64 summation order, never
+//     which terms are summed.
+// On top of the tiles it builds the term kernel's work plan (one contiguous tile
+// range per SM, cut into chunks whose distinct cameras fit the shared-memory
+// accumulator table; each observation's chunk slot and landmark run in the
+// row metadata), the camera -> partial CSR, and the camera-major permutation
+// used by U0/b_p.
 #include <cub/cub.cuh>
 
 #include <algorithm>
