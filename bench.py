@@ -149,7 +149,9 @@ def cpu_term_timer(problem, lam):
 
     desc = (f"one series term (W^T, V^-1, W, U^-1; reference numpy algorithm, oracle/poba_oracle.py) on "
             f"{sub.n_observations} obs / {sub.n_points} landmarks / {sub.n_cameras} cameras of the same problem "
-            f"(landmark-index prefix), extrapolated per observation to {problem.n_observations} obs")
+            f"(landmark-index prefix), extrapolated per observation to {problem.n_observations} obs; numpy "
+            f"threads unrestricted, effectively one core of {os.cpu_count()} host CPUs (the reference's einsum / "
+            f"np.add.at path is single-threaded)")
     return one_term, sub.n_observations, desc
 
 
