@@ -122,6 +122,30 @@ def _f64(a, shape=None):
     return out
 
 
+_PINNED_MIN_BYTES = 4 << 20
+
+
+def host_empty(shape) -> np.ndarray:
+    """Uninitialised float64 host array for a large device download.
+
+    Large results (Delta x_l, landmark positions: 108 MB at C5) are allocated in
+    page-locked memory from PyTorch's caching host allocator, so the library's
+    device-to-host copy lands with one DMA instead of staging through its pinned
+    buffer and a host copy into freshly faulted pages.  The array owns the
+    block (its base is the pinned tensor); dropping it returns the block to the
+    allocator's cache, so the next call of the same size reuses it.
+    """
+    n = int(np.prod(shape))
+    if n * 8 >= _PINNED_MIN_BYTES:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.empty(n, dtype=torch.float64, pin_memory=True).numpy().reshape(shape)
+        except Exception:  # no usable page-locked allocator: plain pages, staged copy
+            pass
+    return np.empty(shape)
+
+
 def shard_bounds(k_per_point, nranks: int) -> np.ndarray:
     """Landmark bounds of each rank's shard (host-only; same plan as sharded contexts)."""
     k = np.ascontiguousarray(k_per_point, dtype=np.int64)
@@ -217,7 +241,7 @@ class Device:
         if base is not None:
             out = np.array(base, dtype=np.float64, copy=True)
         else:  # a shard fills only its own rows
-            out = np.zeros((self.n_pt, 3)) if self.nranks > 1 else np.empty((self.n_pt, 3))
+            out = np.zeros((self.n_pt, 3)) if self.nranks > 1 else host_empty((self.n_pt, 3))
         _check(self._lib.poba_get_points(self._h, _d(out)))
         return out
 
@@ -288,7 +312,7 @@ class Device:
         nz = ctypes.c_int(0)
         dl = None
         if want_delta_l:  # a shard fills only its own rows
-            dl = np.zeros(3 * self.n_pt) if self.nranks > 1 else np.empty(3 * self.n_pt)
+            dl = np.zeros(3 * self.n_pt) if self.nranks > 1 else host_empty(3 * self.n_pt)
         dp = None if delta_p is None else _f64(delta_p)
         _check(self._lib.poba_back_substitute(self._h, _d(dp), _d(dl), ctypes.byref(nz)))
         return dl, bool(nz.value)
