@@ -223,6 +223,7 @@ struct TermArgs {
   double* partials;
   const SeriesState* st;
   int check_stop;
+  unsigned zero;           // always 0 (opaque to the compiler; see the stage refill)
 };
 
 // One CTA per SM streams a contiguous range of warp-tiles; warp w of the CTA
@@ -372,9 +373,23 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
         jr[p] = valid ? reinterpret_cast<const double2*>(stg)[lane * kRow + p] : make_double2(0.0, 0.0);
       }
     }
-    __syncwarp();  // every lane is done with the stage: refill it with this warp's next tile
-    if (lane == 0 && q + 1 < nq) {
-      issue(ti + kTermWarps, t.nx_n & 0xff, t.nx_n >> 8, t.nx_lm0);
+    // Refill the stage with this warp's next tile.  The bulk copy writes
+    // through the async proxy, which is not ordered behind this warp's
+    // shared-memory reads still queued in the LSU (behind the other warps'
+    // traffic): with the rows L2-resident the copy could land first.  So the
+    // issue waits until every lane's stage reads have returned -- each read
+    // feeds a warp-wide XOR that gates the issue.
+    {
+      unsigned dep = (unsigned)t.n ^ (unsigned)t.nx_lm0 ^ (unsigned)slot ^ (unsigned)last;
+#pragma unroll
+      for (int p = 0; p < kJPlanes; ++p)
+        dep ^= (unsigned)__double2hiint(jr[p].x) ^ (unsigned)__double2hiint(jr[p].y);
+#pragma unroll
+      for (int p = 0; p < 6; ++p) dep ^= (unsigned)__double2hiint(vi[p]);
+      dep = __reduce_xor_sync(0xffffffffu, dep);
+      if (lane == 0 && q + 1 < nq && (dep & a.zero) == 0u) {
+        issue(ti + kTermWarps, t.nx_n & 0xff, t.nx_n >> 8, t.nx_lm0);
+      }
     }
     // phase 1: this lane's camera record from the warp's record table (filled
     // at the end of the previous tile)
@@ -871,6 +886,7 @@ TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_sto
   a.partials = c.partials.as<double>();
   a.st = c.state.as<SeriesState>();
   a.check_stop = check_stop ? 1 : 0;
+  a.zero = 0u;
   return a;
 }
 

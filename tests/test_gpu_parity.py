@@ -329,6 +329,22 @@ def test_nccl_context_single_rank(P):
     dev.close()
 
 
+def test_term_pass_bitwise_repeatable_l2_resident(P):
+    """Stage-refill hazard regression: with the whole store L2-resident (C3 x0.1, 18 MB) the
+    bulk copy of a warp's next tile could overtake that warp's queued shared-memory reads of
+    the current one (2.4% of W V^-1 W^T passes differed before the refill was gated on the
+    reads).  400 passes of the fused term kernel must agree bitwise."""
+    from paper_2204_12834_b200 import configs, _lib
+    p = configs.make_config("c3", 0.1)
+    s = P.assemble(p, lam=1e-4)
+    s._activate()
+    dev = s._dp.dev
+    v = np.random.default_rng(5).standard_normal(9 * p.n_cameras)
+    ref = dev.apply(_lib.OP_WVW, v)
+    bad = sum(not np.array_equal(dev.apply(_lib.OP_WVW, v), ref) for _ in range(400))
+    assert bad == 0
+
+
 def test_series_bitwise_reproducible_at_scale(P):
     """C3-shaped problem (many chunks, CTA ranges, long runs of the apply chain): two solves agree bitwise."""
     from paper_2204_12834_b200 import configs
