@@ -20,6 +20,12 @@ namespace {
 constexpr double kMinDepth = 1e-12;   // camera.py:22
 constexpr double kClampLo = 1e-6;     // blocks.py:36
 constexpr double kClampHi = 1e6;      // blocks.py:37
+// 54 fp64 accumulators per lane (~160 registers): small blocks so that three
+// fit an SM instead of one
+#ifndef POBA_CAM_REDUCE_THREADS
+#define POBA_CAM_REDUCE_THREADS 128
+#endif
+constexpr int kCamReduceThreads = POBA_CAM_REDUCE_THREADS;
 
 // Rotation matrix of an axis-angle vector through the unit quaternion, the
 // same construction scipy uses (from_rotvec -> as_matrix).
@@ -66,6 +72,17 @@ struct ObsModel {
   double jl0[3], jl1[3];  // J_point rows
   bool valid;
 };
+
+// a camera's prepared record (R, t, f, k1, k2, pad): eight 16-B loads
+__device__ __forceinline__ void load_prep(const double* __restrict__ prep, int cam, double* cp) {
+  const double2* src = reinterpret_cast<const double2*>(prep + (int64_t)cam * 16);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 v = __ldg(src + k);
+    cp[2 * k] = v.x;
+    cp[2 * k + 1] = v.y;
+  }
+}
 
 // camera.evaluate for one observation (camera.py:85-135)
 template <bool kJac>
@@ -175,7 +192,9 @@ k_lin_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ 
     } else {
       const int lm = t.lm0 + (is_long ? 0 : lidx_s[o]);
       const double* X = points + (int64_t)lm * 3;
-      evaluate_obs<true>(prep + (int64_t)cam_s[o] * 16, X[0], X[1], X[2], pix_s[o], m);
+      double cp[16];
+      load_prep(prep, cam_s[o], cp);
+      evaluate_obs<true>(cp, X[0], X[1], X[2], pix_s[o], m);
       bad = !m.valid;
     }
     // at precision 32 every stored value is rounded to fp32 first and all
@@ -283,7 +302,7 @@ __device__ __forceinline__ int find_camera(const int* __restrict__ off, int n_ca
 // U0 (packed upper 45) and b_p (9) partial sums over chunks of <= 128 observations
 // of one camera, walked in camera-major order; fixed warp-butterfly reduction.
 template <bool F32>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kCamReduceThreads)
 k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cam_start,
                    const int* __restrict__ cperm, const void* __restrict__ J,
                    const double2* __restrict__ Rz, int64_t pad, int n_cam, int n_cc,
@@ -376,7 +395,9 @@ k_cost_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__
         X2 += dl[(int64_t)lm * 3 + 2];
       }
       ObsModel m;
-      evaluate_obs<false>(prep + (int64_t)cam_s[o] * 16, X0, X1, X2, pix_s[o], m);
+      double cp[16];
+      load_prep(prep, cam_s[o], cp);
+      evaluate_obs<false>(cp, X0, X1, X2, pix_s[o], m);
       bad = !m.valid;
       v = m.r0 * m.r0 + m.r1 * m.r1;
     }
@@ -469,13 +490,13 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   }
   // camera side: U0 / b_p via camera-major chunks, then a fixed-order merge
   if (c.n_cchunks) {
-    const unsigned g = grid_for((int64_t)c.n_cchunks * 32, 256);
+    const unsigned g = grid_for((int64_t)c.n_cchunks * 32, kCamReduceThreads);
     if (f32)
-      k_cam_chunk_reduce<true><<<g, 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
+      k_cam_chunk_reduce<true><<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
                                                  c.J.p, c.Rz.as<double2>(), ns, (int)c.n_cam, c.n_cchunks,
                                                  c.cc_part.as<double>());
     else
-      k_cam_chunk_reduce<false><<<g, 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
+      k_cam_chunk_reduce<false><<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
                                                   c.J.p, c.Rz.as<double2>(), ns, (int)c.n_cam, c.n_cchunks,
                                                   c.cc_part.as<double>());
     c.launches++;
