@@ -1,0 +1,58 @@
+"""Run-to-run bitwise repeatability of every device entry point (``-m gpu``).
+
+The library has no floating-point atomics and fixes every reduction order, so
+repeating a call on the same state must reproduce its output bit for bit.  The
+problems are small enough to be L2-resident, where copy/compute overlap races
+show up (the stage-refill hazard); ``tools/det_sweep.py`` runs
+the same sweep with more repetitions.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPS = 8
+
+
+def _problem(name):
+    from paper_2204_12834_b200 import configs
+    return configs.make_mixed_tracks() if name == "mixed" else configs.make_config(name, 0.1)
+
+
+@pytest.mark.parametrize("name,precision", [("mixed", 64), ("c3", 64), ("mixed", 32)])
+def test_entry_points_bitwise_repeatable(name, precision):
+    import paper_2204_12834_b200 as P
+    from paper_2204_12834_b200 import _lib
+    p = _problem(name)
+    s = P.assemble(p, lam=1e-4, precision=precision)
+    s._activate()
+    dev = s._dp.dev
+    rng = np.random.default_rng(3)
+    vc = rng.standard_normal(9 * p.n_cameras)
+    vl = rng.standard_normal(3 * p.n_points)
+    assign, ncl, _ = _lib.cluster_cameras(p.n_cameras, p.n_points, p.cam_indices, p.pt_indices, 16)
+
+    def lin():
+        dev.linearize(p.camera_params, p.points)
+        dev.damp(1e-4)
+        return np.concatenate([dev.read(k).ravel() for k in (_lib.READ_U0, _lib.READ_V0, _lib.READ_B_P,
+                                                              _lib.READ_B_L, _lib.READ_D_P, _lib.READ_D_L)])
+
+    cases = {
+        "linearize+damp": lin,
+        "series": lambda: dev.series_solve(1e-300, 12)[0],
+        "series_apply": lambda: dev.series_apply(vc, 6),
+        "W": lambda: dev.apply(_lib.OP_W, vl),
+        "WT": lambda: dev.apply(_lib.OP_WT, vc),
+        "WVW": lambda: dev.apply(_lib.OP_WVW, vc),
+        "back_substitute": lambda: (dev.series_solve(1e-2, 20), dev.back_substitute()[0])[1],
+        "cost": lambda: np.array([dev.cost(p.camera_params, p.points)[0]]),
+        "pcg": lambda: dev.pcg(2, 3, 1e-6, 20)[0],
+        "post": lambda: dev.series_solve_clustered(assign, ncl, 1e-2, 20)[0],
+    }
+    for label, fn in cases.items():
+        ref = np.array(fn(), copy=True)
+        for _ in range(REPS):
+            assert np.array_equal(np.asarray(fn()), ref), label
