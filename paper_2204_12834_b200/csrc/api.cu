@@ -1,6 +1,7 @@
 // C-ABI entry points of libpoba (see include/poba.h for the contract and the
 // reference function each entry point replaces).
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -88,15 +89,18 @@ void unpack3(const double* p6, double* out9) {
   for (int q = 0; q < 9; ++q) out9[q] = p6[idx[q]];
 }
 
+}  // namespace
+
 // landmark arrays: this rank owns file landmarks [lm_lo, lm_hi); host arrays are
 // full (n_pt rows, file order); the device keeps them in store order
 // (store j <-> file lm_lo + lm_perm[j]), permuted on the device.
-__global__ void k_lm_gather(const double* __restrict__ src, const int* __restrict__ perm, int64_t n, int width,
-                            double* __restrict__ dst) {
-  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= n * width) return;
+// dst row j <- src row idx[j], j in [j0, j1)
+__global__ void k_lm_gather(const double* __restrict__ src, const int* __restrict__ idx, int64_t j0, int64_t j1,
+                            int width, double* __restrict__ dst) {
+  const int64_t q = j0 * width + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= j1 * width) return;
   const int64_t j = q / width;
-  dst[q] = src[(int64_t)perm[j] * width + (q - j * width)];
+  dst[q] = src[(int64_t)idx[j] * width + (q - j * width)];
 }
 __global__ void k_lm_scatter(const double* __restrict__ src, const int* __restrict__ perm, int64_t n, int width,
                              double* __restrict__ dst) {
@@ -145,7 +149,7 @@ int pinned_stage(Ctx& c, size_t bytes) {
   return POBA_OK;
 }
 
-int host_to_device(Ctx& c, void* d_dst, const void* h_src, size_t bytes) {
+int host_to_device(Ctx& c, void* d_dst, const void* h_src, size_t bytes) {  // synchronous
   if (bytes < (4u << 20) || is_pinned(h_src)) {
     PCK(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, c.stream));
     return POBA_OK;
@@ -191,7 +195,7 @@ int lm_upload(Ctx& c, const double* host_full, int width, double* d_local) {
   if (c.n_lm_l == 0) return POBA_OK;
   PTRY(c.lm_stage.alloc(c.n_lm_l * width * 8));
   PTRY(host_to_device(c, c.lm_stage.p, host_full + c.lm_lo * width, c.n_lm_l * width * 8));
-  k_lm_gather<<<grid_for(c.n_lm_l * width, 256), 256, 0, c.stream>>>(c.lm_stage.as<double>(), c.lm_perm.as<int>(),
+  k_lm_gather<<<grid_for(c.n_lm_l * width, 256), 256, 0, c.stream>>>(c.lm_stage.as<double>(), c.lm_perm.as<int>(), 0,
                                                                      c.n_lm_l, width, d_local);
   c.launches++;
   PCK(cudaGetLastError());
@@ -206,6 +210,96 @@ int lm_download(Ctx& c, const double* d_local, int width, double* host_full) {
   PCK(cudaGetLastError());
   return device_to_host(c, host_full + c.lm_lo * width, c.lm_stage.p, c.n_lm_l * width * 8);
 }
+
+// ---- pipelined landmark transfers (single GPU) ---------------------------------------------
+// The landmark range is cut into kXferPieces file-order pieces (cuts planned in
+// build_structure).  Upload: piece i is copied on the transfer stream while the
+// library stream permutes and consumes the store landmarks whose file rows have
+// all arrived; download: the library stream produces a prefix of store
+// landmarks, permutes the file-order piece it completes, and the transfer
+// stream copies it out while the next prefix is computed.
+bool xfer_pipelined(const Ctx& c, int width) {
+  size_t min_bytes = kXferMinBytes;
+  if (const char* e = getenv("POBA_XFER_MIN_BYTES")) min_bytes = (size_t)strtoull(e, nullptr, 10);  // tests
+  return c.nranks == 1 && (int)c.xf_file.size() == kXferPieces + 1 && c.n_lm_l > 0 &&
+         (size_t)c.n_lm_l * width * 8 >= min_bytes;
+}
+
+int xfer_begin(Ctx& c, int width, bool pinned) {
+  if (!c.xfer) {
+    PCK(cudaStreamCreateWithFlags(&c.xfer, cudaStreamNonBlocking));
+    for (auto& e : c.xfer_ev) PCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const size_t bytes = (size_t)c.n_lm_l * width * 8;
+  PTRY(c.lm_stage.alloc(bytes));
+  if (!pinned) PTRY(pinned_stage(c, bytes));
+  // transfers start after everything already queued on the library stream
+  PCK(cudaEventRecord(c.xfer_ev[2 * kXferPieces], c.stream));
+  PCK(cudaStreamWaitEvent(c.xfer, c.xfer_ev[2 * kXferPieces], 0));
+  return POBA_OK;
+}
+
+int lm_upload_piece(Ctx& c, const double* host_full, int width, double* d_local, int i, bool pinned) {
+  const int64_t f0 = c.xf_file[i], f1 = c.xf_file[i + 1];
+  const size_t off = (size_t)f0 * width * 8, bytes = (size_t)(f1 - f0) * width * 8;
+  const char* src = reinterpret_cast<const char*>(host_full + c.lm_lo * width) + off;
+  char* stage = c.lm_stage.as<char>() + off;
+  if (bytes) {
+    if (pinned) {
+      PCK(cudaMemcpyAsync(stage, src, bytes, cudaMemcpyHostToDevice, c.xfer));
+    } else {  // the host copy of piece i overlaps the device work of piece i - 1
+      par_memcpy(static_cast<char*>(c.host_stage) + off, src, bytes);
+      PCK(cudaMemcpyAsync(stage, static_cast<char*>(c.host_stage) + off, bytes, cudaMemcpyHostToDevice, c.xfer));
+    }
+  }
+  PCK(cudaEventRecord(c.xfer_ev[i], c.xfer));
+  PCK(cudaStreamWaitEvent(c.stream, c.xfer_ev[i], 0));
+  const int64_t s0 = c.xf_up_lm[i], s1 = c.xf_up_lm[i + 1];
+  if (s1 > s0) {
+    k_lm_gather<<<grid_for((s1 - s0) * width, 256), 256, 0, c.stream>>>(c.lm_stage.as<double>(), c.lm_perm.as<int>(),
+                                                                       s0, s1, width, d_local);
+    c.launches++;
+  }
+  PCK(cudaGetLastError());
+  return POBA_OK;
+}
+
+int lm_download_piece(Ctx& c, const double* d_local, int width, double* host_full, int i, bool pinned) {
+  const int64_t f0 = c.xf_file[i], f1 = c.xf_file[i + 1];
+  const size_t off = (size_t)f0 * width * 8, bytes = (size_t)(f1 - f0) * width * 8;
+  if (f1 > f0) {
+    k_lm_gather<<<grid_for((f1 - f0) * width, 256), 256, 0, c.stream>>>(d_local, c.lm_inv.as<int>(), f0, f1, width,
+                                                                       c.lm_stage.as<double>());
+    c.launches++;
+    PCK(cudaGetLastError());
+  }
+  PCK(cudaEventRecord(c.xfer_ev[i], c.stream));
+  PCK(cudaStreamWaitEvent(c.xfer, c.xfer_ev[i], 0));
+  if (bytes) {
+    char* dst = pinned ? reinterpret_cast<char*>(host_full + c.lm_lo * width) + off
+                       : static_cast<char*>(c.host_stage) + off;
+    PCK(cudaMemcpyAsync(dst, c.lm_stage.as<char>() + off, bytes, cudaMemcpyDeviceToHost, c.xfer));
+  }
+  PCK(cudaEventRecord(c.xfer_ev[kXferPieces + i], c.xfer));
+  return POBA_OK;
+}
+
+int lm_download_finish(Ctx& c, double* host_full, int width, bool pinned) {
+  if (!pinned) {  // host copies of finished pieces overlap the DMA of later ones
+    for (int i = 0; i < kXferPieces; ++i) {
+      PCK(cudaEventSynchronize(c.xfer_ev[kXferPieces + i]));
+      const size_t off = (size_t)c.xf_file[i] * width * 8;
+      const size_t bytes = (size_t)(c.xf_file[i + 1] - c.xf_file[i]) * width * 8;
+      if (bytes)
+        par_memcpy(reinterpret_cast<char*>(host_full + c.lm_lo * width) + off,
+                   static_cast<char*>(c.host_stage) + off, bytes);
+    }
+  }
+  PCK(cudaStreamSynchronize(c.xfer));
+  return POBA_OK;
+}
+
+namespace {
 
 int copy_down(Ctx& c, const DBuf& src, size_t bytes, std::vector<double>& out) {
   out.resize(bytes / 8);
@@ -403,10 +497,13 @@ int poba_linearize(poba_ctx* ctx, const double* cam_params, const double* points
   NEED(c.have_problem, "no problem set");
   NEED(c.have_pixels, "problem was set without pixels");
   NEED(cam_params, "null camera parameters");
-  if (points) PTRY(poba_set_points(ctx, points));
-  NEED(c.have_points, "no points (pass them or call poba_set_points)");
+  const bool piped = points && poba::xfer_pipelined(c, 3);
+  if (points && !piped) PTRY(poba_set_points(ctx, points));
+  NEED(piped || c.have_points, "no points (pass them or call poba_set_points)");
   PCK(cudaMemcpyAsync(c.cams.p, cam_params, c.n_cam * 9 * 8, cudaMemcpyHostToDevice, c.stream));
-  PTRY(poba::linearize_device(c, false, nullptr, nullptr, nullptr));
+  const int st = poba::linearize_device(c, false, nullptr, nullptr, nullptr, piped ? points : nullptr);
+  if (piped) c.have_points = st == POBA_OK;  // the device copy now holds these points
+  PTRY(st);
   if (n_invalid) *n_invalid = c.n_invalid;
   return POBA_OK;
 }
@@ -536,9 +633,8 @@ int poba_back_substitute(poba_ctx* ctx, const double* delta_p, double* delta_l, 
     NEED(c.have_solution, "no series solution on the device");
   }
   int nz = 0;
-  PTRY(poba::back_substitute_device(c, d_dp, &nz));
+  PTRY(poba::back_substitute_device(c, d_dp, &nz, delta_l));
   if (nonzero) *nonzero = nz;
-  if (delta_l) PTRY(poba::lm_download(c, c.dl.as<double>(), 3, delta_l));
   return POBA_OK;
 }
 

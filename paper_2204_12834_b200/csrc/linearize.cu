@@ -148,7 +148,7 @@ __device__ __forceinline__ void evaluate_obs(const double* __restrict__ cp, doub
 // same order).
 template <bool kExplicit, bool F32>
 __global__ void __launch_bounds__(kBlockTiles * kTile)
-k_lin_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
+k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __restrict__ cam_s,
            const int* __restrict__ file_s, const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s,
            const double* __restrict__ prep, const double* __restrict__ points, const double* __restrict__ ejp,
            const double* __restrict__ ejl, const double* __restrict__ eres, void* __restrict__ J,
@@ -158,8 +158,8 @@ k_lin_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ 
   __shared__ int lstart_all[kBlockTiles][kTile + 1];
   extern __shared__ __align__(16) uint8_t lin_stage[];  // per warp: the tile's rows, written out coalesced
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ti = blockIdx.x * kBlockTiles + w;
-  if (ti >= n_tiles) return;  // warps are independent: no block-wide barrier below
+  const int ti = tile0 + blockIdx.x * kBlockTiles + w;
+  if (ti >= tile_end) return;  // warps are independent: no block-wide barrier below
   double* contrib = contrib_all[w];
   int* lstart = lstart_all[w];
   constexpr int rb = F32 ? kRowBytesF32 : kRowBytes;
@@ -441,7 +441,8 @@ int cameras_prep(Ctx& c, const double* d_cams, double* d_prep) {
   return POBA_OK;
 }
 
-int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, const double* h_res) {
+int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, const double* h_res,
+                     const double* h_points) {
   cudaStream_t s = c.stream;
   const int64_t ns = c.n_slots;
   DBuf ejp, ejl, eres;
@@ -457,25 +458,39 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   }
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 32);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
-  const unsigned nb = grid_for(c.n_tiles, kBlockTiles);
   const bool f32 = c.precision == 32;
   auto lin = [&](auto kern, const double* prep, const double* pts, const double* a, const double* b,
-                 const double* r) {
+                 const double* r, int t0, int t1) {
+    if (t1 <= t0) return;
     const int smem = kBlockTiles * kTile * (f32 ? kRowBytesF32 : kRowBytes);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<nb, kBlockTiles * kTile, smem, s>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(), c.file_s.as<int>(),
-                                            c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(), prep, pts, a, b, r,
-                                            c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
-                                            c.Dl.as<double>(), d_bad);
+    kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, smem, s>>>(
+        c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
+        c.lidx_s.as<uint8_t>(), prep, pts, a, b, r, c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
+        c.Dl.as<double>(), d_bad);
+    c.launches++;
   };
-  if (expl) {
-    if (f32) lin(k_lin_tile<true, true>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>());
-    else lin(k_lin_tile<true, false>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>());
+  auto lin_range = [&](int t0, int t1) {
+    if (expl) {
+      if (f32) lin(k_lin_tile<true, true>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>(), t0, t1);
+      else lin(k_lin_tile<true, false>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>(), t0, t1);
+    } else {
+      if (f32) lin(k_lin_tile<false, true>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr, t0, t1);
+      else lin(k_lin_tile<false, false>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr, t0, t1);
+    }
+  };
+  if (h_points && !expl) {
+    // points arrive in file-order pieces; each piece releases the tiles whose
+    // landmarks are complete (the rest of the pass overlaps the copy)
+    const bool pinned = is_pinned(h_points);
+    PTRY(xfer_begin(c, 3, pinned));
+    for (int i = 0; i < kXferPieces; ++i) {
+      PTRY(lm_upload_piece(c, h_points, 3, c.points.as<double>(), i, pinned));
+      lin_range(c.xf_up_tile[i], c.xf_up_tile[i + 1]);
+    }
   } else {
-    if (f32) lin(k_lin_tile<false, true>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr);
-    else lin(k_lin_tile<false, false>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr);
+    lin_range(0, c.n_tiles);
   }
-  c.launches++;
   PCK(cudaGetLastError());
   if (c.n_long) {
     if (f32)

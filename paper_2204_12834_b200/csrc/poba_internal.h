@@ -179,6 +179,11 @@ struct SeriesGraph {
   int64_t launches = 0;
 };
 
+// pipelined landmark transfers: file-order pieces, used when a single-GPU
+// context moves at least kXferMinBytes of landmark rows
+constexpr int kXferPieces = 8;
+constexpr size_t kXferMinBytes = 16u << 20;
+
 // host-side state of a (resumable) device PCG solve
 struct PcgState {
   bool active = false;
@@ -228,6 +233,16 @@ struct Ctx {
   DBuf lm_stage;     // double staging for landmark uploads/downloads (file order)
   void* host_stage = nullptr;  // pinned host staging for large pageable copies
   size_t host_stage_bytes = 0;
+  // pipelined landmark transfers (kXferPieces + 1 cuts each): piece i holds
+  // file-local landmarks [xf_file[i], xf_file[i+1]); after it arrives, store
+  // landmarks [0, xf_up_lm[i+1]) and tiles [0, xf_up_tile[i+1]) can be formed;
+  // store landmarks [0, xf_dn_lm[i+1]) (tiles [0, xf_dn_tile[i+1])) hold every
+  // landmark of file pieces 0..i
+  std::vector<int64_t> xf_file, xf_up_lm, xf_dn_lm;
+  std::vector<int> xf_up_tile, xf_dn_tile;
+  DBuf lm_inv;       // int32 [n_lm_l] file-local landmark -> store landmark
+  cudaStream_t xfer = nullptr;
+  cudaEvent_t xfer_ev[2 * kXferPieces + 1] = {};
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
   DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
@@ -277,6 +292,7 @@ struct Ctx {
   DBuf ltmp;         // double [n_lm_l*3] scratch / z of long landmarks
   DBuf ctmp;         // double [n_cam*kTStride] scratch
   DBuf ctmp2;        // double [n_cam*kTStride]
+  DBuf wt_in;        // double [n_cam*kTStride] camera input of the W^T tile pass
   DBuf flag;         // int [16]
   DBuf red;          // double scratch for reductions
   DBuf cub_tmp;      // CUB temp storage
@@ -299,6 +315,9 @@ struct Ctx {
   }
   ~Ctx() {
     drop_graphs();
+    for (auto& e : xfer_ev)
+      if (e) cudaEventDestroy(e);
+    if (xfer) cudaStreamDestroy(xfer);
     if (host_stage) cudaFreeHost(host_stage);
   }
 };
@@ -317,11 +336,23 @@ size_t shard_cut(const TilePlan& plan, int64_t n_obs, int r, int nranks);
 // ---- host-side orchestration entry points ---------------------------------------
 int build_structure(Ctx& c, const int64_t* cam_idx, const int64_t* pt_idx, const double* pixels);
 int build_canonical_order(Ctx& c);
-int linearize_device(Ctx& c, bool explicit_jac, const double* jp, const double* jl, const double* res);
+// h_points: upload the points (host, file order) pipelined with the Jacobian pass
+int linearize_device(Ctx& c, bool explicit_jac, const double* jp, const double* jl, const double* res,
+                     const double* h_points = nullptr);
 int damp_device(Ctx& c, double lam, int identity);
 int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_used, int* converged);
 int series_apply_device(Ctx& c, const double* d_v, int order, double* d_out);
-int back_substitute_device(Ctx& c, const double* d_delta_p, int* nonzero);
+// h_delta_l: also download delta_l (host, file order), pipelined with the pass when possible
+int back_substitute_device(Ctx& c, const double* d_delta_p, int* nonzero, double* h_delta_l = nullptr);
+// landmark transfers (api.cu)
+bool is_pinned(const void* p);
+int lm_upload(Ctx& c, const double* host_full, int width, double* d_local);
+int lm_download(Ctx& c, const double* d_local, int width, double* host_full);
+bool xfer_pipelined(const Ctx& c, int width);
+int xfer_begin(Ctx& c, int width, bool pinned);
+int lm_upload_piece(Ctx& c, const double* host_full, int width, double* d_local, int i, bool pinned);
+int lm_download_piece(Ctx& c, const double* d_local, int width, double* host_full, int i, bool pinned);
+int lm_download_finish(Ctx& c, double* host_full, int width, bool pinned);
 int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid);
 int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out);
 int cameras_prep(Ctx& c, const double* d_cams, double* d_prep);

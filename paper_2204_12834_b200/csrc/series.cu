@@ -672,32 +672,56 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
 
 template <int OUT, bool F32>
 __global__ void __launch_bounds__(kBlockTiles * kTile)
-k_wt_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__ cam_s,
-          const uint8_t* __restrict__ lidx_s, const void* __restrict__ J, const double* __restrict__ tin, int ts,
+k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __restrict__ cam_s,
+          const uint8_t* __restrict__ lidx_s, const void* __restrict__ J, const double* __restrict__ tin,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
           int* __restrict__ nonzero_flag) {
   __shared__ double wbuf_all[kBlockTiles][kTile * 3];
   __shared__ int lstart_all[kBlockTiles][kTile + 1];
+  extern __shared__ __align__(16) uint8_t wt_stage[];  // per warp: the tile's rows
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ti = blockIdx.x * kBlockTiles + w;
-  if (ti >= n_tiles) return;
+  const int ti = tile0 + blockIdx.x * kBlockTiles + w;
+  if (ti >= tile_end) return;
   const Tile t = tiles[ti];
   if (t.flags & kTileLong) return;  // handled by k_wt_long
   double* wbuf = wbuf_all[w];
   int* lstart = lstart_all[w];
+  constexpr int rb = F32 ? kRowBytesF32 : kRowBytes;
+  uint8_t* stage = wt_stage + w * kTile * rb;
+  {  // the tile's rows are one contiguous block: coalesced 16-B streaming loads
+    const int4* src = reinterpret_cast<const int4*>(static_cast<const uint8_t*>(J) + (int64_t)ti * kTile * rb);
+    int4* dst = reinterpret_cast<int4*>(stage);
+    const int pieces = (t.n * rb + 15) / 16;
+    constexpr int kPer = (kTile * rb / 16 + 31) / 32;  // all loads in flight before the first store
+    int4 r[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+      if (lane + 32 * u < pieces) r[u] = __ldcs(src + lane + 32 * u);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+      if (lane + 32 * u < pieces) dst[lane + 32 * u] = r[u];
+  }
+  __syncwarp();
   const int64_t o = (int64_t)ti * kTile + lane;
   if (lane < t.n) {
-    const double* tv = tin + (int64_t)cam_s[o] * ts;
+    const double2* tv = reinterpret_cast<const double2*>(tin + (int64_t)cam_s[o] * kTStride);
+    double tc[10];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      const double2 v = __ldg(tv + p);
+      tc[2 * p] = v.x;
+      tc[2 * p + 1] = v.y;
+    }
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = jload<F32>(J, o, j);
-      u0 = fma(v.x, tv[j], u0);
-      u1 = fma(v.y, tv[j], u1);
+      const double2 v = jload<F32>(stage, lane, j);
+      u0 = fma(v.x, tc[j], u0);
+      u1 = fma(v.y, tc[j], u1);
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const double2 v = jload<F32>(J, o, 9 + b);
+      const double2 v = jload<F32>(stage, lane, 9 + b);
       wbuf[lane * 3 + b] = fma(v.x, u0, v.y * u1);
     }
     const int li = lidx_s[o];
@@ -827,17 +851,35 @@ __global__ void k_add_inplace(double* __restrict__ a, const double* __restrict__
 }
 
 template <int OUT>
-void launch_wt_tile(Ctx& c, const double* tin, int ts, const double* bl, double* out, int* flag) {
-  const unsigned g = grid_for(c.n_tiles, kBlockTiles);
-  if (c.precision == 32)
-    k_wt_tile<OUT, true><<<g, kBlockTiles * kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(),
-                                                                  c.lidx_s.as<uint8_t>(), c.J.p, tin, ts, bl,
-                                                                  c.Vinv.as<double>(), out, flag);
-  else
-    k_wt_tile<OUT, false><<<g, kBlockTiles * kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(),
-                                                                   c.lidx_s.as<uint8_t>(), c.J.p, tin, ts, bl,
-                                                                   c.Vinv.as<double>(), out, flag);
+// tin: camera vector in 80-B records (kTStride); see wt_input
+void launch_wt_tile(Ctx& c, const double* tin, const double* bl, double* out, int* flag, int t0 = 0,
+                    int t1 = -1) {
+  if (t1 < 0) t1 = c.n_tiles;
+  if (t1 <= t0) return;
+  const unsigned g = grid_for(t1 - t0, kBlockTiles);
+  if (c.precision == 32) {
+    const int smem = kBlockTiles * kTile * kRowBytesF32;
+    cudaFuncSetAttribute(k_wt_tile<OUT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_wt_tile<OUT, true><<<g, kBlockTiles * kTile, smem, c.stream>>>(c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(),
+                                                                     c.lidx_s.as<uint8_t>(), c.J.p, tin, bl,
+                                                                     c.Vinv.as<double>(), out, flag);
+  } else {
+    const int smem = kBlockTiles * kTile * kRowBytes;
+    cudaFuncSetAttribute(k_wt_tile<OUT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_wt_tile<OUT, false><<<g, kBlockTiles * kTile, smem, c.stream>>>(c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(),
+                                                                      c.lidx_s.as<uint8_t>(), c.J.p, tin, bl,
+                                                                      c.Vinv.as<double>(), out, flag);
+  }
   c.launches++;
+}
+
+// a 9-stride camera vector copied into 80-B records for k_wt_tile's 16-B loads
+int wt_input(Ctx& c, const double* v9, const double** out) {
+  PTRY(c.wt_in.alloc(std::max<int64_t>(c.n_cam, 1) * kTStride * 8));
+  k_restride<<<grid_for(c.n_cam * 9, 256), 256, 0, c.stream>>>(v9, 9, c.n_cam, c.wt_in.as<double>(), kTStride);
+  c.launches++;
+  *out = c.wt_in.as<double>();
+  return POBA_OK;
 }
 
 template <int OUT>
@@ -1138,13 +1180,32 @@ int series_apply_device(Ctx& c, const double* d_v, int order, double* d_out) {
   return POBA_OK;
 }
 
-int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero) {
+int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero, double* h_dl) {
   cudaStream_t s = c.stream;
   int* fl = c.flag.as<int>() + 1;
   PCK(cudaMemsetAsync(fl, 0, 4, s));
-  launch_wt_tile<kOutBack>(c, d_dp, 9, c.bl.as<double>(), c.dl.as<double>(), fl);
-  launch_wt_long<kOutBack>(c, d_dp, 9, c.bl.as<double>(), c.dl.as<double>(), fl, false);
+  const bool piped = h_dl && xfer_pipelined(c, 3);
+  const bool pinned = piped && is_pinned(h_dl);
+  if (piped) {
+    // long landmarks first, then store prefixes; each completed file piece is
+    // permuted and copied out while the next prefix is computed
+    launch_wt_long<kOutBack>(c, d_dp, 9, c.bl.as<double>(), c.dl.as<double>(), fl, false);
+    const double* tin = nullptr;
+    PTRY(wt_input(c, d_dp, &tin));
+    PTRY(xfer_begin(c, 3, pinned));
+    for (int i = 0; i < kXferPieces; ++i) {
+      launch_wt_tile<kOutBack>(c, tin, c.bl.as<double>(), c.dl.as<double>(), fl, c.xf_dn_tile[i],
+                               c.xf_dn_tile[i + 1]);
+      PTRY(lm_download_piece(c, c.dl.as<double>(), 3, h_dl, i, pinned));
+    }
+  } else {
+    const double* tin = nullptr;
+    PTRY(wt_input(c, d_dp, &tin));
+    launch_wt_tile<kOutBack>(c, tin, c.bl.as<double>(), c.dl.as<double>(), fl);
+    launch_wt_long<kOutBack>(c, d_dp, 9, c.bl.as<double>(), c.dl.as<double>(), fl, false);
+  }
   PCK(cudaGetLastError());
+  if (piped) PTRY(lm_download_finish(c, h_dl, 3, pinned));
   int h = 0;
   PCK(cudaMemcpyAsync(&h, fl, 4, cudaMemcpyDeviceToHost, s));
   PCK(cudaStreamSynchronize(s));
@@ -1159,6 +1220,7 @@ int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero) {
   }
   *nonzero = h;
   c.have_delta_l = true;
+  if (h_dl && !piped) PTRY(lm_download(c, c.dl.as<double>(), 3, h_dl));
   return POBA_OK;
 }
 
@@ -1170,10 +1232,13 @@ int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out) {
       PTRY(launch_cam(c, kCamMerge, 0, 0.0, false));
       PCK(cudaMemcpyAsync(d_out, c.rvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, s));
       break;
-    case POBA_OP_WT:
-      launch_wt_tile<kOutWt>(c, d_in, 9, nullptr, d_out, nullptr);
+    case POBA_OP_WT: {
+      const double* tin = nullptr;
+      PTRY(wt_input(c, d_in, &tin));
+      launch_wt_tile<kOutWt>(c, tin, nullptr, d_out, nullptr);
       launch_wt_long<kOutWt>(c, d_in, 9, nullptr, d_out, nullptr, false);
       break;
+    }
     case POBA_OP_U_INV:
       k_cam_mv<<<grid_for(c.n_cam * 9, 256), 256, 0, s>>>(c.Uinv.as<double>(), d_in, c.n_cam, d_out);
       c.launches++;

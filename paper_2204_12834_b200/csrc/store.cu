@@ -538,6 +538,36 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PCK(cudaMemcpyAsync(c.lm_slot0.p, s_slot0.data(), nlm * 4, cudaMemcpyHostToDevice, s));
   PCK(cudaMemcpyAsync(c.lm_k.p, s_k.data(), nlm * 4, cudaMemcpyHostToDevice, s));
   PCK(cudaMemcpyAsync(c.lm_perm.p, c.lm_order_host.data(), nlm * 4, cudaMemcpyHostToDevice, s));
+  {  // cuts of the pipelined landmark transfers (see Ctx::xf_*)
+    const int P = kXferPieces;
+    std::vector<int> inv(std::max<int64_t>(nlm, 1), 0);
+    for (int64_t j = 0; j < nlm; ++j) inv[c.lm_order_host[j]] = (int)j;
+    std::vector<int> up_max(nlm), dn_max(nlm);  // prefix maxima of store->file and file->store
+    for (int64_t j = 0; j < nlm; ++j) {
+      up_max[j] = std::max(j ? up_max[j - 1] : -1, c.lm_order_host[j]);
+      dn_max[j] = std::max(j ? dn_max[j - 1] : -1, inv[j]);
+    }
+    c.xf_file.assign(P + 1, 0);
+    c.xf_up_lm.assign(P + 1, 0);
+    c.xf_dn_lm.assign(P + 1, 0);
+    c.xf_up_tile.assign(P + 1, 0);
+    c.xf_dn_tile.assign(P + 1, 0);
+    for (int i = 0; i <= P; ++i) {
+      const int64_t f = nlm * i / P;
+      c.xf_file[i] = f;
+      // store landmarks whose file rows all lie below f: a prefix (up_max is monotone)
+      c.xf_up_lm[i] = std::lower_bound(up_max.begin(), up_max.end(), (int)f) - up_max.begin();
+      c.xf_dn_lm[i] = f ? (int64_t)dn_max[f - 1] + 1 : 0;
+      int tu = 0, td = 0;
+      while (tu < c.n_tiles && tiles[tu].lm0 + tiles[tu].nlm <= c.xf_up_lm[i]) ++tu;
+      while (td < c.n_tiles && tiles[td].lm0 < c.xf_dn_lm[i]) ++td;
+      c.xf_up_tile[i] = tu;
+      c.xf_dn_tile[i] = td;
+    }
+    c.xf_up_tile[P] = c.xf_dn_tile[P] = c.n_tiles;
+    PTRY(c.lm_inv.alloc(std::max<int64_t>(nlm, 1) * 4));
+    PCK(cudaMemcpyAsync(c.lm_inv.p, inv.data(), nlm * 4, cudaMemcpyHostToDevice, s));
+  }
   if (c.n_long) {
     PTRY(c.long_lm.alloc(c.n_long * 4));
     PCK(cudaMemcpyAsync(c.long_lm.p, c.long_host.data(), c.n_long * 4, cudaMemcpyHostToDevice, s));
