@@ -54,6 +54,15 @@ int poba_nccl_unique_id(void* out_128_bytes);
 int poba_create_sharded(int device, int rank, int nranks, const void* nccl_id_128_bytes,
                         poba_ctx** out);
 int poba_destroy(poba_ctx* ctx);
+/* In-process virtual ranks on one device (testing the sharded path with fewer
+ * GPUs than ranks): a group of nranks (<= 8) contexts, each driven by its own
+ * host thread, whose collectives meet at a host barrier and reduce every
+ * rank's buffer in rank order -- the same partition, store and replicated
+ * camera-side decisions as poba_create_sharded, with the exchange done
+ * without NCCL.  The group must outlive its contexts.                      */
+int poba_local_group_create(int nranks, void** group);
+int poba_local_group_destroy(void* group);
+int poba_create_local(int device, int rank, int nranks, void* group, poba_ctx** out);
 
 /* ---- K0: observation store structure -------------------------------------
  * Replaces blocks._sorted_observation_order (blocks.py:362-372) and

@@ -35,6 +35,9 @@ _SIGS = {
     "poba_nccl_unique_id": (ctypes.c_int, [_P]),
     "poba_create_sharded": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "poba_destroy": (ctypes.c_int, [_P]),
+    "poba_local_group_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_P)]),
+    "poba_local_group_destroy": (ctypes.c_int, [_P]),
+    "poba_create_local": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "poba_set_problem": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I64P, _I64P, _DP]),
     "poba_problem_info": (ctypes.c_int, [_P, _I64P]),
     "poba_get_ordering": (ctypes.c_int, [_P, _I64P, _I64P, _I64P]),
@@ -171,13 +174,35 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class LocalGroup:
+    """In-process virtual ranks on one device (poba_local_group_create).
+
+    Each rank's ``Device(rank=r, nranks=n, group=g)`` must be driven by its own
+    thread (collectives meet at a host barrier); the group outlives them."""
+
+    def __init__(self, nranks: int):
+        self._lib = load()
+        h = _P()
+        _check(self._lib.poba_local_group_create(int(nranks), ctypes.byref(h)))
+        self._h, self.nranks = h, int(nranks)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.poba_local_group_destroy(self._h)
+            self._h = None
+
+
 class Device:
     """One libpoba context: a problem's device-resident store and system."""
 
-    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
+                 group: LocalGroup | None = None):
         lib = load()
         h = _P()
-        if nranks > 1:
+        if group is not None:
+            _check(lib.poba_create_local(device, rank, nranks, group._h, ctypes.byref(h)))
+            self._group = group  # keep the group alive while this context exists
+        elif nranks > 1:
             idbuf = ctypes.create_string_buffer(nccl_id, 128)
             _check(lib.poba_create_sharded(device, rank, nranks, ctypes.cast(idbuf, _P), ctypes.byref(h)))
         else:

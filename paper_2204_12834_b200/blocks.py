@@ -48,8 +48,8 @@ class DeviceProblem:
     """libpoba context holding one problem's observation structure (K0)."""
 
     def __init__(self, cam_indices, pt_indices, pixels, n_cameras, n_points, device=0, rank=0, nranks=1,
-                 nccl_id=None):
-        self.dev = _lib.Device(device, rank, nranks, nccl_id)
+                 nccl_id=None, group=None):
+        self.dev = _lib.Device(device, rank, nranks, nccl_id, group)
         self.n_cameras, self.n_points = int(n_cameras), int(n_points)
         self.n_observations = len(cam_indices)
         self.dev.set_problem(n_cameras, n_points, cam_indices, pt_indices, pixels)

@@ -1,7 +1,10 @@
 // C-ABI entry points of libpoba (see include/poba.h for the contract and the
 // reference function each entry point replaces).
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -67,9 +70,106 @@ const NcclApi* nccl_api() {
   return &api;
 }
 
+// ---- in-process virtual ranks ------------------------------------------------
+// A LocalGroup lets nranks contexts on ONE device (one host thread each) run
+// the sharded path with the same collectives the NCCL communicator provides.
+// Ranks meet at a host barrier after their stream has drained, so no kernel
+// ever waits on another rank's kernel; every rank then reduces all ranks'
+// buffers (same device) in rank order into its own scratch, and a second
+// barrier keeps the sources alive until everyone has read them.
+struct LocalGroup {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  const double* src[kMaxLocalRanks] = {};
+  // false on timeout (a rank failed or never arrived): the group is poisoned
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    if (broken) return false;
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(300), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+
+namespace {
+
+struct RankPtrs {
+  const double* p[kMaxLocalRanks];
+};
+
+// out[i] = op over ranks r = 0..n-1 of p[r][i], in rank order
+template <bool kMax>
+__global__ void k_rank_reduce(RankPtrs src, int n, size_t len, double* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
+    double v = src.p[0][i];
+    for (int r = 1; r < n; ++r) v = kMax ? fmax(v, src.p[r][i]) : v + src.p[r][i];
+    out[i] = v;
+  }
+}
+
+int group_fail() { return fail(POBA_ENCCL, "local rank group: a rank failed or timed out at a collective"); }
+
+// kind 0 sum, 1 max, 2 gather (dst gets n values per rank, rank order)
+int local_collective(Ctx& c, int kind, const double* d_src, double* d_dst, size_t n) {
+  LocalGroup& g = *c.group;
+  PCK(cudaStreamSynchronize(c.stream));
+  {
+    std::lock_guard<std::mutex> lk(g.m);
+    g.src[c.rank] = d_src;
+  }
+  if (!g.barrier()) return group_fail();
+  RankPtrs rp;
+  for (int r = 0; r < g.n; ++r) rp.p[r] = g.src[r];
+  if (kind == 2) {
+    for (int r = 0; r < g.n; ++r)
+      PCK(cudaMemcpyAsync(d_dst + r * n, rp.p[r], n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  } else {
+    PTRY(c.coll_tmp.alloc(n * 8));
+    const unsigned nb = (unsigned)std::min<size_t>((n + 255) / 256, 1184);
+    if (kind == 1) k_rank_reduce<true><<<nb, 256, 0, c.stream>>>(rp, g.n, n, c.coll_tmp.as<double>());
+    else k_rank_reduce<false><<<nb, 256, 0, c.stream>>>(rp, g.n, n, c.coll_tmp.as<double>());
+    PCK(cudaGetLastError());
+  }
+  PCK(cudaStreamSynchronize(c.stream));
+  if (!g.barrier()) return group_fail();
+  if (kind != 2) PCK(cudaMemcpyAsync(d_dst, c.coll_tmp.p, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  return POBA_OK;
+}
+
+}  // namespace
+
 int allreduce_sum(Ctx& c, double* d_buf, size_t n) {
   if (c.nranks <= 1) return POBA_OK;
+  if (c.group) return local_collective(c, 0, d_buf, d_buf, n);
   PNCCL(AllReduce(d_buf, d_buf, n, ncclFloat64, ncclSum, c.comm, c.stream));
+  return POBA_OK;
+}
+
+int allreduce_max(Ctx& c, double* d_buf, size_t n) {
+  if (c.nranks <= 1) return POBA_OK;
+  if (c.group) return local_collective(c, 1, d_buf, d_buf, n);
+  PNCCL(AllReduce(d_buf, d_buf, n, ncclFloat64, ncclMax, c.comm, c.stream));
+  return POBA_OK;
+}
+
+int allgather(Ctx& c, const double* d_src, double* d_dst, size_t n) {
+  if (c.nranks <= 1) return copy_sync(c, d_dst, d_src, n * 8, cudaMemcpyDeviceToDevice);
+  if (c.group) return local_collective(c, 2, d_src, d_dst, n);
+  PNCCL(AllGather(d_src, d_dst, n, ncclFloat64, c.comm, c.stream));
   return POBA_OK;
 }
 
@@ -378,6 +478,30 @@ int poba_create_sharded(int device, int rank, int nranks, const void* nccl_id, p
       return poba::fail(POBA_ENCCL, msg);
     }
   }
+  return POBA_OK;
+}
+
+int poba_local_group_create(int nranks, void** out) {
+  if (!out) return poba::fail(POBA_EINVAL, "null output pointer");
+  if (nranks < 1 || nranks > poba::kMaxLocalRanks) return poba::fail(POBA_EINVAL, "bad rank / nranks");
+  poba::LocalGroup* g = new poba::LocalGroup();
+  g->n = nranks;
+  *out = g;
+  return POBA_OK;
+}
+
+int poba_local_group_destroy(void* group) {
+  delete static_cast<poba::LocalGroup*>(group);
+  return POBA_OK;
+}
+
+int poba_create_local(int device, int rank, int nranks, void* group, poba_ctx** out) {
+  poba::LocalGroup* g = static_cast<poba::LocalGroup*>(group);
+  if (!g || g->n != nranks || rank < 0 || rank >= nranks) return poba::fail(POBA_EINVAL, "bad rank / nranks");
+  PTRY(create_common(device, out));
+  (*out)->c.rank = rank;
+  (*out)->c.nranks = nranks;
+  (*out)->c.group = g;
   return POBA_OK;
 }
 

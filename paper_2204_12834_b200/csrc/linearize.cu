@@ -567,7 +567,7 @@ int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid) {
     std::vector<double> mine = {sum, (double)bad};
     PTRY(c.scratch_b.alloc(2 * 8 * (c.nranks + 1)));
     PCK(cudaMemcpyAsync(c.scratch_b.p, mine.data(), 16, cudaMemcpyHostToDevice, s));
-    PNCCL(AllGather(c.scratch_b.p, c.scratch_b.as<double>() + 2, 2, ncclFloat64, c.comm, s));
+    PTRY(allgather(c, c.scratch_b.as<double>(), c.scratch_b.as<double>() + 2, 2));
     std::vector<double> all(2 * c.nranks);
     PCK(cudaMemcpyAsync(all.data(), c.scratch_b.as<double>() + 2, 16 * c.nranks, cudaMemcpyDeviceToHost, s));
     PCK(cudaStreamSynchronize(s));

@@ -191,12 +191,19 @@ struct PcgState {
   double rz = 0, rz0 = 0, rel = 0;
 };
 
+// in-process group of virtual ranks sharing one device (api.cu): stands in
+// for the NCCL communicator when fewer GPUs than ranks are available
+constexpr int kMaxLocalRanks = 8;
+struct LocalGroup;
+
 struct Ctx {
   int device = 0;
   int precision = 64;  // block storage: 64 (double2 rows) or 32 (float2 rows)
   cudaStream_t stream = nullptr;
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
+  LocalGroup* group = nullptr;  // set instead of comm for in-process virtual ranks
+  DBuf coll_tmp;                // local-group collective result scratch
   int n_sm = 148;
   int64_t launches = 0;
 
@@ -356,7 +363,11 @@ int lm_download_finish(Ctx& c, double* host_full, int width, bool pinned);
 int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid);
 int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out);
 int cameras_prep(Ctx& c, const double* d_cams, double* d_prep);
+// collectives over the context's ranks (NCCL communicator or local group);
+// no-ops at nranks == 1.  Sums are fp64; allgather concatenates in rank order.
 int allreduce_sum(Ctx& c, double* d_buf, size_t n);
+int allreduce_max(Ctx& c, double* d_buf, size_t n);
+int allgather(Ctx& c, const double* d_src, double* d_dst, size_t n);
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches);
 int set_precision_device(Ctx& c, int bits);
 int series_clustered_device(Ctx& c, const int64_t* h_cluster_of_cam, int n_clusters, double eps, int max_order,

@@ -1034,7 +1034,7 @@ int damp_device(Ctx& c, double lam, int identity) {
     double v = (double)h, out = 0;
     PTRY(c.scratch_b.alloc(8));
     PCK(cudaMemcpyAsync(c.scratch_b.p, &v, 8, cudaMemcpyHostToDevice, s));
-    PNCCL(AllReduce(c.scratch_b.p, c.scratch_b.p, 1, ncclFloat64, ncclMax, c.comm, s));
+    PTRY(allreduce_max(c, c.scratch_b.as<double>(), 1));
     PCK(cudaMemcpyAsync(&out, c.scratch_b.p, 8, cudaMemcpyDeviceToHost, s));
     PCK(cudaStreamSynchronize(s));
     h = (int)out;
@@ -1213,7 +1213,7 @@ int back_substitute_device(Ctx& c, const double* d_dp, int* nonzero, double* h_d
     double v = (double)h, out = 0;
     PTRY(c.scratch_b.alloc(8));
     PCK(cudaMemcpyAsync(c.scratch_b.p, &v, 8, cudaMemcpyHostToDevice, s));
-    PNCCL(AllReduce(c.scratch_b.p, c.scratch_b.p, 1, ncclFloat64, ncclMax, c.comm, s));
+    PTRY(allreduce_max(c, c.scratch_b.as<double>(), 1));
     PCK(cudaMemcpyAsync(&out, c.scratch_b.p, 8, cudaMemcpyDeviceToHost, s));
     PCK(cudaStreamSynchronize(s));
     h = (int)out;
