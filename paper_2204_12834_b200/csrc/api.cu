@@ -877,15 +877,22 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
       // observations owned by other ranks are left untouched
       PTRY(poba::build_canonical_order(c));
       const int64_t ns = c.n_slots, n = c.n_obs;
-      std::vector<double> J((size_t)poba::kRow * ns * 2), R(ns * 2);
-      std::vector<int> file(ns), order(n), slot_of_file(n, -1);
+      // tile blocks: 32 metadata words, then 12 planes of 32 column pairs
+      const int64_t per_tile = 12 * poba::kTile * 2;  // values per tile (after the metadata)
+      std::vector<double> J((size_t)c.n_tiles * per_tile), R(ns * 2);
       if (c.precision == 32) {  // fp32 store: widen (exact) for the float64 caller
-        std::vector<float> Jf((size_t)poba::kRow * ns * 2);
+        std::vector<float> Jf((size_t)c.n_tiles * poba::kTileBlockF32 / 4);
         PTRY(poba::copy_sync(c, Jf.data(), c.J.p, Jf.size() * 4, cudaMemcpyDeviceToHost));
-        for (size_t q = 0; q < Jf.size(); ++q) J[q] = (double)Jf[q];
+        for (int64_t t = 0; t < c.n_tiles; ++t)
+          for (int64_t q = 0; q < per_tile; ++q)
+            J[t * per_tile + q] = (double)Jf[t * (poba::kTileBlockF32 / 4) + poba::kMetaBytes / 4 + q];
       } else {
-        PTRY(poba::copy_sync(c, J.data(), c.J.p, J.size() * 8, cudaMemcpyDeviceToHost));
+        std::vector<double> Jd((size_t)c.n_tiles * poba::kTileBlock / 8);
+        PTRY(poba::copy_sync(c, Jd.data(), c.J.p, Jd.size() * 8, cudaMemcpyDeviceToHost));
+        for (int64_t t = 0; t < c.n_tiles; ++t)
+          std::memcpy(&J[t * per_tile], &Jd[t * (poba::kTileBlock / 8) + poba::kMetaBytes / 8], per_tile * 8);
       }
+      std::vector<int> file(ns), order(n), slot_of_file(n, -1);
       PTRY(poba::copy_sync(c, R.data(), c.Rz.p, R.size() * 8, cudaMemcpyDeviceToHost));
       PTRY(poba::copy_sync(c, file.data(), c.file_s.p, ns * 4, cudaMemcpyDeviceToHost));
       PTRY(poba::copy_sync(c, order.data(), c.order.p, n * 4, cudaMemcpyDeviceToHost));
@@ -896,7 +903,7 @@ int poba_read(poba_ctx* ctx, int what, double* dst) {
         if (q < 0) continue;
         for (int a = 0; a < 2; ++a) {
           double* row = dst + (i * 2 + a) * 13;
-          for (int j = 0; j < 12; ++j) row[j] = J[((size_t)q * poba::kRow + j) * 2 + a];
+          for (int j = 0; j < 12; ++j) row[j] = J[(q >> 5) * per_tile + (j * poba::kTile + (q & 31)) * 2 + a];
           row[12] = R[q * 2 + a];
         }
       }

@@ -156,22 +156,15 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
            unsigned long long* __restrict__ n_invalid) {
   __shared__ double contrib_all[kBlockTiles][kTile * 9];
   __shared__ int lstart_all[kBlockTiles][kTile + 1];
-  extern __shared__ __align__(16) uint8_t lin_stage[];  // per warp: the tile's rows, written out coalesced
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = tile0 + blockIdx.x * kBlockTiles + w;
   if (ti >= tile_end) return;  // warps are independent: no block-wide barrier below
   double* contrib = contrib_all[w];
   int* lstart = lstart_all[w];
-  constexpr int rb = F32 ? kRowBytesF32 : kRowBytes;
-  uint8_t* stage = lin_stage + w * kTile * rb;
   const Tile t = tiles[ti];
   const int64_t o = (int64_t)ti * kTile + lane;
   const bool is_long = t.flags & kTileLong;
   bool bad = false;
-  if (lane < t.n) {  // keep the row metadata: it is part of the block written back below
-    if (F32) reinterpret_cast<int2*>(stage)[lane * kRow + 12] = reinterpret_cast<const int2*>(J)[o * kRow + 12];
-    else reinterpret_cast<int4*>(stage)[lane * kRow + 12] = reinterpret_cast<const int4*>(J)[o * kRow + 12];
-  }
   if (lane < t.n) {
     ObsModel m;
     if (kExplicit) {
@@ -204,13 +197,13 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
     for (int j = 0; j < 9; ++j) {
       m.jp0[j] = stored<F32>(m.jp0[j]);
       m.jp1[j] = stored<F32>(m.jp1[j]);
-      jstore<F32>(stage, lane, j, m.jp0[j], m.jp1[j]);
+      jstore<F32>(J, o, j, m.jp0[j], m.jp1[j]);  // plane j: coalesced
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       m.jl0[b] = stored<F32>(m.jl0[b]);
       m.jl1[b] = stored<F32>(m.jl1[b]);
-      jstore<F32>(stage, lane, 9 + b, m.jl0[b], m.jl1[b]);
+      jstore<F32>(J, o, 9 + b, m.jl0[b], m.jl1[b]);
     }
     m.r0 = stored<F32>(m.r0);
     m.r1 = stored<F32>(m.r1);
@@ -232,12 +225,6 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   }
   if (lane == 0) lstart[t.nlm] = t.n;
   __syncwarp();
-  {  // the tile's rows are one contiguous block: 16-B coalesced stores
-    const int4* src = reinterpret_cast<const int4*>(stage);
-    int4* dst = reinterpret_cast<int4*>(static_cast<uint8_t*>(J) + (int64_t)ti * kTile * rb);
-    const int pieces = (t.n * rb + 15) / 16;
-    for (int k = lane; k < pieces; k += 32) dst[k] = src[k];
-  }
   const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
   if (lane == 0 && nbad) atomicAdd(n_invalid, (unsigned long long)nbad);
   __syncwarp();
@@ -462,9 +449,7 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   auto lin = [&](auto kern, const double* prep, const double* pts, const double* a, const double* b,
                  const double* r, int t0, int t1) {
     if (t1 <= t0) return;
-    const int smem = kBlockTiles * kTile * (f32 ? kRowBytesF32 : kRowBytes);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, smem, s>>>(
+    kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
         c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
         c.lidx_s.as<uint8_t>(), prep, pts, a, b, r, c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
         c.Dl.as<double>(), d_bad);

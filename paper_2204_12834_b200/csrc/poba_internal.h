@@ -17,15 +17,20 @@ namespace poba {
 // [t*kTile, t*kTile + n_t); a warp-tile packs whole landmarks (index order, each
 // landmark's observations sorted by camera) up to kTile observations and kTileLm
 // landmarks; a landmark with k > kTile spans consecutive full sub-tiles.  Each
-// slot is one 208-byte row of 13 double2: the 2x9 pose Jacobian (9 column
-// pairs), the 2x3 point Jacobian (3 column pairs) and a 16-byte metadata word
-// (camera, chunk slot of the camera, landmark index in the tile) --
-// the reference's 2x13 block row with the residual column replaced by the
-// metadata (residuals live in their own array; the series never reads them).
+// warp-tile is one contiguous block: a 128-B metadata array (one 32-bit word
+// per slot: chunk slot of the camera, landmark index in the tile, first and
+// last lane of the landmark's run) followed by 12 planes of 32 column pairs --
+// plane p holds column pair p of every slot's 2x12 Jacobian row (J_p: 9 pairs,
+// J_l: 3 pairs), i.e. the reference's 2x13 block row without the residual
+// column (residuals live in their own array; the series never reads them).
+// A warp reads plane p with 32 consecutive 16-B accesses (coalesced in global
+// memory, conflict-free in shared memory), and the tile's copy ends at plane
+// 11's last valid slot.
 constexpr int kTile = 32;         // observation slots per warp-tile (one warp)
 constexpr int kTileLm = 16;       // landmarks per warp-tile (bounds the staged V^-1 slice)
-constexpr int kRow = 13;          // double2 per slot row
-constexpr int kRowBytes = kRow * 16;
+constexpr int kMetaBytes = kTile * 4;                 // per-tile metadata words
+constexpr int kTileBlock = kMetaBytes + 12 * kTile * 16;  // 6272 B per warp-tile (fp64 planes)
+constexpr int kTileBlockF32 = kMetaBytes + 12 * kTile * 8;  // 3200 B (fp32 planes, PoBA-32)
 constexpr int kBlockTiles = 8;    // warp-tiles per CTA in the streaming kernels (256 threads)
 constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
 constexpr int kJPlanes = 12;      // Jacobian column pairs per row
@@ -35,36 +40,46 @@ constexpr int kJPlanes = 12;      // Jacobian column pairs per row
 constexpr int kTermWarps = POBA_TERM_WARPS;  // warps per CTA of the term kernel (one CTA per SM)
 constexpr int kPackWindow = 64;   // landmark lookahead of the tile packer
 constexpr int kTStride = 10;      // doubles per camera record of the term vector / partials (80 B, 16-B aligned)
-// Term-kernel shared memory: per warp one bulk-copy stage (32 rows, the tile
-// descriptor, the V^-1 slice of its <= kTileLm landmarks) and the gathered
+// Term-kernel shared memory: per warp one bulk-copy stage (the tile block, the
+// tile descriptor, the V^-1 slice of its <= kTileLm landmarks) and the gathered
 // camera records of its tile; per CTA the chunk accumulator table (one 80-B
 // record per camera slot of the chunk), the stage barriers and the turn word.
-constexpr int kStRows = kTile * kRowBytes;                       // 6656
-constexpr int kStDesc = kStRows;                                 // 32-B tile descriptor
+constexpr int kStDesc = kTileBlock;                              // 32-B tile descriptor
 constexpr int kStVinv = kStDesc + 32;                            // V^-1 slice
-constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7456
+constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7072
 constexpr int kTRecBytes = kTStride * 8;                         // 80
-constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera-record table = 10016
+constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera-record table = 9632
 constexpr int kTermSmemMax = 227 * 1024;
 constexpr int kTermCtl = kTermWarps * 8 + 16;                    // stage barriers + turn word
 constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kTRecBytes) / 32 * 32;
 constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kTRecBytes;
 static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
+static_assert(kAccSlots < 2048, "chunk slots must fit the 11-bit metadata field");
 static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 
-// PoBA-32 (blocks.py:42-47): block storage may be fp32 (rows of 13 float2 =
-// 104 B, metadata as int2 {slot, run}); every value read from it is widened to
-// fp64 and all arithmetic and reductions stay fp64.
-constexpr int kRowBytesF32 = kRow * 8;
+// PoBA-32 (blocks.py:42-47): block storage may be fp32 (planes of float2);
+// every value read from it is widened to fp64 and all arithmetic and
+// reductions stay fp64.
 
-// metadata word (row entry 12, as int4)
-struct RowMeta {
-  int slot;      // slot of the camera in the chunk accumulator table
-  int run;       // landmark index in the tile (bits 0-7; 0 for a long landmark's sub-tile),
-                 // first (8-15) and last (16-23) lane of the landmark's run
-  int pad;
-  int cam;
-};
+// metadata word of a slot: chunk slot (bits 0-10), landmark index in the tile
+// (11-15; 0 for a long landmark's sub-tile), first (16-20) and last (21-25)
+// lane of the landmark's run
+__host__ __device__ __forceinline__ uint32_t pack_meta(int slot, int li, int first, int last) {
+  return (uint32_t)slot | ((uint32_t)li << 11) | ((uint32_t)first << 16) | ((uint32_t)last << 21);
+}
+__host__ __device__ __forceinline__ int meta_slot(uint32_t m) { return (int)(m & 0x7ffu); }
+__host__ __device__ __forceinline__ int meta_li(uint32_t m) { return (int)((m >> 11) & 0x1fu); }
+__host__ __device__ __forceinline__ int meta_first(uint32_t m) { return (int)((m >> 16) & 0x1fu); }
+__host__ __device__ __forceinline__ int meta_last(uint32_t m) { return (int)((m >> 21) & 0x1fu); }
+template <bool F32>
+constexpr int tile_block_bytes() { return F32 ? kTileBlockF32 : kTileBlock; }
+// bytes of a tile's bulk copy: metadata + planes up to plane 11's last valid
+// slot (fp32: an even slot count, bulk copies move multiples of 16 B)
+template <bool F32>
+__host__ __device__ __forceinline__ uint32_t tile_copy_bytes(int n) {
+  return F32 ? (uint32_t)(kMetaBytes + (11 * kTile + ((n + 1) & ~1)) * 8)
+             : (uint32_t)(kMetaBytes + (11 * kTile + n) * 16);
+}
 
 // Error plumbing ---------------------------------------------------------------
 void set_error(const std::string& msg);
@@ -262,7 +277,7 @@ struct Ctx {
   DBuf cc_cam_off;   // int32 [n_cam+1] camera -> cchunk range
 
   // store (K1), slot space
-  DBuf J;            // [n_slots][kRow] rows (J_p pairs, J_l pairs, metadata): double2, or float2 at precision 32
+  DBuf J;            // [n_tiles] tile blocks (metadata + 12 planes): double2 planes, or float2 at precision 32
   DBuf slot_s;       // int32 [n_slots] chunk slot of each observation's camera (metadata source)
   DBuf Rz;           // double2 [n_slots] residuals
 
@@ -392,19 +407,27 @@ inline int copy_sync(Ctx& c, void* dst, const void* src, size_t bytes, cudaMemcp
 
 // ---- device helpers shared by the tile kernels -----------------------------------
 #ifdef __CUDACC__
-// Jacobian column pair p (0..11) of slot o, widened to fp64
+// Jacobian column pair p (0..11) of slot o, widened to fp64 (tile block layout)
+template <bool F32>
+__device__ __forceinline__ int64_t jindex(int64_t o, int p) {  // element index past the tile's metadata
+  return (o >> 5) * (tile_block_bytes<F32>() / (F32 ? 8 : 16)) + kMetaBytes / (F32 ? 8 : 16) + p * kTile + (o & 31);
+}
 template <bool F32>
 __device__ __forceinline__ double2 jload(const void* __restrict__ J, int64_t o, int p) {
   if (F32) {
-    const float2 v = reinterpret_cast<const float2*>(J)[o * kRow + p];
+    const float2 v = reinterpret_cast<const float2*>(J)[jindex<true>(o, p)];
     return make_double2((double)v.x, (double)v.y);
   }
-  return reinterpret_cast<const double2*>(J)[o * kRow + p];
+  return reinterpret_cast<const double2*>(J)[jindex<false>(o, p)];
 }
 template <bool F32>
 __device__ __forceinline__ void jstore(void* __restrict__ J, int64_t o, int p, double a, double b) {
-  if (F32) reinterpret_cast<float2*>(J)[o * kRow + p] = make_float2((float)a, (float)b);
-  else reinterpret_cast<double2*>(J)[o * kRow + p] = make_double2(a, b);
+  if (F32) reinterpret_cast<float2*>(J)[jindex<true>(o, p)] = make_float2((float)a, (float)b);
+  else reinterpret_cast<double2*>(J)[jindex<false>(o, p)] = make_double2(a, b);
+}
+template <bool F32>
+__device__ __forceinline__ uint32_t* meta_ptr(void* J, int64_t o) {
+  return reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(J) + (o >> 5) * tile_block_bytes<F32>()) + (o & 31);
 }
 // the value fp32 storage keeps (round to nearest, as numpy's astype(float32))
 template <bool F32>

@@ -271,9 +271,8 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
 
   auto issue = [&](int ti, int n, int nlm, int lm0) {  // lane 0
     const uint32_t vbytes = (MODE != kModeW) ? (uint32_t)(nlm * 48) : 0u;
-    // fp32 rows are 104 B: copy an even number of them (bulk copies move multiples of 16 B)
-    const uint32_t rbytes = F32 ? (uint32_t)(((n + 1) & ~1) * kRowBytesF32) : (uint32_t)(n * kRowBytes);
-    const char* src = static_cast<const char*>(a.J) + (int64_t)ti * kTile * (F32 ? kRowBytesF32 : kRowBytes);
+    const uint32_t rbytes = tile_copy_bytes<F32>(n);  // metadata + planes up to plane 11's last slot
+    const char* src = static_cast<const char*>(a.J) + (int64_t)ti * tile_block_bytes<F32>();
     mbar_expect_tx(sbar, rbytes + 32u + vbytes);
     bulk_g2s_stream(stg, src, rbytes, sbar, pol);
     bulk_g2s(stg + kStDesc, a.tk + ti, 32, sbar);
@@ -339,18 +338,12 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     const bool valid = lane < t.n;
     const bool is_long = t.flags & kTileLong;
     int slot = 0, li = 0, first = lane, last = lane;
-    if (valid) {  // slot, landmark run (16-B load; 8-B at precision 32)
-      int2 mv;
-      if (F32) {
-        mv = reinterpret_cast<const int2*>(stg)[lane * kRow + 12];
-      } else {
-        const int4 m4 = reinterpret_cast<const int4*>(stg)[lane * kRow + 12];
-        mv = make_int2(m4.x, m4.y);
-      }
-      slot = mv.x;
-      li = mv.y & 0xff;
-      first = (mv.y >> 8) & 0xff;
-      last = (mv.y >> 16) & 0xff;
+    if (valid) {  // slot, landmark run: the tile's metadata word of this lane
+      const uint32_t mv = reinterpret_cast<const uint32_t*>(stg)[lane];
+      slot = meta_slot(mv);
+      li = meta_li(mv);
+      first = meta_first(mv);
+      last = meta_last(mv);
     }
     const bool is_last = valid && lane == last;
     double vi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -367,10 +360,11 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
 #pragma unroll
     for (int p = 0; p < kJPlanes; ++p) {
       if (F32) {
-        const float2 v = valid ? reinterpret_cast<const float2*>(stg)[lane * kRow + p] : make_float2(0.f, 0.f);
+        const float2 v =
+            valid ? reinterpret_cast<const float2*>(stg + kMetaBytes)[p * kTile + lane] : make_float2(0.f, 0.f);
         jr[p] = make_double2((double)v.x, (double)v.y);
       } else {
-        jr[p] = valid ? reinterpret_cast<const double2*>(stg)[lane * kRow + p] : make_double2(0.0, 0.0);
+        jr[p] = valid ? reinterpret_cast<const double2*>(stg + kMetaBytes)[p * kTile + lane] : make_double2(0.0, 0.0);
       }
     }
     // Refill the stage with this warp's next tile.  The bulk copy writes
@@ -678,7 +672,6 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
           int* __restrict__ nonzero_flag) {
   __shared__ double wbuf_all[kBlockTiles][kTile * 3];
   __shared__ int lstart_all[kBlockTiles][kTile + 1];
-  extern __shared__ __align__(16) uint8_t wt_stage[];  // per warp: the tile's rows
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = tile0 + blockIdx.x * kBlockTiles + w;
   if (ti >= tile_end) return;
@@ -686,22 +679,6 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
   if (t.flags & kTileLong) return;  // handled by k_wt_long
   double* wbuf = wbuf_all[w];
   int* lstart = lstart_all[w];
-  constexpr int rb = F32 ? kRowBytesF32 : kRowBytes;
-  uint8_t* stage = wt_stage + w * kTile * rb;
-  {  // the tile's rows are one contiguous block: coalesced 16-B streaming loads
-    const int4* src = reinterpret_cast<const int4*>(static_cast<const uint8_t*>(J) + (int64_t)ti * kTile * rb);
-    int4* dst = reinterpret_cast<int4*>(stage);
-    const int pieces = (t.n * rb + 15) / 16;
-    constexpr int kPer = (kTile * rb / 16 + 31) / 32;  // all loads in flight before the first store
-    int4 r[kPer];
-#pragma unroll
-    for (int u = 0; u < kPer; ++u)
-      if (lane + 32 * u < pieces) r[u] = __ldcs(src + lane + 32 * u);
-#pragma unroll
-    for (int u = 0; u < kPer; ++u)
-      if (lane + 32 * u < pieces) dst[lane + 32 * u] = r[u];
-  }
-  __syncwarp();
   const int64_t o = (int64_t)ti * kTile + lane;
   if (lane < t.n) {
     const double2* tv = reinterpret_cast<const double2*>(tin + (int64_t)cam_s[o] * kTStride);
@@ -715,13 +692,13 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = jload<F32>(stage, lane, j);
+      const double2 v = jload<F32>(J, o, j);  // plane j: one coalesced 512-B read per warp
       u0 = fma(v.x, tc[j], u0);
       u1 = fma(v.y, tc[j], u1);
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const double2 v = jload<F32>(stage, lane, 9 + b);
+      const double2 v = jload<F32>(J, o, 9 + b);
       wbuf[lane * 3 + b] = fma(v.x, u0, v.y * u1);
     }
     const int li = lidx_s[o];
@@ -858,15 +835,11 @@ void launch_wt_tile(Ctx& c, const double* tin, const double* bl, double* out, in
   if (t1 <= t0) return;
   const unsigned g = grid_for(t1 - t0, kBlockTiles);
   if (c.precision == 32) {
-    const int smem = kBlockTiles * kTile * kRowBytesF32;
-    cudaFuncSetAttribute(k_wt_tile<OUT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_wt_tile<OUT, true><<<g, kBlockTiles * kTile, smem, c.stream>>>(c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(),
+    k_wt_tile<OUT, true><<<g, kBlockTiles * kTile, 0, c.stream>>>(c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(),
                                                                      c.lidx_s.as<uint8_t>(), c.J.p, tin, bl,
                                                                      c.Vinv.as<double>(), out, flag);
   } else {
-    const int smem = kBlockTiles * kTile * kRowBytes;
-    cudaFuncSetAttribute(k_wt_tile<OUT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_wt_tile<OUT, false><<<g, kBlockTiles * kTile, smem, c.stream>>>(c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(),
+    k_wt_tile<OUT, false><<<g, kBlockTiles * kTile, 0, c.stream>>>(c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(),
                                                                       c.lidx_s.as<uint8_t>(), c.J.p, tin, bl,
                                                                       c.Vinv.as<double>(), out, flag);
   }

@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "poba_internal.h"
@@ -117,11 +118,10 @@ __global__ void k_fill_i32(int* __restrict__ a, int64_t n, int v) {
   if (i < n) a[i] = v;
 }
 
-// metadata column (row entry 12) of every slot; one warp per tile
+// metadata word of every slot (the first 128 B of each tile block); one warp per tile
 template <bool F32>
-__global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
-                            const int* __restrict__ slot_s, const uint8_t* __restrict__ lidx_s,
-                            void* __restrict__ J) {
+__global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restrict__ slot_s,
+                            const uint8_t* __restrict__ lidx_s, void* __restrict__ J) {
   const Tile t = tiles[blockIdx.x];
   const int lane = threadIdx.x;
   const int64_t s = (int64_t)blockIdx.x * kTile + lane;
@@ -133,13 +133,7 @@ __global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restric
   const unsigned above = heads & ~((2u << lane) - 1u);
   const int last = (above ? __ffs(above) - 1 : t.n) - 1;
   const int first = 31 - __clz(heads & ((2u << lane) - 1u));
-  RowMeta m;
-  m.slot = valid ? slot_s[s] : 0;
-  m.pad = 0;
-  m.run = valid ? (li | (first << 8) | (last << 16)) : 0;
-  m.cam = cam_s[s];
-  if (F32) reinterpret_cast<int2*>(J)[s * kRow + 12] = make_int2(m.slot, m.run);  // 8-B metadata
-  else *reinterpret_cast<RowMeta*>(reinterpret_cast<double2*>(J) + s * kRow + 12) = m;
+  *meta_ptr<F32>(J, s) = valid ? pack_meta(slot_s[s], li, first, last) : 0u;
 }
 
 __global__ void k_cam_slot_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
@@ -395,18 +389,17 @@ int build_canonical_order(Ctx& c) {
   return POBA_OK;
 }
 
-// (re)allocate the row store for the context's precision and write the metadata
+// (re)allocate the tile-block store for the context's precision and write the metadata
 int alloc_store(Ctx& c) {
-  const size_t row = c.precision == 32 ? (size_t)kRowBytesF32 : (size_t)kRowBytes;
-  const size_t bytes = row * (size_t)c.n_slots;
+  const size_t bytes = (size_t)(c.precision == 32 ? kTileBlockF32 : kTileBlock) * (size_t)c.n_tiles;
   c.J.release();
   PTRY(c.J.alloc(bytes));
   PCK(cudaMemsetAsync(c.J.p, 0, bytes, c.stream));
   if (c.precision == 32)
-    k_pack_meta<true><<<c.n_tiles, kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.slot_s.as<int>(),
+    k_pack_meta<true><<<c.n_tiles, kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.slot_s.as<int>(),
                                                          c.lidx_s.as<uint8_t>(), c.J.p);
   else
-    k_pack_meta<false><<<c.n_tiles, kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.cam_s.as<int>(), c.slot_s.as<int>(),
+    k_pack_meta<false><<<c.n_tiles, kTile, 0, c.stream>>>(c.tiles.as<Tile>(), c.slot_s.as<int>(),
                                                           c.lidx_s.as<uint8_t>(), c.J.p);
   c.launches++;
   PCK(cudaGetLastError());
@@ -424,6 +417,78 @@ int set_precision_device(Ctx& c, int bits) {
   if (c.have_problem) PTRY(alloc_store(c));
   return POBA_OK;
 }
+
+namespace {
+
+// Bank-aware renumbering of one chunk's accumulator slots (host).  The term
+// kernel's apply does 16-B shared-memory accesses to the 80-B record of each
+// distinct camera of a tile (its lowest lane); a 16-B access is served eight
+// lanes at a time, and slot s's j-th piece lies in bank group (5 s + j) mod 8,
+// so lanes of one eight-lane quarter whose slots agree mod 8 serialise.
+// Slots are renumbered so that cameras sharing quarters tend to differ mod 8:
+// greedy colouring (colour = slot mod 8, most-seen camera first, colour
+// capacities keep the numbering dense), colour c's k-th camera gets slot
+// 8k + c.  Only the numbering changes -- every sum keeps its order, so results
+// are bitwise unchanged.
+void color_chunk_slots(const std::vector<int>& hcam, const std::vector<Tile>& tiles, const Chunk& q,
+                       std::vector<int>& obs_slot, std::vector<int>& part_cam) {
+  const int n = q.nslot;
+  if (n <= 8) return;
+  // quarters of leader lanes (first lane of each camera in its tile)
+  std::vector<int> occ_q, occ_s;  // quarter id, old slot of each leader
+  std::vector<int> seen(n, -1);
+  int nq = 0;
+  for (int ti = q.tile0; ti < q.tile1; ++ti) {
+    const int64_t s0 = (int64_t)ti * kTile;
+    for (int i = 0; i < tiles[ti].n; ++i) {
+      const int sl = obs_slot[s0 + i];
+      if (seen[sl] == ti) continue;
+      seen[sl] = ti;
+      occ_q.push_back(nq + i / 8);
+      occ_s.push_back(sl);
+    }
+    nq += kTile / 8;
+  }
+  std::vector<int> off(n + 1, 0), qs(occ_q.size());
+  for (int sl : occ_s) off[sl + 1]++;
+  for (int k = 0; k < n; ++k) off[k + 1] += off[k];
+  {
+    std::vector<int> pos(off.begin(), off.end() - 1);
+    for (size_t k = 0; k < occ_q.size(); ++k) qs[pos[occ_s[k]]++] = occ_q[k];
+  }
+  std::vector<int> order(n);
+  for (int k = 0; k < n; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });
+  std::vector<uint8_t> qcnt((size_t)nq * 8, 0);
+  std::vector<int> color(n, 0), cap(8), used(8, 0);
+  for (int c = 0; c < 8; ++c) cap[c] = n / 8 + (c < n % 8 ? 1 : 0);
+  for (int sl : order) {
+    int64_t cost[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = off[sl]; k < off[sl + 1]; ++k) {
+      const uint8_t* qc = &qcnt[(size_t)qs[k] * 8];
+      for (int c = 0; c < 8; ++c) cost[c] += qc[c];
+    }
+    int best = -1;
+    for (int c = 0; c < 8; ++c) {
+      if (used[c] >= cap[c]) continue;
+      if (best < 0 || cost[c] < cost[best] || (cost[c] == cost[best] && used[c] < used[best])) best = c;
+    }
+    color[sl] = best;
+    used[best]++;
+    for (int k = off[sl]; k < off[sl + 1]; ++k) qcnt[(size_t)qs[k] * 8 + best]++;
+  }
+  std::vector<int> slot_new(n), next(8, 0), cams(n);
+  for (int sl = 0; sl < n; ++sl) slot_new[sl] = 8 * next[color[sl]]++ + color[sl];
+  for (int sl = 0; sl < n; ++sl) cams[slot_new[sl]] = part_cam[q.part0 + sl];
+  for (int sl = 0; sl < n; ++sl) part_cam[q.part0 + sl] = cams[sl];
+  for (int ti = q.tile0; ti < q.tile1; ++ti) {
+    const int64_t s0 = (int64_t)ti * kTile;
+    for (int i = 0; i < tiles[ti].n; ++i) obs_slot[s0 + i] = slot_new[obs_slot[s0 + i]];
+  }
+}
+
+}  // namespace
 
 int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const double* h_pix) {
   const int64_t n = c.n_obs, n_cam = c.n_cam, n_pt = c.n_pt;
@@ -678,6 +743,8 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
       chunks.back().tile1 = cta[b].y;
     }
     for (const Chunk& q : chunks) tiles[q.tile1 - 1].flags |= kTileChunkLast;
+    if (!getenv("POBA_NO_SLOT_COLOR"))
+      for (const Chunk& q : chunks) color_chunk_slots(hcam, tiles, q, obs_slot, part_cam);
     c.n_cta = n_cta;
     PTRY(c.cta_tiles.alloc(n_cta * sizeof(int2)));
     PTRY(poba::copy_sync(c, c.cta_tiles.p, cta.data(), n_cta * sizeof(int2), cudaMemcpyHostToDevice));
