@@ -153,7 +153,7 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
            const double* __restrict__ prep, const double* __restrict__ points, const double* __restrict__ ejp,
            const double* __restrict__ ejl, const double* __restrict__ eres, void* __restrict__ J,
            double2* __restrict__ Rz, double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
-           unsigned long long* __restrict__ n_invalid) {
+           const int* __restrict__ cpos, double2* __restrict__ cmaj, unsigned long long* __restrict__ n_invalid) {
   __shared__ double contrib_all[kBlockTiles][kTile * 9];
   __shared__ int lstart_all[kBlockTiles][kTile + 1];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -208,6 +208,12 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
     m.r0 = stored<F32>(m.r0);
     m.r1 = stored<F32>(m.r1);
     Rz[o] = make_double2(m.r0, m.r1);
+    {  // camera-major copy of J_p and r for the U0 / b_p pass (160 contiguous bytes)
+      double2* cm = cmaj + (int64_t)cpos[o] * 10;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) cm[j] = make_double2(m.jp0[j], m.jp1[j]);
+      cm[9] = make_double2(m.r0, m.r1);
+    }
     double* cc = contrib + lane * 9;
     cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
     cc[1] = m.jl0[0] * m.jl0[1] + m.jl1[0] * m.jl1[1];
@@ -288,12 +294,9 @@ __device__ __forceinline__ int find_camera(const int* __restrict__ off, int n_ca
 
 // U0 (packed upper 45) and b_p (9) partial sums over chunks of <= 128 observations
 // of one camera, walked in camera-major order; fixed warp-butterfly reduction.
-template <bool F32>
 __global__ void __launch_bounds__(kCamReduceThreads)
 k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cam_start,
-                   const int* __restrict__ cperm, const void* __restrict__ J,
-                   const double2* __restrict__ Rz, int64_t pad, int n_cam, int n_cc,
-                   double* __restrict__ out) {
+                   const double2* __restrict__ cmaj, int n_cam, int n_cc, double* __restrict__ out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_cc) return;
@@ -304,15 +307,15 @@ k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ c
 #pragma unroll
   for (int q = 0; q < 54; ++q) acc[q] = 0.0;
   for (int p = p0 + lane; p < p1; p += 32) {
-    const int o = cperm[p];
+    const double2* cm = cmaj + (int64_t)p * 10;
     double a[9], b[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = jload<F32>(J, o, j);
+      const double2 v = __ldcs(cm + j);
       a[j] = v.x;
       b[j] = v.y;
     }
-    const double2 r = Rz[o];
+    const double2 r = __ldcs(cm + 9);
     int q = 0;
 #pragma unroll
     for (int i = 0; i < 9; ++i)
@@ -445,6 +448,7 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   }
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 32);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
+  PTRY(c.cmaj.alloc((size_t)std::max<int64_t>(c.n_obs_l, 1) * 160));
   const bool f32 = c.precision == 32;
   auto lin = [&](auto kern, const double* prep, const double* pts, const double* a, const double* b,
                  const double* r, int t0, int t1) {
@@ -452,7 +456,7 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
     kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
         c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
         c.lidx_s.as<uint8_t>(), prep, pts, a, b, r, c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
-        c.Dl.as<double>(), d_bad);
+        c.Dl.as<double>(), c.cpos.as<int>(), c.cmaj.as<double2>(), d_bad);
     c.launches++;
   };
   auto lin_range = [&](int t0, int t1) {
@@ -491,14 +495,9 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   // camera side: U0 / b_p via camera-major chunks, then a fixed-order merge
   if (c.n_cchunks) {
     const unsigned g = grid_for((int64_t)c.n_cchunks * 32, kCamReduceThreads);
-    if (f32)
-      k_cam_chunk_reduce<true><<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
-                                                 c.J.p, c.Rz.as<double2>(), ns, (int)c.n_cam, c.n_cchunks,
-                                                 c.cc_part.as<double>());
-    else
-      k_cam_chunk_reduce<false><<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
-                                                  c.J.p, c.Rz.as<double2>(), ns, (int)c.n_cam, c.n_cchunks,
-                                                  c.cc_part.as<double>());
+    k_cam_chunk_reduce<<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(),
+                                                      c.cmaj.as<double2>(), (int)c.n_cam, c.n_cchunks,
+                                                      c.cc_part.as<double>());
     c.launches++;
   }
   k_cam_merge54<<<grid_for(c.n_cam * 32, 256), 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_part.as<double>(),

@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
       r[1] = make_double2(o1.x + hg[2], o1.y + hg[3]);
       r[2] = make_double2(o2.x + hg[4], o2.y + hg[5]);
       r[3] = make_double2(o3.x + hg[6], o3.y + hg[7]);
-      r[4] = make_double2(o4.x + hg[8], o4.y);
+      r[4] = make_double2(o4.x + hg[8], o4.y + 0.0);  // keep a 16-B access (the pad is +0.0)
     }
     __syncwarp();
     if (h_flags & kTileChunkLast) {  // write the chunk's partials, clear the table
@@ -390,10 +390,8 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     double tc[10];
     if (MODE == kModeTerm) {
 #pragma unroll
-      for (int p = 0; p < 5; ++p) {
-        const double2 v = ttab[lane * 5 + p];
-        tc[2 * p] = v.x;
-        tc[2 * p + 1] = v.y;
+      for (int p = 0; p < 5; ++p) {  // 16-B loads (a 64-bit load of the last piece would conflict 2-way)
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(tc[2 * p]), "=d"(tc[2 * p + 1]) : "r"(smem_u32(ttab + lane * 5 + p)));
       }
     }
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;

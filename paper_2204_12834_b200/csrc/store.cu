@@ -149,6 +149,11 @@ __global__ void k_low32(const uint64_t* __restrict__ key, int64_t n, int* __rest
   if (i < n) out[i] = (int)(key[i] & 0xffffffffu);
 }
 
+__global__ void k_inverse_perm(const int* __restrict__ perm, int64_t n, int* __restrict__ inv) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) inv[perm[i]] = (int)i;
+}
+
 __global__ void k_cam_degree(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ deg) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) atomicAdd(&deg[(int)(key[i] >> 32)], 1);
@@ -422,16 +427,17 @@ namespace {
 
 // Bank-aware renumbering of one chunk's accumulator slots (host).  The term
 // kernel's apply does 16-B shared-memory accesses to the 80-B record of each
-// distinct camera of a tile (its lowest lane); a 16-B access is served eight
-// lanes at a time, and slot s's j-th piece lies in bank group (5 s + j) mod 8,
-// so lanes of one eight-lane quarter whose slots agree mod 8 serialise.
-// Slots are renumbered so that cameras sharing quarters tend to differ mod 8:
-// greedy colouring (colour = slot mod 8, most-seen camera first, colour
-// capacities keep the numbering dense), colour c's k-th camera gets slot
-// 8k + c.  Only the numbering changes -- every sum keeps its order, so results
-// are bitwise unchanged.
+// distinct camera of a tile (its lowest lane); slot s's j-th piece lies in
+// bank group (5 s + j) mod 8, so leader lanes whose slots agree mod 8
+// serialise (measured: a warp's access costs about the largest number of its
+// leaders sharing a residue).  Slots are renumbered so that cameras seen in
+// the same tile tend to differ mod 8: greedy colouring (colour = slot mod 8,
+// most-seen camera first, colour capacities keep the numbering dense), colour
+// c's k-th camera gets slot 8k + c.  Only the numbering changes -- every sum
+// keeps its order, so results are bitwise unchanged.  `group` lanes form one
+// colouring group (32: the whole tile).
 void color_chunk_slots(const std::vector<int>& hcam, const std::vector<Tile>& tiles, const Chunk& q,
-                       std::vector<int>& obs_slot, std::vector<int>& part_cam) {
+                       std::vector<int>& obs_slot, std::vector<int>& part_cam, int group) {
   const int n = q.nslot;
   if (n <= 8) return;
   // quarters of leader lanes (first lane of each camera in its tile)
@@ -444,10 +450,10 @@ void color_chunk_slots(const std::vector<int>& hcam, const std::vector<Tile>& ti
       const int sl = obs_slot[s0 + i];
       if (seen[sl] == ti) continue;
       seen[sl] = ti;
-      occ_q.push_back(nq + i / 8);
+      occ_q.push_back(nq + i / group);
       occ_s.push_back(sl);
     }
-    nq += kTile / 8;
+    nq += kTile / group;
   }
   std::vector<int> off(n + 1, 0), qs(occ_q.size());
   for (int sl : occ_s) off[sl + 1]++;
@@ -743,8 +749,11 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
       chunks.back().tile1 = cta[b].y;
     }
     for (const Chunk& q : chunks) tiles[q.tile1 - 1].flags |= kTileChunkLast;
-    if (!getenv("POBA_NO_SLOT_COLOR"))
-      for (const Chunk& q : chunks) color_chunk_slots(hcam, tiles, q, obs_slot, part_cam);
+    if (!getenv("POBA_NO_SLOT_COLOR")) {
+      const char* g = getenv("POBA_SLOT_GROUP");  // A/B: lanes per colouring group (8, 16 or 32)
+      const int group = (g && (atoi(g) == 8 || atoi(g) == 16)) ? atoi(g) : 32;
+      for (const Chunk& q : chunks) color_chunk_slots(hcam, tiles, q, obs_slot, part_cam, group);
+    }
     c.n_cta = n_cta;
     PTRY(c.cta_tiles.alloc(n_cta * sizeof(int2)));
     PTRY(poba::copy_sync(c, c.cta_tiles.p, cta.data(), n_cta * sizeof(int2), cudaMemcpyHostToDevice));
@@ -799,6 +808,9 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     PTRY(c.cperm.alloc(nl * 4));
     k_low32<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, c.cperm.as<int>());
+    PTRY(c.cpos.alloc(ns * 4));
+    k_inverse_perm<<<grid_for(nl, B), B, 0, s>>>(c.cperm.as<int>(), nl, c.cpos.as<int>());
+    c.launches++;
     DBuf deg, ccnt;
     PTRY(deg.alloc((n_cam + 1) * 4));
     PTRY(ccnt.alloc((n_cam + 1) * 4));
