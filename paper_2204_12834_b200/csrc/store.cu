@@ -750,8 +750,8 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     }
     for (const Chunk& q : chunks) tiles[q.tile1 - 1].flags |= kTileChunkLast;
     if (!getenv("POBA_NO_SLOT_COLOR")) {
-      const char* g = getenv("POBA_SLOT_GROUP");  // A/B: lanes per colouring group (8, 16 or 32)
-      const int group = (g && (atoi(g) == 8 || atoi(g) == 16)) ? atoi(g) : 32;
+      const char* g = getenv("POBA_SLOT_GROUP");  // A/B: lanes per colouring group (8 = one quarter, 16, 32)
+      const int group = (g && (atoi(g) == 16 || atoi(g) == 32)) ? atoi(g) : 8;
       for (const Chunk& q : chunks) color_chunk_slots(hcam, tiles, q, obs_slot, part_cam, group);
     }
     c.n_cta = n_cta;
