@@ -246,12 +246,6 @@ struct TermArgs {
 //            pre-summed in lane order.
 // After the last tile of a chunk its warp writes the table out once (one 80-B
 // partial per (chunk, camera)) and clears it before passing the turn on.
-#ifndef POBA_PERMUTE_APPLY
-#define POBA_PERMUTE_APPLY 1
-#endif
-#ifndef POBA_REC64
-#define POBA_REC64 0
-#endif
 template <int MODE, bool F32>
 __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
@@ -317,11 +311,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     r[1] = make_double2(o1.x + v[2], o1.y + v[3]);
     r[2] = make_double2(o2.x + v[4], o2.y + v[5]);
     r[3] = make_double2(o3.x + v[6], o3.y + v[7]);
-#if POBA_REC64
     r[4] = make_double2(o4.x + v[8], o4.y);
-#else
-    r[4] = make_double2(o4.x + v[8], o4.y + 0.0);  // keep a 16-B access (the pad is +0.0)
-#endif
   };
   auto apply_held = [&]() {
     if (h_ti != range.x) turn_wait(wid);
@@ -402,18 +392,9 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     if (MODE == kModeTerm) {
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
-#if POBA_REC64
         const double2 v = ttab[lane * 5 + p];
         tc[2 * p] = v.x;
         tc[2 * p + 1] = v.y;
-#else
-        // 16-B loads (a 64-bit load of the last piece would conflict 2-way).
-        // The memory clobber keeps them ahead of the table's refill below.
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
-                     : "=d"(tc[2 * p]), "=d"(tc[2 * p + 1])
-                     : "r"(smem_u32(ttab + lane * 5 + p))
-                     : "memory");
-#endif
       }
     }
     double w0 = 0.0, w1 = 0.0, w2 = 0.0;
@@ -491,50 +472,10 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
       }
     }
     if (q > 0) apply_held();
-#if POBA_PERMUTE_APPLY
-    // Bank-balanced apply lanes.  A 16-B shared access is served eight lanes
-    // at a time, and piece j of slot s's record lies in bank group
-    // (5 s + j) mod 8, so the applying lanes are permuted before they are
-    // held: the r-th applying lane (r < 4) whose slot is c (mod 8) moves to
-    // lane 8 r + c, and any further ones fill the lanes left free, so each
-    // eight-lane quarter touches distinct bank groups where it can.  The
-    // slots of a tile are distinct, so no sum changes.
-    {
-      unsigned mine = 0u;  // applying lanes whose slot is = lane (mod 8)
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const unsigned mc = __ballot_sync(0xffffffffu, apply && (slot & 7) == cc);
-        if ((lane & 7) == cc) mine = mc;
-      }
-      const unsigned lt = (1u << lane) - 1u;
-      const unsigned free_pos = __ballot_sync(0xffffffffu, __popc(mine) <= (lane >> 3));
-      const unsigned mine_own = __shfl_sync(0xffffffffu, mine, slot & 7);  // my colour's mask
-      const int rank = __popc(mine_own & lt);
-      const unsigned over = __ballot_sync(0xffffffffu, apply && rank >= 4);
-      int pos = 8 * rank + (slot & 7);
-      if (apply && rank >= 4) {  // the k-th free lane
-        unsigned f = free_pos;
-        for (int k = __popc(over & lt); k > 0; --k) f &= f - 1u;
-        pos = __ffs(f) - 1;
-      }
-      uint8_t* src_tab = reinterpret_cast<uint8_t*>(ttab);  // this tile's records are consumed
-      __syncwarp();
-      if (apply) src_tab[pos] = (uint8_t)lane;
-      __syncwarp();
-      const bool occupied = !((free_pos >> lane) & 1u) || __popc(free_pos & lt) < __popc(over);
-      const int src = occupied ? src_tab[lane] : lane;
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 9; ++j) hg[j] = __shfl_sync(0xffffffffu, g[j], src);
-      h_slot = __shfl_sync(0xffffffffu, slot, src);
-      h_apply = occupied;
-    }
-#else
 #pragma unroll
     for (int j = 0; j < 9; ++j) hg[j] = g[j];
     h_slot = slot;
     h_apply = apply;
-#endif
     h_ti = ti;
     h_flags = t.flags;
     h_part0 = t.part0;

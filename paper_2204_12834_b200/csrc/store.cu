@@ -427,15 +427,15 @@ namespace {
 
 // Bank-aware renumbering of one chunk's accumulator slots (host).  The term
 // kernel's apply does 16-B shared-memory accesses to the 80-B record of each
-// distinct camera of a tile (its lowest lane); slot s's j-th piece lies in
-// bank group (5 s + j) mod 8, so leader lanes whose slots agree mod 8
-// serialise (measured: a warp's access costs about the largest number of its
-// leaders sharing a residue).  Slots are renumbered so that cameras seen in
-// the same tile tend to differ mod 8: greedy colouring (colour = slot mod 8,
-// most-seen camera first, colour capacities keep the numbering dense), colour
-// c's k-th camera gets slot 8k + c.  Only the numbering changes -- every sum
-// keeps its order, so results are bitwise unchanged.  `group` lanes form one
-// colouring group (32: the whole tile).
+// distinct camera of a tile (its lowest lane); a 16-B access is served eight
+// lanes at a time and slot s's j-th piece lies in bank group (5 s + j) mod 8,
+// so lanes of one eight-lane quarter whose slots agree mod 8 serialise.
+// Slots are renumbered so that cameras sharing quarters tend to differ mod 8:
+// greedy colouring (colour = slot mod 8, most-seen camera first, colour
+// capacities keep the numbering dense), colour c's k-th camera gets slot
+// 8k + c.  Only the numbering changes -- every sum keeps its order, so results
+// are bitwise unchanged.  `group` lanes form one colouring group (8: a
+// quarter; A/B in profiles/r01c_term_c5.md).
 void color_chunk_slots(const std::vector<int>& hcam, const std::vector<Tile>& tiles, const Chunk& q,
                        std::vector<int>& obs_slot, std::vector<int>& part_cam, int group) {
   const int n = q.nslot;
