@@ -17,6 +17,10 @@ namespace poba {
 
 namespace {
 
+constexpr int kLinRec = 11;  // double2 per staged camera-major record (10 used)
+constexpr int kLinRecSmem = kBlockTiles * kTile * kLinRec * 16;
+
+
 constexpr double kMinDepth = 1e-12;   // camera.py:22
 constexpr double kClampLo = 1e-6;     // blocks.py:36
 constexpr double kClampHi = 1e6;      // blocks.py:37
@@ -156,6 +160,9 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
            const int* __restrict__ cpos, double2* __restrict__ cmaj, unsigned long long* __restrict__ n_invalid) {
   __shared__ double contrib_all[kBlockTiles][kTile * 9];
   __shared__ int lstart_all[kBlockTiles][kTile + 1];
+  // per warp: the tile's camera-major records (J_p pairs + residual, 176-B
+  // stride so that 16-B accesses of eight consecutive lanes hit distinct banks)
+  extern __shared__ __align__(16) double2 lin_rec[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = tile0 + blockIdx.x * kBlockTiles + w;
   if (ti >= tile_end) return;  // warps are independent: no block-wide barrier below
@@ -208,11 +215,11 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
     m.r0 = stored<F32>(m.r0);
     m.r1 = stored<F32>(m.r1);
     Rz[o] = make_double2(m.r0, m.r1);
-    {  // camera-major copy of J_p and r for the U0 / b_p pass (160 contiguous bytes)
-      double2* cm = cmaj + (int64_t)cpos[o] * 10;
+    {  // this observation's camera-major record, staged for the cooperative write below
+      double2* rec = lin_rec + (w * kTile + lane) * kLinRec;
 #pragma unroll
-      for (int j = 0; j < 9; ++j) cm[j] = make_double2(m.jp0[j], m.jp1[j]);
-      cm[9] = make_double2(m.r0, m.r1);
+      for (int j = 0; j < 9; ++j) rec[j] = make_double2(m.jp0[j], m.jp1[j]);
+      rec[9] = make_double2(m.r0, m.r1);
     }
     double* cc = contrib + lane * 9;
     cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
@@ -231,6 +238,17 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   }
   if (lane == 0) lstart[t.nlm] = t.n;
   __syncwarp();
+  {  // camera-major copy of J_p and r for the U0 / b_p pass: each 160-B record
+     // is written by ten lanes as one contiguous run (three records per step)
+    const int my_pos = lane < t.n ? cpos[o] : 0;
+    const int sub = lane / 10, piece = lane - sub * 10;
+    const double2* rec = lin_rec + w * kTile * kLinRec;
+    for (int i0 = 0; i0 < t.n; i0 += 3) {
+      const int i = i0 + sub;
+      const int pos = __shfl_sync(0xffffffffu, my_pos, i & 31);
+      if (sub < 3 && i < t.n) cmaj[(int64_t)pos * 10 + piece] = rec[i * kLinRec + piece];
+    }
+  }
   const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
   if (lane == 0 && nbad) atomicAdd(n_invalid, (unsigned long long)nbad);
   __syncwarp();
@@ -453,7 +471,8 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   auto lin = [&](auto kern, const double* prep, const double* pts, const double* a, const double* b,
                  const double* r, int t0, int t1) {
     if (t1 <= t0) return;
-    kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, 0, s>>>(
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLinRecSmem);
+    kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, kLinRecSmem, s>>>(
         c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
         c.lidx_s.as<uint8_t>(), prep, pts, a, b, r, c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
         c.Dl.as<double>(), c.cpos.as<int>(), c.cmaj.as<double2>(), d_bad);
