@@ -42,6 +42,18 @@ def test_no_device_fails_loudly():
         _lib.Device(0)
 
 
+def test_local_group_host_contract():
+    """In-process virtual-rank groups (poba_local_group_create) are host objects: they are
+    created and destroyed without a GPU, and bad rank counts are rejected."""
+    from paper_2204_12834_b200 import _lib
+    g = _lib.LocalGroup(4)
+    assert g.nranks == 4
+    g.close()
+    for bad in (0, 9):
+        with pytest.raises(ValueError, match="nranks"):
+            _lib.LocalGroup(bad)
+
+
 def test_problem_validation_messages():
     from paper_2204_12834_b200.problem import Problem
     cams = np.zeros((2, 9))
