@@ -665,8 +665,10 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
 // W^T-type passes with landmark output (apply_wt, back-substitution, long z)
 // ---------------------------------------------------------------------------
 
+// (min 3 blocks per SM: lets ptxas keep the twelve plane loads in flight
+// together instead of sinking each next to its first use)
 template <int OUT, bool F32>
-__global__ void __launch_bounds__(kBlockTiles * kTile)
+__global__ void __launch_bounds__(kBlockTiles * kTile, 3)
 k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __restrict__ cam_s,
           const uint8_t* __restrict__ lidx_s, const void* __restrict__ J, const double* __restrict__ tin,
           const double* __restrict__ bl, const double* __restrict__ Vinv, double* __restrict__ out,
@@ -682,7 +684,13 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
   int* lstart = lstart_all[w];
   const int64_t o = (int64_t)ti * kTile + lane;
   if (lane < t.n) {
-    const double2* tv = reinterpret_cast<const double2*>(tin + (int64_t)cam_s[o] * kTStride);
+    // all twelve planes in flight first (one coalesced 512-B read per plane
+    // per warp), then the camera record they are contracted with
+    double2 jr[kJPlanes];
+#pragma unroll
+    for (int p = 0; p < kJPlanes; ++p) jr[p] = jload<F32>(J, o, p);
+    const int cam = cam_s[o];
+    const double2* tv = reinterpret_cast<const double2*>(tin + (int64_t)cam * kTStride);
     double tc[10];
 #pragma unroll
     for (int p = 0; p < 5; ++p) {
@@ -693,15 +701,11 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
     double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = jload<F32>(J, o, j);  // plane j: one coalesced 512-B read per warp
-      u0 = fma(v.x, tc[j], u0);
-      u1 = fma(v.y, tc[j], u1);
+      u0 = fma(jr[j].x, tc[j], u0);
+      u1 = fma(jr[j].y, tc[j], u1);
     }
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const double2 v = jload<F32>(J, o, 9 + b);
-      wbuf[lane * 3 + b] = fma(v.x, u0, v.y * u1);
-    }
+    for (int b = 0; b < 3; ++b) wbuf[lane * 3 + b] = fma(jr[9 + b].x, u0, jr[9 + b].y * u1);
     const int li = lidx_s[o];
     if (lane == 0 || lidx_s[o - 1] != li) lstart[li] = lane;
   }

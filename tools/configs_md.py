@@ -44,8 +44,15 @@ for k, r in d["configs"].items():
     out.append(f"| {k} | m={st['max_order']}, ε={st['epsilon']}, ≤{st['max_outer_iterations']} its | "
                + " | ".join(cell(r, c[0]) for c in cols)
                + f" | {r['gpu_lm']['costs'][-1]:.10g} | {ref_final} | {diff} |")
-out += ["", "C4/C5 reference LM runs are estimated at hours (SURVEY §8(d)) and were not run; their f* comes from "
-        "the GPU runs. PCG at C5 breaks down (p·Sp ≤ 0 in fp64 on the ill-conditioned λ = 1e-4 system), which "
-        "the reference's own `pcg` asserts on as well. PoST uses `max_cluster_size` = 100 (LmConfig default); its "
-        "time includes the host covisibility clustering."]
+broken = [k for k, r in d["configs"].items() if any(isinstance(v, dict) and "error" in v for v in r.values())]
+note = ("C4/C5 reference LM runs are estimated at hours (SURVEY §8(d)) and were not run; their f* comes from "
+        "the GPU runs. ")
+if broken:
+    note += (f"PCG breaks down on {', '.join(broken)} (p·Sp ≤ 0 in fp64 on the ill-conditioned λ = 1e-4 system), "
+             "which the reference's own `pcg` asserts on as well. ")
+note += ("PoST uses `max_cluster_size` = 100 (LmConfig default); its time includes the host covisibility "
+         "clustering. The final costs of different inner solvers differ on C3–C5 because each LM run stops at its "
+         "own relative-decrease test; the series solver's per-iteration costs match the reference to the listed "
+         "relative difference where the reference was run.")
+out += ["", note]
 print("\n".join(out))
