@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -431,15 +432,20 @@ namespace {
 // lanes at a time and slot s's j-th piece lies in bank group (5 s + j) mod 8,
 // so lanes of one eight-lane quarter whose slots agree mod 8 serialise.
 // Slots are renumbered so that cameras sharing quarters tend to differ mod 8:
-// greedy colouring (colour = slot mod 8, most-seen camera first, colour
-// capacities keep the numbering dense), colour c's k-th camera gets slot
-// 8k + c.  Only the numbering changes -- every sum keeps its order, so results
-// are bitwise unchanged.  `group` lanes form one colouring group (8: a
-// quarter; A/B in profiles/r01c_term_c5.md).
-void color_chunk_slots(const std::vector<int>& hcam, const std::vector<Tile>& tiles, const Chunk& q,
-                       std::vector<int>& obs_slot, std::vector<int>& part_cam, int group) {
+// colour = slot mod 8; greedy colouring (most-seen camera first) followed by
+// local-search passes that move a camera to the colour it shares the fewest
+// quarters with.  Colour classes may exceed n/8 by kSlotSlack (the chunk cut
+// leaves room), so the numbering can have holes: colour c's k-th camera gets
+// slot 8k + c, the chunk's slot count becomes 8 x (largest class), and a hole's
+// partial is written as zeros and never merged (camera -1).  Only the
+// numbering changes -- every sum keeps its order, so results are bitwise
+// unchanged.  `group` lanes form one colouring group (8: a quarter).
+// Returns the chunk's new camera-of-slot list (size = new slot count).
+std::vector<int> color_chunk_slots(const std::vector<Tile>& tiles, const Chunk& q, std::vector<int>& obs_slot,
+                                   const std::vector<int>& part_cam, int group, int passes) {
   const int n = q.nslot;
-  if (n <= 8) return;
+  std::vector<int> cam_of(part_cam.begin() + q.part0, part_cam.begin() + q.part0 + n);
+  if (n <= 8) return cam_of;
   // quarters of leader lanes (first lane of each camera in its tile)
   std::vector<int> occ_q, occ_s;  // quarter id, old slot of each leader
   std::vector<int> seen(n, -1);
@@ -467,31 +473,56 @@ void color_chunk_slots(const std::vector<int>& hcam, const std::vector<Tile>& ti
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return off[a + 1] - off[a] > off[b + 1] - off[b]; });
   std::vector<uint8_t> qcnt((size_t)nq * 8, 0);
-  std::vector<int> color(n, 0), cap(8), used(8, 0);
-  for (int c = 0; c < 8; ++c) cap[c] = n / 8 + (c < n % 8 ? 1 : 0);
-  for (int sl : order) {
-    int64_t cost[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::vector<int> color(n, -1), used(8, 0);
+  const int cap = (n + 7) / 8 + kSlotSlack;
+  auto costs = [&](int sl, int64_t* cost) {
+    for (int c = 0; c < 8; ++c) cost[c] = 0;
     for (int k = off[sl]; k < off[sl + 1]; ++k) {
       const uint8_t* qc = &qcnt[(size_t)qs[k] * 8];
       for (int c = 0; c < 8; ++c) cost[c] += qc[c];
     }
+  };
+  auto place = [&](int sl, int c, int d) {
+    for (int k = off[sl]; k < off[sl + 1]; ++k) qcnt[(size_t)qs[k] * 8 + c] += d;
+    used[c] += d;
+  };
+  int64_t cost[8];
+  for (int sl : order) {
+    costs(sl, cost);
     int best = -1;
     for (int c = 0; c < 8; ++c) {
-      if (used[c] >= cap[c]) continue;
+      if (used[c] >= cap) continue;
       if (best < 0 || cost[c] < cost[best] || (cost[c] == cost[best] && used[c] < used[best])) best = c;
     }
     color[sl] = best;
-    used[best]++;
-    for (int k = off[sl]; k < off[sl + 1]; ++k) qcnt[(size_t)qs[k] * 8 + best]++;
+    place(sl, best, 1);
   }
-  std::vector<int> slot_new(n), next(8, 0), cams(n);
+  for (int pass = 0; pass < passes; ++pass) {
+    int moved = 0;
+    for (int sl : order) {
+      const int cur = color[sl];
+      place(sl, cur, -1);
+      costs(sl, cost);
+      int best = cur;
+      for (int c = 0; c < 8; ++c)
+        if (c != cur && used[c] < cap && cost[c] < cost[best]) best = c;
+      color[sl] = best;
+      place(sl, best, 1);
+      moved += best != cur;
+    }
+    if (!moved) break;
+  }
+  int rows = 0;
+  for (int c = 0; c < 8; ++c) rows = std::max(rows, used[c]);
+  std::vector<int> slot_new(n), next(8, 0), cams(8 * rows, -1);
   for (int sl = 0; sl < n; ++sl) slot_new[sl] = 8 * next[color[sl]]++ + color[sl];
-  for (int sl = 0; sl < n; ++sl) cams[slot_new[sl]] = part_cam[q.part0 + sl];
-  for (int sl = 0; sl < n; ++sl) part_cam[q.part0 + sl] = cams[sl];
+  for (int sl = 0; sl < n; ++sl) cams[slot_new[sl]] = cam_of[sl];
+  while (!cams.empty() && cams.back() < 0) cams.pop_back();  // trailing holes need no partial
   for (int ti = q.tile0; ti < q.tile1; ++ti) {
     const int64_t s0 = (int64_t)ti * kTile;
     for (int i = 0; i < tiles[ti].n; ++i) obs_slot[s0 + i] = slot_new[obs_slot[s0 + i]];
   }
+  return cams;
 }
 
 }  // namespace
@@ -727,7 +758,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
           tstamp[cam] = ti;
           if (ch < 0 || stamp[cam] != ch) ++fresh;
         }
-        if (ch < 0 || cnt + fresh > kAccSlots) {
+        if (ch < 0 || cnt + fresh > kAccSlots - 8 * kSlotSlack) {
           if (ch >= 0) chunks.back().tile1 = ti;
           chunks.push_back(Chunk{ti, ti, (int)part_cam.size(), 0});
           ch = (int)chunks.size() - 1;
@@ -752,7 +783,42 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     if (!getenv("POBA_NO_SLOT_COLOR")) {
       const char* g = getenv("POBA_SLOT_GROUP");  // A/B: lanes per colouring group (8 = one quarter, 16, 32)
       const int group = (g && (atoi(g) == 16 || atoi(g) == 32)) ? atoi(g) : 8;
-      for (const Chunk& q : chunks) color_chunk_slots(hcam, tiles, q, obs_slot, part_cam, group);
+      const char* ps = getenv("POBA_SLOT_PASSES");  // A/B: local-search passes after the greedy colouring
+      const int passes = ps ? std::max(0, atoi(ps)) : kSlotPasses;
+      std::vector<int> pc;  // rebuilt camera of every partial (-1: hole)
+      pc.reserve(part_cam.size() + chunks.size() * 8 * kSlotSlack);
+      for (Chunk& q : chunks) {
+        std::vector<int> cams = color_chunk_slots(tiles, q, obs_slot, part_cam, group, passes);
+        q.part0 = (int)pc.size();
+        q.nslot = (int)cams.size();
+        pc.insert(pc.end(), cams.begin(), cams.end());
+      }
+      part_cam.swap(pc);
+    }
+    if (getenv("POBA_SLOT_STATS")) {  // bank-conflict model: sum over quarters of the largest residue class
+      int64_t wf = 0, ideal = 0;
+      std::vector<int> last(c.n_cam, -1);
+      for (int ti = 0; ti < c.n_tiles; ++ti) {
+        const int64_t s0 = (int64_t)ti * kTile;
+        int cnt[4][8] = {};
+        for (int i = 0; i < tiles[ti].n; ++i) {
+          const int cam = hcam[s0 + i];
+          if (last[cam] == ti) continue;
+          last[cam] = ti;
+          cnt[i / 8][obs_slot[s0 + i] & 7]++;
+        }
+        for (int qq = 0; qq < 4; ++qq) {
+          int mx = 0, tot = 0;
+          for (int r = 0; r < 8; ++r) {
+            mx = std::max(mx, cnt[qq][r]);
+            tot += cnt[qq][r];
+          }
+          wf += mx;
+          ideal += tot ? 1 : 0;
+        }
+      }
+      fprintf(stderr, "poba slot stats: %d chunks, %zu partials, %.3f wavefronts per apply access per tile (ideal %.3f)\n",
+              (int)chunks.size(), part_cam.size(), (double)wf / c.n_tiles, (double)ideal / c.n_tiles);
     }
     c.n_cta = n_cta;
     PTRY(c.cta_tiles.alloc(n_cta * sizeof(int2)));
@@ -789,10 +855,12 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   {  // camera -> partials, chunk order
     const int n_u = c.n_partials;
     std::vector<int> off(n_cam + 1, 0), idx(std::max(n_u, 1));
-    for (int p = 0; p < n_u; ++p) off[part_cam[p] + 1]++;
+    for (int p = 0; p < n_u; ++p)
+      if (part_cam[p] >= 0) off[part_cam[p] + 1]++;  // holes of the slot numbering are never merged
     for (int64_t q = 0; q < n_cam; ++q) off[q + 1] += off[q];
     std::vector<int> pos(off.begin(), off.end() - 1);
-    for (int p = 0; p < n_u; ++p) idx[pos[part_cam[p]]++] = p;
+    for (int p = 0; p < n_u; ++p)
+      if (part_cam[p] >= 0) idx[pos[part_cam[p]]++] = p;
     PTRY(c.part_idx.alloc(std::max(n_u, 1) * 4));
     PTRY(poba::copy_sync(c, c.part_idx.p, idx.data(), std::max(n_u, 1) * 4, cudaMemcpyHostToDevice));
     PTRY(c.part_cam_off.alloc((n_cam + 1) * 4));

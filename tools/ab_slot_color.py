@@ -3,7 +3,9 @@
     python tools/ab_slot_color.py [config] [scale] [variants...]
 
 variants: none (first-appearance numbering, POBA_NO_SLOT_COLOR), g8 / g16 /
-g32 (bank-aware colouring over groups of 8 / 16 / 32 lanes).  Builds the same
+g32 (bank-aware colouring over groups of 8 / 16 / 32 lanes), p0 / p4 / p8
+(greedy colouring followed by 0 / 4 / 8 local-search passes).  With
+POBA_SLOT_STATS=1 the library prints its bank-conflict model per build.  Builds the same
 problem once per variant (interleaved twice), times the fused term kernel
 with CUDA events inside the library, and checks that the series solution is
 bitwise identical across variants (only the slot numbering differs).
@@ -22,12 +24,14 @@ variants = sys.argv[3:] or ["none", "g32"]
 p = configs.make_config(name, scale, seed=0)
 out = {}
 for tag in variants * 2:
-    os.environ.pop("POBA_NO_SLOT_COLOR", None)
-    os.environ.pop("POBA_SLOT_GROUP", None)
+    for k in ("POBA_NO_SLOT_COLOR", "POBA_SLOT_GROUP", "POBA_SLOT_PASSES"):
+        os.environ.pop(k, None)
     if tag == "none":
         os.environ["POBA_NO_SLOT_COLOR"] = "1"
-    else:
+    elif tag.startswith("g"):
         os.environ["POBA_SLOT_GROUP"] = tag[1:]
+    elif tag.startswith("p"):
+        os.environ["POBA_SLOT_PASSES"] = tag[1:]
     dp = blocks.DeviceProblem(p.cam_indices, p.pt_indices, p.pixels, p.n_cameras, p.n_points)
     dev = dp.dev
     dev.set_points(p.points)
