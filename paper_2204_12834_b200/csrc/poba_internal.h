@@ -56,7 +56,7 @@ constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kTRecB
 static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
 static_assert(kAccSlots < 2048, "chunk slots must fit the 11-bit metadata field");
 constexpr int kSlotSlack = 2;   // extra slots per bank colour class in the slot numbering (store.cu)
-constexpr int kSlotPasses = 4;  // local-search passes of the slot colouring
+constexpr int kSlotPasses = 2;  // local-search passes of the slot colouring
 static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 
 // PoBA-32 (blocks.py:42-47): block storage may be fp32 (planes of float2);
