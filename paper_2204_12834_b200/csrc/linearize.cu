@@ -17,6 +17,9 @@ namespace poba {
 
 namespace {
 
+#ifndef POBA_LIN_COOP_PREP
+#define POBA_LIN_COOP_PREP 1
+#endif
 constexpr int kLinRec = 11;  // double2 per staged camera-major record (10 used)
 constexpr int kLinRecSmem = kBlockTiles * kTile * kLinRec * 16;
 
@@ -168,10 +171,43 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   if (ti >= tile_end) return;  // warps are independent: no block-wide barrier below
   double* contrib = contrib_all[w];
   int* lstart = lstart_all[w];
-  const Tile t = tiles[ti];
   const int64_t o = (int64_t)ti * kTile + lane;
+  // per-slot loads first, all independent of the tile descriptor (slot arrays
+  // cover the padding too), so their latencies overlap
+  const int cam_o = cam_s[o];
+  const int cpos_o = cpos[o];
+  const int li_o = lidx_s[o];
+  const Tile t = tiles[ti];
   const bool is_long = t.flags & kTileLong;
   bool bad = false;
+  double cp[16];  // this observation's camera record (R, t, f, k1, k2, pad)
+  if (!kExplicit) {
+    const int my_cam = lane < t.n ? cam_o : 0;
+#if POBA_LIN_COOP_PREP
+    // the tile's 32 camera records (128 B each) gathered cooperatively, four
+    // records per 16-B load instruction, through the warp's shared stage
+    // (144-B stride: conflict-free 16-B reads by consecutive lanes)
+    double2* pst = lin_rec + w * kTile * kLinRec;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int r = 4 * k + (lane >> 3), piece = lane & 7;
+      const int cam = __shfl_sync(0xffffffffu, my_cam, r);
+      if (r < t.n) pst[r * 9 + piece] = __ldg(reinterpret_cast<const double2*>(prep + (int64_t)cam * 16) + piece);
+    }
+    __syncwarp();
+    if (lane < t.n) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double2 v = pst[lane * 9 + k];
+        cp[2 * k] = v.x;
+        cp[2 * k + 1] = v.y;
+      }
+    }
+    __syncwarp();  // the stage is reused for the camera-major records below
+#else
+    if (lane < t.n) load_prep(prep, my_cam, cp);
+#endif
+  }
   if (lane < t.n) {
     ObsModel m;
     if (kExplicit) {
@@ -190,10 +226,8 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
       m.r1 = eres[f * 2 + 1];
       m.valid = true;
     } else {
-      const int lm = t.lm0 + (is_long ? 0 : lidx_s[o]);
+      const int lm = t.lm0 + (is_long ? 0 : li_o);
       const double* X = points + (int64_t)lm * 3;
-      double cp[16];
-      load_prep(prep, cam_s[o], cp);
       evaluate_obs<true>(cp, X[0], X[1], X[2], pix_s[o], m);
       bad = !m.valid;
     }
@@ -232,7 +266,7 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
     cc[7] = m.jl0[1] * m.r0 + m.jl1[1] * m.r1;
     cc[8] = m.jl0[2] * m.r0 + m.jl1[2] * m.r1;
     if (!is_long) {
-      const int li = lidx_s[o];
+      const int li = li_o;
       if (lane == 0 || lidx_s[o - 1] != li) lstart[li] = lane;
     }
   }
@@ -240,7 +274,7 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   __syncwarp();
   {  // camera-major copy of J_p and r for the U0 / b_p pass: each 160-B record
      // is written by ten lanes as one contiguous run (three records per step)
-    const int my_pos = lane < t.n ? cpos[o] : 0;
+    const int my_pos = lane < t.n ? cpos_o : 0;
     const int sub = lane / 10, piece = lane - sub * 10;
     const double2* rec = lin_rec + w * kTile * kLinRec;
     for (int i0 = 0; i0 < t.n; i0 += 3) {

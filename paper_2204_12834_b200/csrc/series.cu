@@ -678,18 +678,20 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = tile0 + blockIdx.x * kBlockTiles + w;
   if (ti >= tile_end) return;
+  const int64_t o = (int64_t)ti * kTile + lane;
+  // all twelve planes in flight first (one coalesced 512-B read per plane per
+  // warp; the tile block covers the padding lanes), together with the slot's
+  // camera and the tile descriptor; then the camera record
+  double2 jr[kJPlanes];
+#pragma unroll
+  for (int p = 0; p < kJPlanes; ++p) jr[p] = jload<F32>(J, o, p);
+  const int cam = cam_s[o];
+  const int li_o = lidx_s[o];
   const Tile t = tiles[ti];
   if (t.flags & kTileLong) return;  // handled by k_wt_long
   double* wbuf = wbuf_all[w];
   int* lstart = lstart_all[w];
-  const int64_t o = (int64_t)ti * kTile + lane;
   if (lane < t.n) {
-    // all twelve planes in flight first (one coalesced 512-B read per plane
-    // per warp), then the camera record they are contracted with
-    double2 jr[kJPlanes];
-#pragma unroll
-    for (int p = 0; p < kJPlanes; ++p) jr[p] = jload<F32>(J, o, p);
-    const int cam = cam_s[o];
     const double2* tv = reinterpret_cast<const double2*>(tin + (int64_t)cam * kTStride);
     double tc[10];
 #pragma unroll
@@ -706,7 +708,7 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
     }
 #pragma unroll
     for (int b = 0; b < 3; ++b) wbuf[lane * 3 + b] = fma(jr[9 + b].x, u0, jr[9 + b].y * u1);
-    const int li = lidx_s[o];
+    const int li = li_o;
     if (lane == 0 || lidx_s[o - 1] != li) lstart[li] = lane;
   }
   if (lane == 0) lstart[t.nlm] = t.n;
