@@ -335,26 +335,18 @@ __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restric
   }
 }
 
-__device__ __forceinline__ int find_camera(const int* __restrict__ off, int n_cam, int cc) {
-  int lo = 0, hi = n_cam;  // last camera with off[c] <= cc
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (off[mid] <= cc) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 
 // U0 (packed upper 45) and b_p (9) partial sums over chunks of <= 128 observations
 // of one camera, walked in camera-major order; fixed warp-butterfly reduction.
 // (A variant staging each group of 32 records through shared memory with
 // coalesced loads was slower: 230 registers, 2.5 vs 1.7 ms at C5.)
 __global__ void __launch_bounds__(kCamReduceThreads)
-k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cam_start,
-                   const double2* __restrict__ cmaj, int n_cam, int n_cc, double* __restrict__ out) {
+k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cc_cam, const int* __restrict__ cam_start,
+                   const double2* __restrict__ cmaj, int n_cc, double* __restrict__ out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_cc) return;
-  const int cam = find_camera(cc_cam_off, n_cam, warp);
+  const int cam = cc_cam[warp];
   const int p0 = cam_start[cam] + (warp - cc_cam_off[cam]) * kCamChunk;
   const int p1 = min(p0 + kCamChunk, cam_start[cam + 1]);
   double acc[54];
@@ -550,8 +542,8 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   // camera side: U0 / b_p via camera-major chunks, then a fixed-order merge
   if (c.n_cchunks) {
     const unsigned g = grid_for((int64_t)c.n_cchunks * 32, kCamReduceThreads);
-    k_cam_chunk_reduce<<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(),
-                                                      c.cmaj.as<double2>(), (int)c.n_cam, c.n_cchunks,
+    k_cam_chunk_reduce<<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_cam.as<int>(),
+                                                      c.cam_start.as<int>(), c.cmaj.as<double2>(), c.n_cchunks,
                                                       c.cc_part.as<double>());
     c.launches++;
   }

@@ -22,27 +22,18 @@ void launch_cam_mv(Ctx& c, const double* M45, const double* v, double* out);
 
 namespace {
 
-__device__ __forceinline__ int find_cam(const int* __restrict__ off, int n_cam, int cc) {
-  int lo = 0, hi = n_cam;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (off[mid] <= cc) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // per camera-major chunk (<= kCamChunk observations of one camera):
 // sum of W_o V_l^-1 W_o^T, W_o = J_p^T J_l (9x3), packed upper 45
 template <bool F32>
 __global__ void __launch_bounds__(128)
-k_schur_diag_chunk(const int* __restrict__ cc_cam_off, const int* __restrict__ cam_start,
+k_schur_diag_chunk(const int* __restrict__ cc_cam_off, const int* __restrict__ cc_cam, const int* __restrict__ cam_start,
                    const int* __restrict__ cperm, const void* __restrict__ J, const Tile* __restrict__ tiles,
                    const uint8_t* __restrict__ lidx_s, const double* __restrict__ Vinv, int n_cam, int n_cc,
                    double* __restrict__ out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_cc) return;
-  const int cam = find_cam(cc_cam_off, n_cam, warp);
+  const int cam = cc_cam[warp];
   const int p0 = cam_start[cam] + (warp - cc_cam_off[cam]) * kCamChunk;
   const int p1 = min(p0 + kCamChunk, cam_start[cam + 1]);
   double acc[45];
@@ -152,12 +143,12 @@ int schur_diag_device(Ctx& c, double* d_out45 /* nullable */) {
     const int threads = 128;
     const unsigned g = grid_for((int64_t)c.n_cchunks * 32, threads);
     if (c.precision == 32)
-      k_schur_diag_chunk<true><<<g, threads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
+      k_schur_diag_chunk<true><<<g, threads, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_cam.as<int>(), c.cam_start.as<int>(), c.cperm.as<int>(),
                                                      c.J.p, c.tiles.as<Tile>(), c.lidx_s.as<uint8_t>(),
                                                      c.Vinv.as<double>(), (int)n_cam, c.n_cchunks,
                                                      c.cc_part.as<double>());
     else
-      k_schur_diag_chunk<false><<<g, threads, 0, s>>>(c.cc_cam_off.as<int>(), c.cam_start.as<int>(),
+      k_schur_diag_chunk<false><<<g, threads, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_cam.as<int>(), c.cam_start.as<int>(),
                                                       c.cperm.as<int>(), c.J.p, c.tiles.as<Tile>(),
                                                       c.lidx_s.as<uint8_t>(), c.Vinv.as<double>(), (int)n_cam,
                                                       c.n_cchunks, c.cc_part.as<double>());

@@ -279,6 +279,7 @@ struct Ctx {
   DBuf cmaj;         // double2 [n_obs_l][10] J_p column pairs + residual, camera-major (U0 / b_p pass)
   DBuf cam_start;    // int32 [n_cam+1] camera -> first position in cperm
   DBuf cc_cam_off;   // int32 [n_cam+1] camera -> cchunk range
+  DBuf cc_cam;       // int32 [n_cchunks] cchunk -> camera
 
   // store (K1), slot space
   DBuf J;            // [n_tiles] tile blocks (metadata + 12 planes): double2 planes, or float2 at precision 32

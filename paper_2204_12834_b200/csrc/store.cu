@@ -160,6 +160,13 @@ __global__ void k_cam_degree(const uint64_t* __restrict__ key, int64_t n, int* _
   if (i < n) atomicAdd(&deg[(int)(key[i] >> 32)], 1);
 }
 
+// camera of every camera-major reduction chunk (replaces a per-warp binary search)
+__global__ void k_cc_cam(const int* __restrict__ cc_cam_off, int64_t n_cam, int* __restrict__ cc_cam) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= n_cam) return;
+  for (int k = cc_cam_off[c]; k < cc_cam_off[c + 1]; ++k) cc_cam[k] = (int)c;
+}
+
 __global__ void k_cc_counts(const int* __restrict__ deg, int64_t n_cam, int* __restrict__ cnt) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c < n_cam) cnt[c] = (deg[c] + kCamChunk - 1) / kCamChunk;
@@ -895,6 +902,10 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PCK(cudaMemcpyAsync(&ncc, c.cc_cam_off.as<int>() + n_cam, 4, cudaMemcpyDeviceToHost, s));
     PCK(cudaStreamSynchronize(s));
     c.n_cchunks = ncc;
+    PTRY(c.cc_cam.alloc((size_t)std::max(ncc, 1) * 4));
+    k_cc_cam<<<grid_for(n_cam, B), B, 0, s>>>(c.cc_cam_off.as<int>(), n_cam, c.cc_cam.as<int>());
+    c.launches++;
+    PCK(cudaGetLastError());
   }
 
   // --- store rows (J + metadata) and work buffers ------------------------------------------------------------
