@@ -526,10 +526,17 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
   if (cam < a.n_cam) {
     if (kFromPartials) {
       const int p0 = a.part_cam_off[cam], p1 = a.part_cam_off[cam + 1];
-      for (int p = p0 + lane; p < p1; p += 32) {
-        const double* src = a.partials + (int64_t)a.part_idx[p] * kTStride;
+      for (int p = p0 + lane; p < p1; p += 32) {  // 80-B partial records: five 16-B loads
+        const double2* src = reinterpret_cast<const double2*>(a.partials + (int64_t)a.part_idx[p] * kTStride);
+        double v[10];
 #pragma unroll
-        for (int j = 0; j < 9; ++j) r[j] += src[j];
+        for (int k = 0; k < 5; ++k) {
+          const double2 w = src[k];
+          v[2 * k] = w.x;
+          v[2 * k + 1] = w.y;
+        }
+#pragma unroll
+        for (int j = 0; j < 9; ++j) r[j] += v[j];
       }
 #pragma unroll
       for (int j = 0; j < 9; ++j)
