@@ -338,8 +338,9 @@ __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restric
 
 // U0 (packed upper 45) and b_p (9) partial sums over chunks of <= 128 observations
 // of one camera, walked in camera-major order; fixed warp-butterfly reduction.
-// (A variant staging each group of 32 records through shared memory with
-// coalesced loads was slower: 230 registers, 2.5 vs 1.7 ms at C5.)
+// (Variants staging each group of 32 records through shared memory -- with
+// coalesced loads, or double-buffered with cp.async -- were slower; see
+// profiles/r01e_linearize_ab.md.)
 __global__ void __launch_bounds__(kCamReduceThreads)
 k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cc_cam, const int* __restrict__ cam_start,
                    const double2* __restrict__ cmaj, int n_cc, double* __restrict__ out) {
@@ -352,8 +353,7 @@ k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ c
   double acc[54];
 #pragma unroll
   for (int q = 0; q < 54; ++q) acc[q] = 0.0;
-  for (int p = p0 + lane; p < p1; p += 32) {
-    const double2* cm = cmaj + (int64_t)p * 10;
+  auto fold = [&](const double2* cm) {  // one record: 45 products of J_p, 9 of J_p with r
     double a[9], b[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
@@ -369,7 +369,8 @@ k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ c
       for (int j = i; j < 9; ++j) acc[q++] += a[i] * a[j] + b[i] * b[j];
 #pragma unroll
     for (int i = 0; i < 9; ++i) acc[45 + i] += a[i] * r.x + b[i] * r.y;
-  }
+  };
+  for (int p = p0 + lane; p < p1; p += 32) fold(cmaj + (int64_t)p * 10);
 #pragma unroll
   for (int q = 0; q < 54; ++q) {
     double v = acc[q];

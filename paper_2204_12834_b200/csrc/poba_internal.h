@@ -32,7 +32,10 @@ constexpr int kMetaBytes = kTile * 4;                 // per-tile metadata words
 constexpr int kTileBlock = kMetaBytes + 12 * kTile * 16;  // 6272 B per warp-tile (fp64 planes)
 constexpr int kTileBlockF32 = kMetaBytes + 12 * kTile * 8;  // 3200 B (fp32 planes, PoBA-32)
 constexpr int kBlockTiles = 8;    // warp-tiles per CTA in the streaming kernels (256 threads)
-constexpr int kCamChunk = 128;    // observations per camera-major reduction chunk
+#ifndef POBA_CAM_CHUNK
+#define POBA_CAM_CHUNK 1024
+#endif
+constexpr int kCamChunk = POBA_CAM_CHUNK;  // observations per camera-major reduction chunk
 constexpr int kJPlanes = 12;      // Jacobian column pairs per row
 #ifndef POBA_TERM_WARPS
 #define POBA_TERM_WARPS 12

@@ -56,3 +56,30 @@ def test_entry_points_bitwise_repeatable(name, precision):
         ref = np.array(fn(), copy=True)
         for _ in range(REPS):
             assert np.array_equal(np.asarray(fn()), ref), label
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_slot_numbering_does_not_change_results(name, monkeypatch):
+    """The bank-aware accumulator slot numbering (store.cu color_chunk_slots) only renames
+    slots: with it off (first-appearance numbering) every series term and the solve are
+    bitwise identical."""
+    from paper_2204_12834_b200 import blocks, configs
+    p = configs.make_config(name, 0.1 if name == "c3" else 0.02)
+
+    def solve():
+        dp = blocks.DeviceProblem(p.cam_indices, p.pt_indices, p.pixels, p.n_cameras, p.n_points)
+        dev = dp.dev
+        dev.set_points(p.points)
+        dev.linearize(p.camera_params)
+        dev.damp(1e-4)
+        x, order, _, _ = dev.series_solve(1e-300, 10)
+        dl, _ = dev.back_substitute()
+        info = dev.info()
+        dev.close()
+        return x, dl, info
+
+    x0, dl0, i0 = solve()
+    monkeypatch.setenv("POBA_NO_SLOT_COLOR", "1")
+    x1, dl1, i1 = solve()
+    assert i0["n_chunks"] == i1["n_chunks"]
+    assert np.array_equal(x0, x1) and np.array_equal(dl0, dl1)
