@@ -181,6 +181,15 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   const bool is_long = t.flags & kTileLong;
   bool bad = false;
   double cp[16];  // this observation's camera record (R, t, f, k1, k2, pad)
+  double X0 = 0.0, X1 = 0.0, X2 = 0.0;
+  double2 pix = make_double2(0.0, 0.0);
+  if (!kExplicit && lane < t.n) {  // point and pixel loads in flight during the camera gather
+    const double* X = points + (int64_t)(t.lm0 + (is_long ? 0 : li_o)) * 3;
+    X0 = X[0];
+    X1 = X[1];
+    X2 = X[2];
+    pix = pix_s[o];
+  }
   if (!kExplicit) {
     const int my_cam = lane < t.n ? cam_o : 0;
 #if POBA_LIN_COOP_PREP
@@ -226,9 +235,7 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
       m.r1 = eres[f * 2 + 1];
       m.valid = true;
     } else {
-      const int lm = t.lm0 + (is_long ? 0 : li_o);
-      const double* X = points + (int64_t)lm * 3;
-      evaluate_obs<true>(cp, X[0], X[1], X[2], pix_s[o], m);
+      evaluate_obs<true>(cp, X0, X1, X2, pix, m);
       bad = !m.valid;
     }
     // at precision 32 every stored value is rounded to fp32 first and all
