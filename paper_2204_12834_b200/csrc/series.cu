@@ -357,15 +357,17 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
         vi[2 * p + 1] = v.y;
       }
     }
+    // Lanes past the tile's end read stale stage entries: harmless, since
+    // they are never a landmark's last lane, the segmented scan only pulls
+    // from lower lanes, and they apply nothing (no select needed).
     double2 jr[kJPlanes];
 #pragma unroll
     for (int p = 0; p < kJPlanes; ++p) {
       if (F32) {
-        const float2 v =
-            valid ? reinterpret_cast<const float2*>(stg + kMetaBytes)[p * kTile + lane] : make_float2(0.f, 0.f);
+        const float2 v = reinterpret_cast<const float2*>(stg + kMetaBytes)[p * kTile + lane];
         jr[p] = make_double2((double)v.x, (double)v.y);
       } else {
-        jr[p] = valid ? reinterpret_cast<const double2*>(stg + kMetaBytes)[p * kTile + lane] : make_double2(0.0, 0.0);
+        jr[p] = reinterpret_cast<const double2*>(stg + kMetaBytes)[p * kTile + lane];
       }
     }
     // Refill the stage with this warp's next tile.  The bulk copy writes
