@@ -157,6 +157,9 @@ int poba_cost(poba_ctx* ctx, const double* cam_params, const double* points, int
 int poba_set_points(poba_ctx* ctx, const double* points);
 int poba_accept_points(poba_ctx* ctx); /* points += last delta_l (lm.py:140) */
 int poba_get_points(poba_ctx* ctx, double* points);
+/* every rank's rows (sharded contexts; collective: all ranks call it) -- the
+   state lm.run returns (lm.py:228-232, BaState) */
+int poba_get_points_all(poba_ctx* ctx, double* points);
 
 /* ---- operator passes (DampedSystem.apply_*, blocks.py:214-254) --------------- */
 #define POBA_OP_W 0      /* (3 n_pt) -> (9 n_cam)   */

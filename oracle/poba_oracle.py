@@ -693,3 +693,65 @@ def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
             tr.iterations.append(OracleIter(it, c, lam, order, False, tbad, inner))
             tr.times.append(clock() - t0)
     return tr, cams, pts
+
+
+# ---------------------------------------------------------------------------
+# configuration-scale operator passes (C restatement, oracle/poba_term.c)
+# ---------------------------------------------------------------------------
+
+_TERM_LIB = None
+
+
+def term_library():
+    """ctypes handle of oracle/lib/libpoba_oracle.so (built by ``make oracle``);
+    None if it is not built.  Test infrastructure, like the rest of this file."""
+    global _TERM_LIB
+    if _TERM_LIB is None:
+        import ctypes
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libpoba_oracle.so")
+        if not os.path.exists(path):
+            return None
+        lib = ctypes.CDLL(path)
+        P = ctypes.c_void_p
+        for name in ("oracle_apply_wt", "oracle_apply_w"):
+            f = getattr(lib, name)
+            f.restype = ctypes.c_int
+            f.argtypes = [ctypes.c_int64, P, P, P, ctypes.c_int64, P, P, ctypes.c_int]
+        lib.oracle_max_threads.restype = ctypes.c_int
+        _TERM_LIB = lib
+    return _TERM_LIB
+
+
+class ScaleOracleSystem(OracleSystem):
+    """OracleSystem whose W and W^T passes (blocks.py:214-236) run in the C
+    restatement (oracle/poba_term.c, OpenMP over landmark runs / observation
+    ranges) -- for parity checks at C4/C5 size.  U^-1, V^-1, b_tilde, the
+    damping and the inverses are the numpy restatement above."""
+
+    def __init__(self, lin: OracleLin, lam: float, damping: str = "marquardt", threads: int | None = None):
+        super().__init__(lin, lam, damping)
+        self._lib = term_library()
+        if self._lib is None:
+            raise RuntimeError("oracle/lib/libpoba_oracle.so is not built (make oracle)")
+        self.threads = int(threads or self._lib.oracle_max_threads())
+        self._store = np.ascontiguousarray(lin.store, dtype=np.float64)
+        self._cs = np.ascontiguousarray(lin.cam_sorted, dtype=np.int64)
+        self._ps = np.ascontiguousarray(lin.pt_sorted, dtype=np.int64)
+
+    def _call(self, fn, n_out_rows, width, v):
+        v = np.ascontiguousarray(v, dtype=np.float64).ravel()
+        out = np.empty(n_out_rows * width)
+        rc = fn(len(self._cs), self._store.ctypes.data, self._cs.ctypes.data, self._ps.ctypes.data, n_out_rows,
+                v.ctypes.data, out.ctypes.data, self.threads)
+        if rc:
+            raise MemoryError("oracle pass failed")
+        return out
+
+    def apply_w(self, v_l):
+        self.passes["w"] += 1
+        return self._call(self._lib.oracle_apply_w, self.n_cameras, POSE, v_l)
+
+    def apply_wt(self, v_p):
+        self.passes["wt"] += 1
+        return self._call(self._lib.oracle_apply_wt, self.n_points, POINT, v_p)

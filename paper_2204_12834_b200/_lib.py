@@ -52,6 +52,7 @@ _SIGS = {
     "poba_set_points": (ctypes.c_int, [_P, _DP]),
     "poba_accept_points": (ctypes.c_int, [_P]),
     "poba_get_points": (ctypes.c_int, [_P, _DP]),
+    "poba_get_points_all": (ctypes.c_int, [_P, _DP]),
     "poba_apply": (ctypes.c_int, [_P, ctypes.c_int, _DP, _DP]),
     "poba_read": (ctypes.c_int, [_P, ctypes.c_int, _DP]),
     "poba_time_terms": (ctypes.c_int, [_P, ctypes.c_int, _DP, _DP, _IP]),
@@ -268,6 +269,13 @@ class Device:
         else:  # a shard fills only its own rows
             out = np.zeros((self.n_pt, 3)) if self.nranks > 1 else host_empty((self.n_pt, 3))
         _check(self._lib.poba_get_points(self._h, _d(out)))
+        return out
+
+    def get_points_all(self):
+        """Every landmark's point: a sharded context gathers the other ranks' rows
+        (collective -- every rank calls it)."""
+        out = host_empty((self.n_pt, 3))
+        _check(self._lib.poba_get_points_all(self._h, _d(out)))
         return out
 
     def accept_points(self):

@@ -12,6 +12,7 @@ attributes the reference exposes as arrays (``U0``, ``V``, ``U_inv``, ``b_p``,
 from __future__ import annotations
 
 import logging
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -59,6 +60,12 @@ class DeviceProblem:
         self.source = None           # what produced the current linearization
         self._ordering = None
         self._groups = None
+        # One context is shared by every system built on this problem.  Each
+        # activate-then-call sequence, and a whole lm.run, holds this lock, so
+        # concurrent runs on one problem (the reference's
+        # evalkit.run_benchmark(parallel=True), evalkit.py:162-196) serialise
+        # on the device instead of overwriting each other's state mid-solve.
+        self.lock = threading.RLock()
 
     def ordering(self):
         if self._ordering is None:
@@ -76,23 +83,62 @@ def _signature(problem):
             problem.cam_indices.shape, problem.n_cameras, problem.n_points)
 
 
+_FULL_COPY_OBS = 2_000_000
+
+
 def _snapshot(problem):
-    """Cheap content check of the observation arrays (full for small problems)."""
-    n = problem.cam_indices.shape[0]
-    if n <= 2_000_000:
-        return (problem.cam_indices.copy(), problem.pt_indices.copy(), np.array(problem.pixels, copy=True))
-    idx = np.linspace(0, n - 1, 4096).astype(np.int64)
-    return (problem.cam_indices[idx].copy(), problem.pt_indices[idx].copy(), np.array(problem.pixels[idx]))
+    """What a cached device store is validated against on the next lookup.
+
+    Up to 2M observations: full copies of the observation arrays, compared
+    element-wise.  Larger problems (C4, C5) are not copied; instead the arrays
+    are made read-only for as long as the cache holds them, so an in-place edit
+    raises at the write instead of silently reusing a stale device store (the
+    flags are restored by ``invalidate``).  Arrays that are views of memory we
+    cannot lock are validated by a full-content digest on every lookup."""
+    arrs = (problem.cam_indices, problem.pt_indices, problem.pixels)
+    if problem.cam_indices.shape[0] <= _FULL_COPY_OBS:
+        return ("copy", tuple(np.array(a, copy=True) for a in arrs))
+    locked = []
+    for a in arrs:
+        if isinstance(a, np.ndarray) and a.base is None and a.flags.writeable:
+            a.flags.writeable = False
+            locked.append(a)
+    if all(isinstance(a, np.ndarray) and (a.base is None) and not a.flags.writeable for a in arrs):
+        return ("locked", locked)
+    return ("digest", _digest(arrs), locked)
+
+
+def _digest(arrs):
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    for a in arrs:
+        h.update(np.ascontiguousarray(a).view(np.uint8).reshape(-1))
+    return h.digest()
 
 
 def _same_snapshot(problem, snap):
-    n = problem.cam_indices.shape[0]
-    if n <= 2_000_000:
-        arrs = (problem.cam_indices, problem.pt_indices, problem.pixels)
-    else:
-        idx = np.linspace(0, n - 1, 4096).astype(np.int64)
-        arrs = (problem.cam_indices[idx], problem.pt_indices[idx], problem.pixels[idx])
-    return all(np.array_equal(a, b) for a, b in zip(arrs, snap))
+    arrs = (problem.cam_indices, problem.pt_indices, problem.pixels)
+    if snap[0] == "copy":
+        return all(a.shape == b.shape and np.array_equal(a, b) for a, b in zip(arrs, snap[1]))
+    if snap[0] == "locked":
+        return all(not a.flags.writeable for a in arrs)
+    return _digest(arrs) == snap[1]
+
+
+def invalidate(problem) -> None:
+    """Drop ``problem``'s cached device store (call after editing its observation
+    arrays in place) and restore the write flags the cache set."""
+    cached = getattr(problem, "_poba_device", None)
+    if cached is None:
+        return
+    snap = cached[1]
+    if snap[0] in ("locked", "digest"):
+        for a in snap[-1]:
+            a.flags.writeable = True
+    try:
+        object.__delattr__(problem, "_poba_device")
+    except AttributeError:
+        pass
 
 
 def device_problem(problem, device: int = 0) -> DeviceProblem:
@@ -101,6 +147,8 @@ def device_problem(problem, device: int = 0) -> DeviceProblem:
     sig = _signature(problem)
     if cached is not None and cached[0] == sig and _same_snapshot(problem, cached[1]):
         return cached[2]
+    if cached is not None:
+        invalidate(problem)
     dp = DeviceProblem(problem.cam_indices, problem.pt_indices, problem.pixels, problem.n_cameras,
                        problem.n_points, device=device)
     try:
@@ -168,8 +216,9 @@ class LandmarkBlockStore:
     @property
     def storage_obs(self):
         if self._storage is None:
-            self._lin._activate()
-            self._storage = self._dp.dev.read(_lib.READ_STORAGE).astype(self.dtype, copy=False)
+            with self._dp.lock:
+                self._lin._activate()
+                self._storage = self._dp.dev.read(_lib.READ_STORAGE).astype(self.dtype, copy=False)
         return self._storage
 
     @property
@@ -198,6 +247,25 @@ class LandmarkBlockStore:
 # Linearization / DampedSystem
 # ---------------------------------------------------------------------------
 
+_STATE_COPY_BYTES = 32 << 20
+
+
+def _sample_index(n):
+    return np.unique(np.linspace(0, n - 1, min(n, 65536)).astype(np.int64))
+
+
+def _frozen_state(cams, pts):
+    """The state a Linearization re-linearizes from if another linearization
+    replaced it on the device.  Cameras are always copied; points are copied up
+    to 32 MB (every config but C5), larger point arrays are kept by reference
+    with a sampled fingerprint that is re-checked before they are used again,
+    so an in-place edit fails loudly instead of silently changing the system."""
+    cams = np.array(cams, dtype=np.float64, copy=True)
+    if pts.nbytes <= _STATE_COPY_BYTES:
+        return cams, np.array(pts, dtype=np.float64, copy=True), None
+    idx = _sample_index(len(pts))
+    return cams, pts, (idx, pts[idx].copy())
+
 class Linearization:
     """Device linearization (reference blocks.py:115-137); arrays read back lazily."""
 
@@ -219,6 +287,11 @@ class Linearization:
         if dp.generation == self._gen:
             return
         kind = self._source[0]
+        if kind == "state" and self._source[3] is not None:
+            idx, vals = self._source[3]
+            if not np.array_equal(self._source[2][idx], vals):
+                raise ValueError("the points array this linearization was built from was modified in "
+                                 "place; linearize the new state instead")
         dp.dev.set_precision(self.precision)
         if kind == "state":
             dp.dev.linearize(self._source[1], self._source[2])
@@ -230,8 +303,9 @@ class Linearization:
 
     def _read(self, key, what):
         if key not in self._cache:
-            self._activate()
-            self._cache[key] = self._dp.dev.read(what)
+            with self._dp.lock:
+                self._activate()
+                self._cache[key] = self._dp.dev.read(what)
         return self._cache[key]
 
     @property
@@ -303,10 +377,11 @@ class DampedSystem:
         self.lam = float(lam)
         self.damping = damping
         self._dp = lin._dp
-        lin._activate()
-        self._dp.dev.damp(self.lam, damping == "identity")
-        self._dp.active_system = self
-        self._gen = self._dp.generation
+        with self._dp.lock:
+            lin._activate()
+            self._dp.dev.damp(self.lam, damping == "identity")
+            self._dp.active_system = self
+            self._gen = self._dp.generation
         self.counters = OperatorCounts()
         self._b_tilde = None
         self._cache = {}
@@ -321,8 +396,9 @@ class DampedSystem:
 
     def _read(self, key, what):
         if key not in self._cache:
-            self._activate()
-            self._cache[key] = self._dp.dev.read(what)
+            with self._dp.lock:
+                self._activate()
+                self._cache[key] = self._dp.dev.read(what)
         return self._cache[key]
 
     # -- attributes ------------------------------------------------------------
@@ -382,8 +458,9 @@ class DampedSystem:
 
     # -- operator passes ------------------------------------------------------------
     def _op(self, op, v):
-        self._activate()
-        return self._dp.dev.apply(op, v)
+        with self._dp.lock:
+            self._activate()
+            return self._dp.dev.apply(op, v)
 
     def apply_w(self, v_l):
         """W v_l, landmark space to pose space (blocks.py:214-224)."""
@@ -423,8 +500,9 @@ class DampedSystem:
             if self._b_l_override is not None:
                 self._b_tilde = self.b_p - self.apply_w(self.apply_v_inv(self._b_l_override))
             else:
-                self._activate()
-                self._b_tilde = self._dp.dev.read(_lib.READ_B_TILDE)
+                with self._dp.lock:
+                    self._activate()
+                    self._b_tilde = self._dp.dev.read(_lib.READ_B_TILDE)
                 self.counters.w += 1
                 self.counters.v_inv += 1
         return self._b_tilde
@@ -449,13 +527,12 @@ def linearize(problem, state=None, precision: int = 64, device: int = 0) -> Line
     cams = np.ascontiguousarray(state.camera_params, dtype=np.float64)
     pts = np.ascontiguousarray(state.points, dtype=np.float64)
     dp = device_problem(problem, device)
-    dp.dev.set_precision(precision)
-    n_invalid = dp.dev.linearize(cams, pts)
-    if n_invalid:
-        log.warning("%d observation(s) had zero projected depth and were zeroed", n_invalid)
-    # the source arrays are kept by reference (no copy), like the reference keeps
-    # no copy at all; callers must not mutate them while the Linearization lives
-    return Linearization(dp, ("state", cams, pts), n_invalid, precision)
+    with dp.lock:
+        dp.dev.set_precision(precision)
+        n_invalid = dp.dev.linearize(cams, pts)
+        if n_invalid:
+            log.warning("%d observation(s) had zero projected depth and were zeroed", n_invalid)
+        return Linearization(dp, ("state",) + _frozen_state(cams, pts), n_invalid, precision)
 
 
 def assemble(problem, state=None, lam: float = 1e-4, precision: int = 64,

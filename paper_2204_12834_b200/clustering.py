@@ -115,9 +115,10 @@ def solve_clustered(system, partition: CameraClustering, epsilon: float = 0.01,
     sys_ = _device_system(system)
     if partition.assignment.shape[0] != sys_.n_cameras:
         raise ValueError("partition does not match the system's camera count")
-    vs = _virtual_store(sys_, partition)
-    vs.linearize_like(sys_.lin)
-    vs.dp.dev.damp(sys_.lam, sys_.damping == "identity")
-    dp, order, conv = vs.dp.dev.series_solve_clustered(partition.assignment, partition.n_clusters, epsilon,
-                                                       max_order)
+    with sys_._dp.lock:
+        vs = _virtual_store(sys_, partition)
+        vs.linearize_like(sys_.lin)
+        vs.dp.dev.damp(sys_.lam, sys_.damping == "identity")
+        dp, order, conv = vs.dp.dev.series_solve_clustered(partition.assignment, partition.n_clusters, epsilon,
+                                                           max_order)
     return ClusteredSolveResult(dp, order, conv)

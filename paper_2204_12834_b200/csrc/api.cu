@@ -608,6 +608,47 @@ int poba_get_points(poba_ctx* ctx, double* points) {
   return poba::lm_download(c, c.points.as<double>(), 3, points);
 }
 
+// every rank's landmark rows, gathered (a sharded context's poba_get_points
+// fills only its own rows): the ranks' (lm_lo, n_lm_l) pairs are all-gathered
+// first, then the file-order rows padded to the largest shard, so the gather
+// is exact (no arithmetic on the values).
+int poba_get_points_all(poba_ctx* ctx, double* points) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_points, "no device points");
+  NEED(points, "null points");
+  if (c.nranks <= 1) return poba::lm_download(c, c.points.as<double>(), 3, points);
+  const int R = c.nranks;
+  DBuf d_rng, d_all;
+  PTRY(d_rng.alloc(2 * 8));
+  PTRY(d_all.alloc((size_t)2 * R * 8));
+  const double rng[2] = {(double)c.lm_lo, (double)c.n_lm_l};
+  PTRY(poba::copy_sync(c, d_rng.p, rng, sizeof rng, cudaMemcpyHostToDevice));
+  PTRY(poba::allgather(c, d_rng.as<double>(), d_all.as<double>(), 2));
+  std::vector<double> all(2 * R);
+  PTRY(poba::copy_sync(c, all.data(), d_all.p, all.size() * 8, cudaMemcpyDeviceToHost));
+  int64_t maxn = 1;
+  for (int r = 0; r < R; ++r) maxn = std::max<int64_t>(maxn, (int64_t)all[2 * r + 1]);
+  DBuf d_mine, d_rows;
+  PTRY(d_mine.alloc((size_t)maxn * 3 * 8));
+  PTRY(d_rows.alloc((size_t)R * maxn * 3 * 8));
+  PCK(cudaMemsetAsync(d_mine.p, 0, (size_t)maxn * 3 * 8, c.stream));
+  if (c.n_lm_l > 0) {
+    poba::k_lm_scatter<<<poba::grid_for(c.n_lm_l * 3, 256), 256, 0, c.stream>>>(c.points.as<double>(), c.lm_perm.as<int>(),
+                                                                    c.n_lm_l, 3, d_mine.as<double>());
+    c.launches++;
+    PCK(cudaGetLastError());
+  }
+  PTRY(poba::allgather(c, d_mine.as<double>(), d_rows.as<double>(), (size_t)maxn * 3));
+  std::vector<double> rows((size_t)R * maxn * 3);
+  PTRY(poba::copy_sync(c, rows.data(), d_rows.p, rows.size() * 8, cudaMemcpyDeviceToHost));
+  for (int r = 0; r < R; ++r) {
+    const int64_t lo = (int64_t)all[2 * r], n = (int64_t)all[2 * r + 1];
+    std::memcpy(points + lo * 3, rows.data() + (size_t)r * maxn * 3, (size_t)n * 3 * 8);
+  }
+  return POBA_OK;
+}
+
 int poba_accept_points(poba_ctx* ctx) {
   CTX_CHECK(ctx);
   Ctx& c = ctx->c;

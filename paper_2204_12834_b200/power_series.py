@@ -83,7 +83,9 @@ def power_series_solve(system, epsilon: float = 0.01, max_order: int = 20,
         if max_order >= 1:
             raise ValueError("epsilon must be positive")
         eps = 1.0
-    dp, order, conv, ratios = sys_._dp.dev.series_solve(eps, max_order, want_ratios=return_ratios)
+    with sys_._dp.lock:
+        sys_._activate()
+        dp, order, conv, ratios = sys_._dp.dev.series_solve(eps, max_order, want_ratios=return_ratios)
     c = sys_.counters
     if sys_._b_tilde is None:
         c.w += 1
@@ -102,7 +104,9 @@ def apply_series_inverse(system, v: np.ndarray, order: int) -> np.ndarray:
     if order < 0:
         raise ValueError("order must be non-negative")
     sys_ = _device_system(system)
-    out = sys_._dp.dev.series_apply(np.asarray(v, dtype=np.float64), order)
+    with sys_._dp.lock:
+        sys_._activate()
+        out = sys_._dp.dev.series_apply(np.asarray(v, dtype=np.float64), order)
     sys_.counters.u_inv += order + 1
     sys_.counters.w += order
     sys_.counters.wt += order
@@ -113,7 +117,9 @@ def apply_series_inverse(system, v: np.ndarray, order: int) -> np.ndarray:
 def back_substitute(system, delta_p: np.ndarray) -> np.ndarray:
     """dx_l = -V^-1 (b_l + W^T dx_p) (power_series.py:94-100)."""
     sys_ = _device_system(system)
-    dl, _ = sys_._dp.dev.back_substitute(np.asarray(delta_p, dtype=np.float64))
+    with sys_._dp.lock:
+        sys_._activate()
+        dl, _ = sys_._dp.dev.back_substitute(np.asarray(delta_p, dtype=np.float64))
     sys_.counters.wt += 1
     sys_.counters.v_inv += 1
     return dl

@@ -62,17 +62,27 @@ class _DevicePreconditioner:
 def schur_diagonal_blocks(system) -> np.ndarray:
     """The 9x9 diagonal blocks of S: U_c - sum_l W_cl V_l^-1 W_cl^T (solvers.py:71-85)."""
     sys_ = _device_system(system)
-    return sys_._dp.dev.schur_diagonal()
+    with sys_._dp.lock:
+        sys_._activate()
+        return sys_._dp.dev.schur_diagonal()
 
 
 def make_schur_jacobi_preconditioner(system):
     """Block-Jacobi preconditioner from the true diagonal of S (solvers.py:88-95)."""
     sys_ = _device_system(system)
-    sys_._dp.dev.schur_diagonal()  # raises ValueError if a block is not SPD, as the reference
+    with sys_._dp.lock:
+        sys_._activate()
+        sys_._dp.dev.schur_diagonal()  # raises ValueError if a block is not SPD, as the reference
     return _DevicePreconditioner(sys_, _lib.PRECOND_SCHUR_JACOBI)
 
 
 def _pcg_device(sys_, pre: _DevicePreconditioner, tol, max_iter, callback):
+    with sys_._dp.lock:
+        sys_._activate()
+        return _pcg_device_locked(sys_, pre, tol, max_iter, callback)
+
+
+def _pcg_device_locked(sys_, pre, tol, max_iter, callback):
     dev = sys_._dp.dev
     if callback is None:
         dp, it, rel, conv, _ = dev.pcg(pre.kind, pre.order, tol, max_iter)

@@ -1,0 +1,181 @@
+"""Parity at the benchmark configurations' FULL size (C3, C4, C5).
+
+The golden fixtures pin the path on small problems; the perf claims rest on
+C4 (10.3M observations) and C5 (29.1M, the bench workload).  These cases run
+the CUDA path through the C-ABI on the full configurations and compare with
+the oracle on identical seeded inputs:
+
+  * canonical ordering and k-groups bit-exact against ``np.lexsort((cam, pt,
+    k[pt]))`` (reference blocks.py:362-372, 405-417) at C3, C4 and C5;
+  * C4: the linearization (U0, V0, b_p, b_l, D) and the damped inverses
+    (blocks.py:375-402, 164-192), one W V^-1 W^T pass;
+  * one teacher-forced LM iteration at each config's own series settings --
+    linearize, damp (lambda = 1e-4), power_series_solve at the config's m and
+    epsilon with its LIVE stop test (power_series.py:53-77), back-substitution
+    (power_series.py:94-100), the trial state and its cost (lm.py:107-144):
+    increments <= 1e-9 relative, cost <= 1e-8 relative, identical order_used
+    and converged flag.
+
+The oracle is poba_oracle's numpy restatement (linearization, inverses, U^-1,
+V^-1, cost) with the W / W^T passes in its C restatement (oracle/poba_term.c,
+pinned to the reference goldens by test_oracle_golden.py) so a C5 series takes
+seconds instead of minutes.  Set POBA_PARITY_OUT=<file.json> to record the
+measured errors.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+INC_TOL = 1e-9    # north star: increments within 1e-9 relative
+COST_TOL = 1e-8   # north star: per-LM-iteration cost within 1e-8 relative
+
+_PROBLEMS = {}
+_ORACLE_LIN = {}
+_RECORD = {}
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    d = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (d if d else 1.0))
+
+
+def problem(name):
+    from paper_2204_12834_b200 import configs
+    key = "c3" if name == "c3m64" else name
+    if key not in _PROBLEMS:
+        _PROBLEMS[key] = configs.make_config(key, 1.0, seed=0)
+    return _PROBLEMS[key]
+
+
+def oracle_linearization(name):
+    """The oracle's linearization at the initial state (cached: C5's store is 6 GB)."""
+    from oracle import poba_oracle as O
+    key = "c3" if name == "c3m64" else name
+    if key not in _ORACLE_LIN:
+        _ORACLE_LIN.clear()
+        p = problem(key)
+        _ORACLE_LIN[key] = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points)
+    return _ORACLE_LIN[key]
+
+
+def record(name, **kv):
+    _RECORD.setdefault(name, {}).update(kv)
+    out = os.environ.get("POBA_PARITY_OUT")
+    if out:
+        with open(out, "w") as fh:
+            json.dump(_RECORD, fh, indent=1, sort_keys=True)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from oracle import poba_oracle as O
+    if O.term_library() is None:
+        pytest.skip("oracle/lib/libpoba_oracle.so not built (make oracle)")
+    import paper_2204_12834_b200 as pkg
+    return pkg
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_canonical_order_full_size(P, name):
+    from oracle import poba_oracle as O
+    p = problem(name)
+    k = np.bincount(p.pt_indices, minlength=p.n_points)
+    want = np.lexsort((p.cam_indices, p.pt_indices, k[p.pt_indices]))
+    dp = P.blocks.device_problem(p)
+    order, cs, ps = dp.ordering()
+    assert np.array_equal(order, want)
+    assert np.array_equal(cs, p.cam_indices[want]) and np.array_equal(ps, p.pt_indices[want])
+    gk, gstart, gn = dp.groups()
+    og = O.k_groups(cs, ps, p.n_points)
+    assert gk.tolist() == [g.k for g in og]
+    assert gstart.tolist() == [g.start for g in og]
+    assert gn.tolist() == [g.n for g in og]
+    record(name, n_obs=int(p.n_observations), ordering="bit-exact", n_groups=len(og), max_k=int(k.max()))
+
+
+def test_c4_linearization_and_operator_full_size(P):
+    from oracle import poba_oracle as O
+    from paper_2204_12834_b200 import _lib
+    p = problem("c4")
+    lam = 1e-4
+    lin_o = oracle_linearization("c4")
+    lin = P.linearize(p)
+    errs = {key: rel(getattr(lin, key), getattr(lin_o, key)) for key in ("U0", "V0", "b_p", "b_l", "D_p", "D_l")}
+    for key, e in errs.items():
+        assert e <= 1e-11, (key, e)
+    assert lin.n_invalid == lin_o.n_invalid
+    s_o = O.ScaleOracleSystem(lin_o, lam)
+    s = lin.damp(lam)
+    e_vinv = rel(s.V_inv, s_o.V_inv)
+    assert e_vinv <= 1e-9
+    # U^-1 per 9x9 block (entries inherit kappa(U)); and as an operator on vectors
+    du = np.linalg.norm(s.U_inv - s_o.U_inv, axis=(1, 2)) / np.linalg.norm(s_o.U_inv, axis=(1, 2))
+    assert du.max() <= 1e-6, du.max()
+    v = np.random.default_rng(11).standard_normal(9 * p.n_cameras)
+    e_uinv = rel(s.apply_u_inv(v), s_o.apply_u_inv(v))
+    assert e_uinv <= INC_TOL
+    assert rel(s.b_tilde(), s_o.b_tilde()) <= INC_TOL
+    s._activate()
+    got = s._dp.dev.apply(_lib.OP_WVW, v)
+    want = s_o.apply_w(s_o.apply_v_inv(s_o.apply_wt(v)))
+    e_wvw = rel(got, want)
+    assert e_wvw <= 1e-12
+    record("c4", **{f"rel_{k}": v_ for k, v_ in errs.items()}, rel_V_inv=e_vinv, max_block_rel_U_inv=float(du.max()),
+           rel_U_inv_apply=e_uinv, rel_WVWt_pass=e_wvw)
+
+
+@pytest.mark.parametrize("name", ["c3", "c3m64", "c4", "c5"])
+def test_teacher_forced_lm_iteration_full_size(P, name):
+    """linearize -> damp -> series at the config's (m, epsilon) with the live stop
+    test -> back-substitution -> trial state -> cost, against the oracle."""
+    from oracle import poba_oracle as O
+    from paper_2204_12834_b200 import configs
+    p = problem(name)
+    st = configs.LM_SETTINGS[name]
+    lam, eps, m = st.initial_lambda, st.epsilon, st.max_order
+    t0 = time.perf_counter()
+    lin_o = oracle_linearization(name)
+    s_o = O.ScaleOracleSystem(lin_o, lam)
+    ratios_o = []
+    x_o, order_o, conv_o = O.series_solve(s_o, eps, m, ratios_o)
+    dl_o = O.back_sub(s_o, x_o)
+    cams_t, pts_t = O.retract(p.camera_params, p.points, x_o, dl_o)
+    cost0_o, bad0_o = O.cost(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points)
+    cost_o, bad_o = O.cost(p.cam_indices, p.pt_indices, p.pixels, cams_t, pts_t)
+    t_oracle = time.perf_counter() - t0
+
+    state0 = P.BaState.from_problem(p)
+    cost0, bad0 = P.residual_cost(p, state0)
+    s = P.assemble(p, state0, lam=lam)
+    r, ratios = P.power_series_solve(s, eps, m, return_ratios=True)
+    dl = P.back_substitute(s, r.delta_p)
+    trial = P.apply_update(state0, r.delta_p, dl)
+    cost, bad = P.residual_cost(p, trial)
+    # teacher-forced cost: the GPU cost kernel at the oracle's trial state
+    cost_tf, _ = P.residual_cost(p, P.BaState(cams_t, pts_t))
+
+    assert r.order_used == order_o and r.converged == conv_o, (r.order_used, order_o, r.converged, conv_o)
+    e_p, e_l = rel(r.delta_p, x_o), rel(dl, dl_o)
+    assert e_p <= INC_TOL and e_l <= INC_TOL, (e_p, e_l)
+    e_c0 = abs(cost0 - cost0_o) / cost0_o
+    e_c = abs(cost - cost_o) / cost_o
+    e_tf = abs(cost_tf - cost_o) / cost_o
+    assert e_c0 <= COST_TOL and e_c <= COST_TOL and e_tf <= COST_TOL, (e_c0, e_c, e_tf)
+    assert (bad0, bad) == (bad0_o, bad_o)
+    assert (cost < cost0) == (cost_o < cost0_o)  # the LM accept decision (lm.py:207) agrees
+    e_ratio = max(abs(a - b) / b for a, b in zip(ratios[1:1 + len(ratios_o)], ratios_o))  # ratios[i]: order i
+    record(name, m=m, epsilon=eps, order_used=int(r.order_used), converged=bool(r.converged),
+           rel_delta_p=e_p, rel_delta_l=e_l, rel_cost0=e_c0, rel_trial_cost=e_c, rel_trial_cost_teacher_forced=e_tf,
+           max_rel_stop_ratio=float(e_ratio), cost0=cost0, trial_cost=cost, accepted=bool(cost < cost0),
+           oracle_s=t_oracle)

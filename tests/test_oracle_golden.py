@@ -303,3 +303,48 @@ def test_post_clustering_matches_reference(tag):
                 dp, order, conv = O.solve_clustered(lin, lam, a, n, eps, m)
                 assert [order, conv] == z[q + "order_conv"].tolist()
                 assert rel(dp, z[q + "delta_p"]) < 1e-10
+
+
+# ---- the C restatement of W / W^T used for configuration-scale parity -------------------
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("threads", [1, 3])
+def test_scale_oracle_matches_reference(name, threads):
+    """oracle/poba_term.c (ScaleOracleSystem) reproduces the reference's golden
+    b_tilde, series increments and back-substitutions, and the numpy oracle's
+    W / W^T passes to a few ulps, for any thread count."""
+    if O.term_library() is None:
+        pytest.skip("oracle/lib/libpoba_oracle.so not built (make oracle)")
+    p, z = golden_problem(name)
+    lin = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points)
+    j = 0
+    while f"lam{j}" in z:
+        s = O.ScaleOracleSystem(lin, float(z[f"lam{j}"]), threads=threads)
+        ref = O.OracleSystem(lin, float(z[f"lam{j}"]))
+        rng = np.random.default_rng(j)
+        vp, vl = rng.standard_normal(9 * p.n_cameras), rng.standard_normal(3 * p.n_points)
+        assert rel(s.apply_wt(vp), ref.apply_wt(vp)) < 1e-14
+        assert rel(s.apply_w(vl), ref.apply_w(vl)) < 1e-14
+        assert rel(s.b_tilde(), z[f"sys{j}_b_tilde"]) < 1e-12
+        i = 0
+        while f"sys{j}_solve{i}_eps" in z:
+            pre = f"sys{j}_solve{i}_"
+            dp, order, conv = O.series_solve(s, float(z[pre + "eps"]), int(z[pre + "m"]))
+            assert order == int(z[pre + "order"]) and conv == bool(z[pre + "converged"])
+            assert rel(dp, z[pre + "delta_p"]) < 1e-11
+            assert rel(O.back_sub(s, dp), z[pre + "delta_l"]) < 1e-11
+            i += 1
+        j += 1
+
+
+def test_scale_oracle_at_medium_size():
+    """C3 x 0.2 (~175k observations, hundreds of landmark runs per thread):
+    C passes vs the numpy restatement."""
+    if O.term_library() is None:
+        pytest.skip("oracle/lib/libpoba_oracle.so not built (make oracle)")
+    from paper_2204_12834_b200 import configs
+    p = configs.make_config("c3", 0.2, seed=0)
+    lin = O.linearize(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points)
+    s, ref = O.ScaleOracleSystem(lin, 1e-4, threads=4), O.OracleSystem(lin, 1e-4)
+    vp = np.random.default_rng(3).standard_normal(9 * p.n_cameras)
+    assert rel(s.apply_w(s.apply_v_inv(s.apply_wt(vp))), ref.apply_w(ref.apply_v_inv(ref.apply_wt(vp)))) < 1e-13
