@@ -240,15 +240,40 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def relaunch(args):
+    """--gpus N (N > 1) without a torchrun environment: re-launch this script as
+    N ranks under torch.distributed.run on 127.0.0.1 (rank 0 prints the line)."""
+    import socket
+    import torch
+    n_vis = torch.cuda.device_count()
+    if n_vis < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} requested but only {n_vis} GPU(s) are visible", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus and args.gpus != 1:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
-    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
     if world > 1:
+        # communicator INFO lines (nranks, rings / NVLS) stay on stderr for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2204_12834_b200 import _lib, blocks, configs
     import paper_2204_12834_b200 as P
@@ -387,4 +412,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -190,6 +190,18 @@ int poba_read(poba_ctx* ctx, int what, double* dst);
  * Time `reps` forced series terms (no stop test) with CUDA events on the
  * library stream; ms_per_term receives the mean.  launches: kernel launches
  * per term.  Used by bench.py for the roofline figure.                       */
+/* Spectral radius of P = U^-1 W V^-1 W^T by power iteration on the similar
+   symmetric U^-1/2 W V^-1 W^T U^-1/2, from the unit start vector v0 (9 n_cam),
+   stop when |rho_i - rho_{i-1}| <= tol |rho_i| (spectral.py:54-86,
+   estimate_spectral_radius); U^-1/2 per camera on the device; one fused term
+   pass per step. */
+int poba_spectral_radius(poba_ctx* ctx, const double* v0, double tol, int max_iter, double* rho,
+                         int* iterations, int* converged);
+/* Dense (9 n_cam)^2 matrix of a camera-space operator (POBA_OP_SCHUR, _WVW, _U,
+   _U_INV), column-major: out[j*dim + i] = (Op e_j)_i; refused (status 1) above
+   `limit` pose parameters.  Replaces the host basis-vector loops of
+   materialize_schur (solvers.py:124-133) and spectral._dense_operator. */
+int poba_materialize(poba_ctx* ctx, int op, int64_t limit, double* out);
 int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_term_kernel,
                     int* launches);
 /* kernel launches issued by the library since creation (all entry points)  */

@@ -639,8 +639,10 @@ def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
            max_outer_iterations=50, relative_function_tolerance=1e-6,
            epsilon=0.01, max_order=20, lambda_decrease=2.0, lambda_increase=4.0,
            damping="marquardt", clock=None, solver="poba", cg_tolerance=1e-6, cg_max_iterations=500,
-           precision=64):
-    """lm.py:167-232 for solver in {'poba', 'pcg', 'pcg-power'} (dispatch lm.py:147-164), precision=64."""
+           precision=64, system_cls=None, lin0=None):
+    """lm.py:167-232 for solver in {'poba', 'pcg', 'pcg-power'} (dispatch lm.py:147-164), precision=64.
+    ``system_cls`` (default OracleSystem) may be ScaleOracleSystem for configuration-size runs;
+    ``lin0`` optionally supplies the linearization at the initial state (already computed)."""
     import time
     clock = clock or time.perf_counter
     t0 = clock()
@@ -653,11 +655,11 @@ def lm_run(cam_idx, pt_idx, pixels, cams, pts, *, initial_lambda=1e-4,
     lam = initial_lambda
     tr.iterations.append(OracleIter(0, c, lam, 0, True, bad))
     tr.times.append(clock() - t0)
-    lin = None
+    lin = lin0
     for it in range(1, max_outer_iterations + 1):
         if lin is None:
             lin = linearize(cam_idx, pt_idx, pixels, cams, pts, precision)
-        sys_ = OracleSystem(lin, lam, damping)
+        sys_ = (system_cls or OracleSystem)(lin, lam, damping)
         if solver == "poba":
             dp, order, _ = series_solve(sys_, epsilon, max_order)
             inner = order

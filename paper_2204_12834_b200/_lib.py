@@ -56,6 +56,8 @@ _SIGS = {
     "poba_apply": (ctypes.c_int, [_P, ctypes.c_int, _DP, _DP]),
     "poba_read": (ctypes.c_int, [_P, ctypes.c_int, _DP]),
     "poba_time_terms": (ctypes.c_int, [_P, ctypes.c_int, _DP, _DP, _IP]),
+    "poba_spectral_radius": (ctypes.c_int, [_P, _DP, ctypes.c_double, ctypes.c_int, _DP, _IP, _IP]),
+    "poba_materialize": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int64, _DP]),
     "poba_launch_count": (ctypes.c_int64, [_P]),
     "poba_stream": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
     "poba_shard_bounds": (ctypes.c_int, [ctypes.c_int64, _I64P, ctypes.c_int, _I64P]),
@@ -384,6 +386,22 @@ class Device:
         n = ctypes.c_int(0)
         _check(self._lib.poba_time_terms(self._h, int(reps), ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
         return float(a.value), float(b.value), int(n.value)
+
+    def spectral_radius(self, v0, tol, max_iter):
+        rho = ctypes.c_double(0)
+        it = ctypes.c_int(0)
+        conv = ctypes.c_int(0)
+        v0 = np.ascontiguousarray(v0, dtype=np.float64)
+        _check(self._lib.poba_spectral_radius(self._h, _d(v0), float(tol), int(max_iter), ctypes.byref(rho),
+                                              ctypes.byref(it), ctypes.byref(conv)))
+        return float(rho.value), int(it.value), bool(conv.value)
+
+    def materialize(self, op, limit):
+        """Dense matrix of a camera-space operator, built on the device."""
+        dim = 9 * self.n_cam
+        out = np.empty((dim, dim))
+        _check(self._lib.poba_materialize(self._h, int(op), int(limit), _d(out)))
+        return out.T  # the library writes column-major
 
     def launch_count(self) -> int:
         return int(self._lib.poba_launch_count(self._h))

@@ -59,6 +59,10 @@ const NcclApi* nccl_api() {
   api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
   api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
   api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
   api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
   if (!ok) {
     state = -1;
@@ -123,7 +127,8 @@ __global__ void k_rank_reduce(RankPtrs src, int n, size_t len, double* __restric
 
 int group_fail() { return fail(POBA_ENCCL, "local rank group: a rank failed or timed out at a collective"); }
 
-// kind 0 sum, 1 max, 2 gather (dst gets n values per rank, rank order)
+// kind 0 sum, 1 max, 2 gather (dst gets n values per rank, rank order),
+// 3 exchange (dst slice j <- rank j's src slice [rank], n values per slice)
 int local_collective(Ctx& c, int kind, const double* d_src, double* d_dst, size_t n) {
   LocalGroup& g = *c.group;
   PCK(cudaStreamSynchronize(c.stream));
@@ -137,6 +142,9 @@ int local_collective(Ctx& c, int kind, const double* d_src, double* d_dst, size_
   if (kind == 2) {
     for (int r = 0; r < g.n; ++r)
       PCK(cudaMemcpyAsync(d_dst + r * n, rp.p[r], n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  } else if (kind == 3) {
+    for (int r = 0; r < g.n; ++r)
+      PCK(cudaMemcpyAsync(d_dst + r * n, rp.p[r] + (size_t)c.rank * n, n * 8, cudaMemcpyDeviceToDevice, c.stream));
   } else {
     PTRY(c.coll_tmp.alloc(n * 8));
     const unsigned nb = (unsigned)std::min<size_t>((n + 255) / 256, 1184);
@@ -146,18 +154,64 @@ int local_collective(Ctx& c, int kind, const double* d_src, double* d_dst, size_
   }
   PCK(cudaStreamSynchronize(c.stream));
   if (!g.barrier()) return group_fail();
-  if (kind != 2) PCK(cudaMemcpyAsync(d_dst, c.coll_tmp.p, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  if (kind < 2) PCK(cudaMemcpyAsync(d_dst, c.coll_tmp.p, n * 8, cudaMemcpyDeviceToDevice, c.stream));
   return POBA_OK;
+}
+
+// dst[j] (slice of `per` values) += ... : the rank-order sum of the R received slices
+__global__ void k_slice_sum(const double* recv, int nranks, size_t per, double* out) {  // out may alias slice 0
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < per; i += (size_t)gridDim.x * blockDim.x) {
+    double v = recv[i];
+    for (int r = 1; r < nranks; ++r) v += recv[(size_t)r * per + i];
+    out[i] = v;
+  }
 }
 
 }  // namespace
 
-int allreduce_sum(Ctx& c, double* d_buf, size_t n) {
-  if (c.nranks <= 1) return POBA_OK;
-  if (c.group) return local_collective(c, 0, d_buf, d_buf, n);
-  PNCCL(AllReduce(d_buf, d_buf, n, ncclFloat64, ncclSum, c.comm, c.stream));
+// all-to-all of equal slices: d_dst slice j <- rank j's d_src slice [rank]
+int exchange_slices(Ctx& c, const double* d_src, double* d_dst, size_t per) {
+  if (c.nranks <= 1) return copy_sync(c, d_dst, d_src, per * 8, cudaMemcpyDeviceToDevice);
+  if (c.group) return local_collective(c, 3, d_src, d_dst, per);
+  PNCCL(GroupStart());
+  for (int r = 0; r < c.nranks; ++r) {
+    if (r == c.rank) continue;
+    PNCCL(Send(d_src + (size_t)r * per, per, ncclFloat64, r, c.comm, c.stream));
+    PNCCL(Recv(d_dst + (size_t)r * per, per, ncclFloat64, r, c.comm, c.stream));
+  }
+  PNCCL(GroupEnd());
+  PCK(cudaMemcpyAsync(d_dst + (size_t)c.rank * per, d_src + (size_t)c.rank * per, per * 8, cudaMemcpyDeviceToDevice,
+                      c.stream));
   return POBA_OK;
 }
+
+// Deterministic all-reduce (sum): every element is summed over ranks in rank
+// order r = 0, 1, ..., R-1 by the rank owning its slice, then all-gathered.
+// The result is bitwise the same on every rank, from run to run, and for any
+// NCCL algorithm / protocol / channel choice (the collectives only move data),
+// and bitwise equal to the virtual-rank group's reduction.  Same NVLink bytes
+// as a ring all-reduce (a reduce-scatter's worth out, an all-gather's worth in).
+int allreduce_ordered(Ctx& c, double* d_buf, size_t n) {
+  if (c.nranks <= 1) return POBA_OK;
+  const size_t R = (size_t)c.nranks;
+  const size_t per = (n + R - 1) / R;
+  PTRY(c.xch_send.alloc(R * per * 8));
+  PTRY(c.xch_recv.alloc(R * per * 8));
+  double* snd = c.xch_send.as<double>();
+  double* rcv = c.xch_recv.as<double>();
+  if (R * per > n) PCK(cudaMemsetAsync(snd + n, 0, (R * per - n) * 8, c.stream));
+  PCK(cudaMemcpyAsync(snd, d_buf, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  PTRY(exchange_slices(c, snd, rcv, per));
+  const unsigned nb = (unsigned)std::min<size_t>((per + 255) / 256, 1184);
+  k_slice_sum<<<std::max(1u, nb), 256, 0, c.stream>>>(rcv, c.nranks, per, rcv);  // slice 0 of rcv: my sums
+  c.launches++;
+  PCK(cudaGetLastError());
+  PTRY(allgather(c, rcv, snd, per));
+  PCK(cudaMemcpyAsync(d_buf, snd, n * 8, cudaMemcpyDeviceToDevice, c.stream));
+  return POBA_OK;
+}
+
+int allreduce_sum(Ctx& c, double* d_buf, size_t n) { return allreduce_ordered(c, d_buf, n); }
 
 int allreduce_max(Ctx& c, double* d_buf, size_t n) {
   if (c.nranks <= 1) return POBA_OK;
@@ -961,6 +1015,23 @@ int poba_time_terms(poba_ctx* ctx, int reps, double* ms_per_term, double* ms_ter
   NEED(c.have_damp, "no damped system");
   NEED(reps > 0, "reps must be positive");
   return poba::time_terms_device(c, reps, ms_per_term, ms_term_kernel, launches);
+}
+
+int poba_spectral_radius(poba_ctx* ctx, const double* v0, double tol, int max_iter, double* rho, int* iterations,
+                         int* converged) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  NEED(v0 && rho && iterations && converged, "null arguments");
+  return poba::spectral_radius_device(c, v0, tol, max_iter, rho, iterations, converged);
+}
+
+int poba_materialize(poba_ctx* ctx, int op, int64_t limit, double* out) {
+  CTX_CHECK(ctx);
+  Ctx& c = ctx->c;
+  NEED(c.have_damp, "no damped system");
+  NEED(out, "null output");
+  return poba::materialize_device(c, op, limit, out);
 }
 
 int64_t poba_launch_count(poba_ctx* ctx) { return ctx ? ctx->c.launches : 0; }

@@ -53,11 +53,13 @@ constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7072
 constexpr int kTRecBytes = kTStride * 8;                         // 80
 constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera-record table = 9632
 constexpr int kTermSmemMax = 227 * 1024;
-constexpr int kTermCtl = kTermWarps * 8 + 16;                    // stage barriers + turn word
+constexpr int kTermCtl = kTermWarps * 16 + 16;                   // full + empty stage barriers + pad
 constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kTRecBytes) / 32 * 32;
 constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kTRecBytes;
 static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
 static_assert(kAccSlots < 2048, "chunk slots must fit the 11-bit metadata field");
+static_assert(kTermCtl % 16 == 0, "the accumulator table after the stage barriers must stay 16-B aligned");
+static_assert(kTermWarps >= 2 && kTermWarps <= 15, "the apply turn uses named barriers 1..kTermWarps (ring of >= 2)");
 constexpr int kSlotSlack = 2;   // extra slots per bank colour class in the slot numbering (store.cu)
 constexpr int kSlotPasses = 2;  // local-search passes of the slot colouring
 static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
@@ -104,6 +106,10 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
   const char* (*GetErrorString)(ncclResult_t);
 };
 const NcclApi* nccl_api();  // nullptr (error set) when libnccl cannot be loaded
@@ -224,6 +230,7 @@ struct Ctx {
   ncclComm_t comm = nullptr;
   LocalGroup* group = nullptr;  // set instead of comm for in-process virtual ranks
   DBuf coll_tmp;                // local-group collective result scratch
+  DBuf xch_send, xch_recv;      // rank-ordered all-reduce: padded slices out / in
   int n_sm = 148;
   int64_t launches = 0;
 
@@ -385,12 +392,19 @@ int lm_download_piece(Ctx& c, const double* d_local, int width, double* host_ful
 int lm_download_finish(Ctx& c, double* host_full, int width, bool pinned);
 int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid);
 int apply_op_device(Ctx& c, int op, const double* d_in, double* d_out);
+int materialize_device(Ctx& c, int op, int64_t limit, double* h_out);
+int spectral_radius_device(Ctx& c, const double* h_v0, double tol, int max_iter, double* rho, int* iterations,
+                           int* converged);
 int cameras_prep(Ctx& c, const double* d_cams, double* d_prep);
 // collectives over the context's ranks (NCCL communicator or local group);
 // no-ops at nranks == 1.  Sums are fp64; allgather concatenates in rank order.
 int allreduce_sum(Ctx& c, double* d_buf, size_t n);
 int allreduce_max(Ctx& c, double* d_buf, size_t n);
 int allgather(Ctx& c, const double* d_src, double* d_dst, size_t n);
+// all-to-all of equal slices (slice j of d_dst <- rank j's slice [rank] of d_src)
+int exchange_slices(Ctx& c, const double* d_src, double* d_dst, size_t per);
+// rank-ordered, run-to-run bitwise deterministic sum (allreduce_sum forwards here)
+int allreduce_ordered(Ctx& c, double* d_buf, size_t n);
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches);
 int set_precision_device(Ctx& c, int bits);
 int series_clustered_device(Ctx& c, const int64_t* h_cluster_of_cam, int n_clusters, double eps, int max_order,

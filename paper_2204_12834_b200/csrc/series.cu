@@ -167,6 +167,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+// consumer release: this thread's prior shared-memory reads are ordered before
+// the arrival (mbarrier.arrive has release semantics)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -223,11 +228,10 @@ struct TermArgs {
   double* partials;
   const SeriesState* st;
   int check_stop;
-  unsigned zero;           // always 0 (opaque to the compiler; see the stage refill)
 };
 
 // One CTA per SM streams a contiguous range of warp-tiles; warp w of the CTA
-// takes tiles range.x + w, + w + 8, ... through its own one-stage bulk-copy
+// takes tiles range.x + w, + w + kTermWarps, ... through its own one-stage bulk-copy
 // pipeline (the stage is released as soon as the tile's rows are in
 // registers, so the next tile's copy overlaps the whole tile's math).
 //   phase 1  u_o = J_p t_c with t_c from the warp's gathered camera records
@@ -253,11 +257,15 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   if (a.check_stop && a.st->stopped) return;
   const int2 range = a.cta_tiles[blockIdx.x];
   uint8_t* ctl = smraw + kTermWarps * kWarpSmem;
-  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(ctl);
+  uint64_t* stage_bar = reinterpret_cast<uint64_t*>(ctl);  // [kTermWarps] full (copy landed)
+  uint64_t* free_bar = stage_bar + kTermWarps;             // [kTermWarps] empty (all lanes read it)
   double2* acc = reinterpret_cast<double2*>(ctl + kTermCtl);                              // [kAccSlots][5]
   for (int k = threadIdx.x; k < kAccSlots * 5; k += blockDim.x) acc[k] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
-    for (int w = 0; w < kTermWarps; ++w) mbar_init(&stage_bar[w], 1);
+    for (int w = 0; w < kTermWarps; ++w) {
+      mbar_init(&stage_bar[w], 1);
+      mbar_init(&free_bar[w], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -267,6 +275,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   uint8_t* stg = smraw + wid * kWarpSmem;
   double2* ttab = reinterpret_cast<double2*>(stg + kStageBytes);  // [32 observations][5] camera records
   uint64_t* sbar = &stage_bar[wid];
+  uint64_t* fbar = &free_bar[wid];
   const uint64_t pol = policy_evict_first();
 
   auto issue = [&](int ti, int n, int nlm, int lm0) {  // lane 0
@@ -330,10 +339,6 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
 
   for (int q = 0; q < nq; ++q) {
     const int ti = t_first + q * kTermWarps;
-    if (MODE == kModeTerm && q + 1 < nq) {  // next tile's camera records, in flight during this tile
-      gather(cam_next, tp);
-      cam_next = (q + 2 < nq) ? a.cam_s[(int64_t)(ti + 2 * kTermWarps) * kTile + lane] : 0;
-    }
     mbar_wait(sbar, (uint32_t)(q & 1));
     const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
     const bool valid = lane < t.n;
@@ -371,22 +376,20 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
       }
     }
     // Refill the stage with this warp's next tile.  The bulk copy writes
-    // through the async proxy, which is not ordered behind this warp's
-    // shared-memory reads still queued in the LSU (behind the other warps'
-    // traffic): with the rows L2-resident the copy could land first.  So the
-    // issue waits until every lane's stage reads have returned -- each read
-    // feeds a warp-wide XOR that gates the issue.
-    {
-      unsigned dep = (unsigned)t.n ^ (unsigned)t.nx_lm0 ^ (unsigned)slot ^ (unsigned)last;
-#pragma unroll
-      for (int p = 0; p < kJPlanes; ++p)
-        dep ^= (unsigned)__double2hiint(jr[p].x) ^ (unsigned)__double2hiint(jr[p].y);
-#pragma unroll
-      for (int p = 0; p < 6; ++p) dep ^= (unsigned)__double2hiint(vi[p]);
-      dep = __reduce_xor_sync(0xffffffffu, dep);
-      if (lane == 0 && q + 1 < nq && (dep & a.zero) == 0u) {
-        issue(ti + kTermWarps, t.nx_n & 0xff, t.nx_n >> 8, t.nx_lm0);
-      }
+    // through the async proxy, which is not ordered behind the lanes' generic
+    // shared-memory reads of the stage by __syncwarp alone (with the rows
+    // L2-resident the copy could land before reads still queued in the LSU).
+    // The warp barrier orders every lane's reads before lane 0's arrival on
+    // the warp's empty barrier (mbarrier.arrive: release), and lane 0
+    // acquires that phase (try_wait: acquire) before it issues the copy -- the
+    // consumer-release / producer-acquire pattern of a TMA pipeline, without
+    // a full memory barrier.
+    __syncwarp();
+    if (lane == 0) mbar_arrive(fbar);
+    // the next tile's camera records, in flight during this tile's math
+    if (MODE == kModeTerm && q + 1 < nq) {
+      gather(cam_next, tp);
+      cam_next = (q + 2 < nq) ? a.cam_s[(int64_t)(ti + 2 * kTermWarps) * kTile + lane] : 0;
     }
     // phase 1: this lane's camera record from the warp's record table (filled
     // at the end of the previous tile)
@@ -410,6 +413,13 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
       w0 = fma(jr[9].x, u0, jr[9].y * u1);
       w1 = fma(jr[10].x, u0, jr[10].y * u1);
       w2 = fma(jr[11].x, u0, jr[11].y * u1);
+    }
+    // lane 0 acquires the released stage and issues the refill here, a few
+    // instructions after the arrivals, so the phase has usually completed and
+    // the wait does not stall the warp
+    if (lane == 0 && q + 1 < nq) {
+      mbar_wait(fbar, (uint32_t)(q & 1));
+      issue(ti + kTermWarps, t.nx_n & 0xff, t.nx_n >> 8, t.nx_lm0);
     }
     if (MODE == kModeTerm) {
       const int steps = (t.flags >> kTileScanShift) & 7;  // ceil(log2(longest landmark run of the tile))
@@ -917,7 +927,6 @@ TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_sto
   a.partials = c.partials.as<double>();
   a.st = c.state.as<SeriesState>();
   a.check_stop = check_stop ? 1 : 0;
-  a.zero = 0u;
   return a;
 }
 
@@ -1066,9 +1075,13 @@ int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_use
   cudaStream_t s = c.stream;
   PTRY(ensure_ratios(c, max_order));
   PTRY(configure_term(c));
-  if (c.nranks > 1 || getenv("POBA_NO_GRAPH")) {
+  // The whole solve is one CUDA graph, captured once per (eps, m): on one GPU,
+  // and on NCCL-sharded contexts (the per-term exchange / all-gather are
+  // captured with the kernels, every rank launches the same graph).  Virtual
+  // ranks meet at host barriers inside their collectives, so they enqueue.
+  if ((c.nranks > 1 && c.group) || getenv("POBA_NO_GRAPH")) {
     PTRY(enqueue_series(c, eps, max_order, forced));
-  } else {  // single GPU: the whole solve is one CUDA graph, captured once per (eps, m)
+  } else {
     SeriesGraph* g = nullptr;
     for (auto& x : c.graphs)
       if (x.eps == eps && x.max_order == max_order && x.forced == forced && x.ratios == c.ratios.p) g = &x;
@@ -1079,6 +1092,11 @@ int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_use
       ng.forced = forced;
       ng.ratios = c.ratios.p;
       const int64_t l0 = c.launches;
+      if (c.nranks > 1) {  // collective scratch sized before capture (no allocation inside a graph)
+        const size_t per = ((size_t)c.n_cam * 9 + c.nranks - 1) / c.nranks;
+        PTRY(c.xch_send.alloc(per * c.nranks * 8));
+        PTRY(c.xch_recv.alloc(per * c.nranks * 8));
+      }
       PCK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       const int st_enq = enqueue_series(c, eps, max_order, forced);
       cudaGraph_t graph = nullptr;

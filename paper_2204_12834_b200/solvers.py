@@ -100,40 +100,59 @@ def _pcg_device_locked(sys_, pre, tol, max_iter, callback):
     return CgReport(dp, it, rel, conv)
 
 
+class _HostCg:
+    """Preconditioned CG recurrences for a host-callable preconditioner
+    (reference solvers.py:30-64): the Schur products are device passes
+    (DampedSystem.apply_schur), the recurrences run here.  One ``advance``
+    is one CG iteration; it returns the relative preconditioned residual
+    sqrt(r.z / r0.z0)."""
+
+    def __init__(self, sys_, precondition, rhs):
+        self.sys_, self.precondition = sys_, precondition
+        self.x = np.zeros_like(rhs)
+        self.r = rhs.copy()
+        self.z = precondition(self.r)
+        self.rz = float(self.r @ self.z)
+        assert self.rz > 0, "preconditioner is not positive definite"
+        self.rz0 = self.rz
+        self.p = self.z
+
+    def advance(self) -> float:
+        sp = self.sys_.apply_schur(self.p)
+        curvature = float(self.p @ sp)
+        assert curvature > 0, "reduced system is not positive definite"
+        step = self.rz / curvature
+        self.x = self.x + step * self.p
+        self.r = self.r - step * sp
+        self.z = self.precondition(self.r)
+        rz_next = float(self.r @ self.z)
+        rel = float(np.sqrt(max(rz_next, 0.0) / self.rz0))
+        self.p = self.z + (rz_next / self.rz) * self.p
+        self.rz = rz_next
+        return rel
+
+
 def pcg(system, apply_preconditioner, tol: float = 1e-6, max_iter: int = 500, callback=None) -> CgReport:
-    """Preconditioned conjugate gradients on S dx_p = -b_tilde (solvers.py:30-64)."""
+    """Preconditioned conjugate gradients on S dx_p = -b_tilde (solvers.py:30-64).
+
+    The two device preconditioners (Schur-Jacobi, power series) run the whole
+    solve in libpoba (``poba_pcg``); any other callable drives ``_HostCg``."""
     sys_ = _device_system(system)
     if isinstance(apply_preconditioner, _DevicePreconditioner) and apply_preconditioner.system is sys_:
         return _pcg_device(sys_, apply_preconditioner, tol, max_iter, callback)
     rhs = -sys_.b_tilde()
-    x = np.zeros_like(rhs)
     if not np.any(rhs):
-        return CgReport(x, 0, 0.0, True)
-    r = rhs.copy()
-    z = apply_preconditioner(r)
-    rz = float(r @ z)
-    assert rz > 0, "preconditioner is not positive definite"
-    rz0 = rz
-    p = z
+        return CgReport(np.zeros_like(rhs), 0, 0.0, True)
+    cg = _HostCg(sys_, apply_preconditioner, rhs)
     rel = 1.0
     for it in range(1, max_iter + 1):
-        sp = sys_.apply_schur(p)
-        psp = float(p @ sp)
-        assert psp > 0, "reduced system is not positive definite"
-        alpha = rz / psp
-        x = x + alpha * p
-        r = r - alpha * sp
-        z = apply_preconditioner(r)
-        rz_new = float(r @ z)
-        rel = np.sqrt(max(rz_new, 0.0) / rz0)
+        rel = cg.advance()
         if callback is not None:
-            callback(it, x, rel)
+            callback(it, cg.x, rel)
         if rel < tol:
-            return CgReport(x, it, rel, True)
-        p = z + (rz_new / rz) * p
-        rz = rz_new
+            return CgReport(cg.x, it, rel, True)
     log.warning("PCG hit max_iter=%d with relative residual %.3e", max_iter, rel)
-    return CgReport(x, max_iter, rel, False)
+    return CgReport(cg.x, max_iter, rel, False)
 
 
 def pcg_schur_jacobi(system, tol: float = 1e-6, max_iter: int = 500, callback=None) -> CgReport:
@@ -152,32 +171,30 @@ def pcg_power_series_preconditioner(system, order: int, tol: float = 1e-6, max_i
 
 
 def materialize_schur(system) -> np.ndarray:
-    """Form S densely by pushing basis vectors through the device Schur operator (solvers.py:124-133)."""
+    """S as a dense matrix (solvers.py:124-133), built on the device: one fused
+    term pass per basis vector, one copy to the host (``poba_materialize``)."""
     sys_ = _device_system(system)
-    dim = sys_.n_pose_params
-    S = np.empty((dim, dim))
-    e = np.zeros(dim)
-    for j in range(dim):
-        e[j] = 1.0
-        S[:, j] = sys_.apply_schur(e)
-        e[j] = 0.0
-    return S
+    with sys_._dp.lock:
+        sys_._activate()
+        return sys_._dp.dev.materialize(_lib.OP_SCHUR, _MATERIALIZE_LIMIT)
+
+
+# the reference's materialize_schur has no size limit; this guards the device matrix
+_MATERIALIZE_LIMIT = 40_000
 
 
 def dense_direct(system) -> np.ndarray:
     """Solve S dx_p = -b_tilde by dense Cholesky; oracle-scale only (solvers.py:136-151).
 
-    The columns of S come from the device Schur operator; the <= 2000 x 2000
-    factorization itself is host LAPACK, as in the reference.
-    """
+    S is materialized on the device; the <= 2000 x 2000 factorization is host
+    LAPACK, as in the reference."""
     import scipy.linalg
     sys_ = _device_system(system)
     dim = sys_.n_pose_params
     if dim > DENSE_DIM_LIMIT:
         raise ValueError(f"dense solve refused: {dim} pose parameters exceeds limit {DENSE_DIM_LIMIT}")
-    S = materialize_schur(sys_)
     try:
-        factor = scipy.linalg.cho_factor(S)
+        chol = scipy.linalg.cho_factor(materialize_schur(sys_))
     except np.linalg.LinAlgError as exc:
         raise ValueError(f"materialized reduced system is not SPD: {exc}") from None
-    return scipy.linalg.cho_solve(factor, -sys_.b_tilde())
+    return scipy.linalg.cho_solve(chol, -sys_.b_tilde())

@@ -13,8 +13,19 @@ the oracle on identical seeded inputs:
     linearize, damp (lambda = 1e-4), power_series_solve at the config's m and
     epsilon with its LIVE stop test (power_series.py:53-77), back-substitution
     (power_series.py:94-100), the trial state and its cost (lm.py:107-144):
-    increments <= 1e-9 relative, cost <= 1e-8 relative, identical order_used
-    and converged flag.
+    increments <= 1e-9 relative, identical order_used and converged flag, the
+    GPU cost of the oracle's trial state <= 1e-8 relative and the same accept
+    decision;
+  * the LM trace itself (lm.py:167-232) for the first iterations of every
+    config (rejects, lambda schedule, accepts, relinearizations): per-LM-
+    iteration cost <= 1e-8 relative, identical accept / lambda / order.
+
+A REJECTED trial step's cost never enters the trace, and at lambda = 1e-4 the
+first steps of C3/C4 are wild (trial cost ~1e6 x the current one, points
+thrown to near-zero depth), where a 4e-12 difference in the increments moves
+the trial cost by ~1e-8: that value is recorded, and asserted only for
+accepted steps; the cost kernel itself is held to 1e-8 at the same state
+(teacher-forced).
 
 The oracle is poba_oracle's numpy restatement (linearization, inverses, U^-1,
 V^-1, cost) with the W / W^T passes in its C restatement (oracle/poba_term.c,
@@ -121,7 +132,7 @@ def test_c4_linearization_and_operator_full_size(P):
     assert e_vinv <= 1e-9
     # U^-1 per 9x9 block (entries inherit kappa(U)); and as an operator on vectors
     du = np.linalg.norm(s.U_inv - s_o.U_inv, axis=(1, 2)) / np.linalg.norm(s_o.U_inv, axis=(1, 2))
-    assert du.max() <= 1e-6, du.max()
+    assert du.max() <= 1e-9, du.max()
     v = np.random.default_rng(11).standard_normal(9 * p.n_cameras)
     e_uinv = rel(s.apply_u_inv(v), s_o.apply_u_inv(v))
     assert e_uinv <= INC_TOL
@@ -171,11 +182,49 @@ def test_teacher_forced_lm_iteration_full_size(P, name):
     e_c0 = abs(cost0 - cost0_o) / cost0_o
     e_c = abs(cost - cost_o) / cost_o
     e_tf = abs(cost_tf - cost_o) / cost_o
-    assert e_c0 <= COST_TOL and e_c <= COST_TOL and e_tf <= COST_TOL, (e_c0, e_c, e_tf)
+    assert e_c0 <= COST_TOL and e_tf <= COST_TOL, (e_c0, e_tf)
     assert (bad0, bad) == (bad0_o, bad_o)
     assert (cost < cost0) == (cost_o < cost0_o)  # the LM accept decision (lm.py:207) agrees
+    if cost_o < cost0_o:  # an accepted step's cost is the next trace entry
+        assert e_c <= COST_TOL, e_c
     e_ratio = max(abs(a - b) / b for a, b in zip(ratios[1:1 + len(ratios_o)], ratios_o))  # ratios[i]: order i
     record(name, m=m, epsilon=eps, order_used=int(r.order_used), converged=bool(r.converged),
            rel_delta_p=e_p, rel_delta_l=e_l, rel_cost0=e_c0, rel_trial_cost=e_c, rel_trial_cost_teacher_forced=e_tf,
            max_rel_stop_ratio=float(e_ratio), cost0=cost0, trial_cost=cost, accepted=bool(cost < cost0),
            oracle_s=t_oracle)
+
+
+# iterations compared per config: enough to cover the initial rejects, the
+# lambda schedule and at least two accepted steps with relinearization
+LM_ITERS = {"c3": 12, "c3m64": 8, "c4": 5, "c5": 5}
+
+
+@pytest.mark.parametrize("name", ["c3", "c3m64", "c4", "c5"])
+def test_lm_trace_full_size(P, name):
+    """lm.run on the GPU vs the oracle's LM loop (the reference algorithm,
+    lm.py:167-232) on the full configuration: per-iteration cost <= 1e-8."""
+    from oracle import poba_oracle as O
+    from paper_2204_12834_b200 import configs
+    p = problem(name)
+    st = configs.LM_SETTINGS[name]
+    n_it = LM_ITERS[name]
+    kw = dict(initial_lambda=st.initial_lambda, max_outer_iterations=n_it, epsilon=st.epsilon,
+              max_order=st.max_order)
+    t0 = time.perf_counter()
+    tr_o, _, _ = O.lm_run(p.cam_indices, p.pt_indices, p.pixels, p.camera_params, p.points,
+                          system_cls=O.ScaleOracleSystem, lin0=oracle_linearization(name), **kw)
+    t_oracle = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    tr = P.run(p, P.LmConfig(**kw))
+    t_gpu = time.perf_counter() - t0
+    want = np.array([i.cost for i in tr_o.iterations])
+    got = np.array([i.cost for i in tr.iterations])
+    assert len(got) == len(want)
+    err = np.abs(got - want) / want
+    assert err.max() <= COST_TOL, err
+    assert [i.accepted for i in tr.iterations] == [i.accepted for i in tr_o.iterations]
+    assert [i.lam for i in tr.iterations] == [i.lam for i in tr_o.iterations]
+    assert [i.order_m for i in tr.iterations] == [i.order_m for i in tr_o.iterations]
+    record(name, lm_iterations=n_it, lm_max_rel_cost=float(err.max()),
+           lm_accepted=[bool(i.accepted) for i in tr.iterations], lm_costs=got.tolist(),
+           lm_orders=[int(i.order_m) for i in tr.iterations], lm_oracle_s=t_oracle, lm_gpu_s=t_gpu)
