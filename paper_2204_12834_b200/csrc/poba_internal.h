@@ -4,9 +4,20 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cassert>
 #include <cstdint>
 #include <string>
 #include <vector>
+
+// Device-side bounds checks (index < bound on every gathered / scattered
+// table): compiled in with -DPOBA_DEVICE_CHECKS for the checked build the GPU
+// tests run against (tools/build_variant.sh checked -DPOBA_DEVICE_CHECKS);
+// compute-sanitizer is not available on the GPU pool.
+#ifdef POBA_DEVICE_CHECKS
+#define POBA_DCHECK(cond) assert(cond)
+#else
+#define POBA_DCHECK(cond) ((void)0)
+#endif
 
 #include "../../include/poba.h"
 
@@ -62,6 +73,7 @@ static_assert(kTermCtl % 16 == 0, "the accumulator table after the stage barrier
 static_assert(kTermWarps >= 2 && kTermWarps <= 15, "the apply turn uses named barriers 1..kTermWarps (ring of >= 2)");
 constexpr int kSlotSlack = 2;   // extra slots per bank colour class in the slot numbering (store.cu)
 constexpr int kSlotPasses = 2;  // local-search passes of the slot colouring
+constexpr int kLaneRounds = 2;  // rounds of within-run lane ordering + re-colouring (store.cu)
 static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 
 // PoBA-32 (blocks.py:42-47): block storage may be fp32 (planes of float2);

@@ -228,6 +228,7 @@ struct TermArgs {
   double* partials;
   const SeriesState* st;
   int check_stop;
+  int n_cam, n_partials, n_lm;  // bounds for the checked build (POBA_DEVICE_CHECKS)
 };
 
 // One CTA per SM streams a contiguous range of warp-tiles; warp w of the CTA
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     for (int r = 0; r < 5; ++r) {
       const int k = 32 * r + lane;
       const int cam = __shfl_sync(0xffffffffu, cam_lane, k / 5);
+      POBA_DCHECK(cam >= 0 && cam < a.n_cam);
       tp[r] = reinterpret_cast<const double2*>(a.tin + (int64_t)cam * kTStride)[k % 5];
     }
   };
@@ -314,6 +316,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
   int h_slot = 0, h_ti = -1, h_flags = 0, h_part0 = 0, h_nslot = 0;
   bool h_apply = false;
   auto rmw = [&](int sl, const double* v) {
+    POBA_DCHECK(sl >= 0 && sl < kAccSlots);
     double2* r = acc + sl * 5;
     const double2 o0 = r[0], o1 = r[1], o2 = r[2], o3 = r[3], o4 = r[4];
     r[0] = make_double2(o0.x + v[0], o0.y + v[1]);
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
     if (h_apply) rmw(h_slot, hg);
     __syncwarp();
     if (h_flags & kTileChunkLast) {  // write the chunk's partials, clear the table
+      POBA_DCHECK(h_part0 >= 0 && h_nslot <= kAccSlots && h_part0 + h_nslot <= a.n_partials);
       double2* out = reinterpret_cast<double2*>(a.partials) + (int64_t)h_part0 * 5;
       for (int k = lane; k < h_nslot * 5; k += 32) {
         out[k] = acc[k];
@@ -348,6 +352,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
       const uint32_t mv = reinterpret_cast<const uint32_t*>(stg)[lane];
       slot = meta_slot(mv);
       li = meta_li(mv);
+      POBA_DCHECK(slot < t.nslot && li < kTileLm && t.lm0 + li < a.n_lm);
       first = meta_first(mv);
       last = meta_last(mv);
     }
@@ -539,6 +544,7 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
     if (kFromPartials) {
       const int p0 = a.part_cam_off[cam], p1 = a.part_cam_off[cam + 1];
       for (int p = p0 + lane; p < p1; p += 32) {  // 80-B partial records: five 16-B loads
+        POBA_DCHECK(a.part_idx[p] >= 0);
         const double2* src = reinterpret_cast<const double2*>(a.partials + (int64_t)a.part_idx[p] * kTStride);
         double v[10];
 #pragma unroll
@@ -927,6 +933,9 @@ TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_sto
   a.partials = c.partials.as<double>();
   a.st = c.state.as<SeriesState>();
   a.check_stop = check_stop ? 1 : 0;
+  a.n_cam = (int)c.n_cam;
+  a.n_partials = c.n_partials;
+  a.n_lm = (int)c.n_lm_l;
   return a;
 }
 

@@ -114,6 +114,18 @@ __global__ void k_fill_slots(const uint64_t* __restrict__ key, const int* __rest
   lidx_s[s] = lm_tidx[l];
 }
 
+// slot arrays after the within-run lane reordering: new slot s <- old slot perm[s]
+__global__ void k_permute_slots(const int* __restrict__ perm, int64_t ns, const int* __restrict__ cam_in,
+                                const int* __restrict__ file_in, const double2* __restrict__ pix_in,
+                                int* __restrict__ cam_out, int* __restrict__ file_out, double2* __restrict__ pix_out) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= ns) return;
+  const int64_t o = perm[q];
+  cam_out[q] = cam_in[o];
+  file_out[q] = file_in[o];
+  pix_out[q] = pix_in[o];
+}
+
 __global__ void k_fill_i32(int* __restrict__ a, int64_t n, int v) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) a[i] = v;
@@ -532,6 +544,64 @@ std::vector<int> color_chunk_slots(const std::vector<Tile>& tiles, const Chunk& 
   return cams;
 }
 
+// Drop the holes of a chunk's slot numbering (cameras -1) so that a second
+// colouring round starts from dense slots and stays within kAccSlots.
+std::vector<int> compact_chunk_slots(const std::vector<Tile>& tiles, const Chunk& q, std::vector<int>& obs_slot,
+                                     const std::vector<int>& part_cam) {
+  std::vector<int> remap(q.nslot, -1), cams;
+  for (int sl = 0; sl < q.nslot; ++sl)
+    if (part_cam[q.part0 + sl] >= 0) {
+      remap[sl] = (int)cams.size();
+      cams.push_back(part_cam[q.part0 + sl]);
+    }
+  for (int ti = q.tile0; ti < q.tile1; ++ti) {
+    const int64_t s0 = (int64_t)ti * kTile;
+    for (int i = 0; i < tiles[ti].n; ++i) obs_slot[s0 + i] = remap[obs_slot[s0 + i]];
+  }
+  return cams;
+}
+
+// Within-run lane order of one tile.  The accumulator apply of the term kernel
+// accesses 16-B pieces of 80-B slot records: the 8 lanes of a quarter-warp are
+// served by one shared-memory wavefront only if their slots differ mod 8 (the
+// slot colouring's "colour").  Landmark runs must stay contiguous (segmented
+// scan), but a run's observations may take any order: each position of a run,
+// in lane order, takes the remaining observation whose colour is least used by
+// the camera leaders already placed in that position's quarter (a camera
+// already placed at a lower lane is pre-summed, not applied: free anywhere).
+// Writes perm[new lane] = old lane.
+void order_tile_lanes(const Tile& t, const int* slot, const uint8_t* lidx, int* perm) {
+  int cnt[4][8] = {};
+  int used = 0;  // bitmask of old lanes already placed
+  int placed_slots[kTile];
+  int n_placed = 0;
+  for (int a = 0; a < t.n;) {
+    int b = a + 1;
+    while (b < t.n && lidx[b] == lidx[a]) ++b;
+    for (int pos = a; pos < b; ++pos) {
+      const int qd = pos >> 3;
+      int best = -1, best_cost = 1 << 30;
+      for (int i = a; i < b; ++i) {
+        if (used & (1 << i)) continue;
+        bool dup = false;
+        for (int k = 0; k < n_placed; ++k) dup |= placed_slots[k] == slot[i];
+        const int cost = dup ? -1 : cnt[qd][slot[i] & 7];
+        if (cost < best_cost) {
+          best_cost = cost;
+          best = i;
+        }
+      }
+      used |= 1 << best;
+      perm[pos] = best;
+      if (best_cost >= 0) {
+        cnt[qd][slot[best] & 7]++;
+        placed_slots[n_placed++] = slot[best];
+      }
+    }
+    a = b;
+  }
+}
+
 }  // namespace
 
 int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const double* h_pix) {
@@ -801,6 +871,65 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
         pc.insert(pc.end(), cams.begin(), cams.end());
       }
       part_cam.swap(pc);
+      // rounds of within-run lane ordering (host permutation of the tile's
+      // slots, applied to the device slot arrays) and re-colouring
+      const char* lr = getenv("POBA_LANE_ROUNDS");  // A/B: 0 disables
+      const int rounds = lr ? std::max(0, atoi(lr)) : kLaneRounds;
+      if (rounds > 0) {
+        std::vector<uint8_t> hl(ns);
+        PTRY(poba::copy_sync(c, hl.data(), c.lidx_s.p, ns, cudaMemcpyDeviceToHost));
+        std::vector<int> perm(ns), tmp_slot(ns), tmp_cam(ns);
+        std::vector<int> total(ns);
+        for (int64_t q = 0; q < ns; ++q) total[q] = (int)q;  // composed new -> original slot
+        for (int round = 0; round < rounds; ++round) {
+          for (int64_t q = 0; q < ns; ++q) perm[q] = (int)q;
+          for (int ti = 0; ti < c.n_tiles; ++ti) {
+            if (tiles[ti].flags & kTileLong) continue;
+            const int64_t s0 = (int64_t)ti * kTile;
+            int lp[kTile];
+            order_tile_lanes(tiles[ti], &obs_slot[s0], &hl[s0], lp);
+            for (int i = 0; i < tiles[ti].n; ++i) perm[s0 + i] = (int)(s0 + lp[i]);
+          }
+          for (int64_t q = 0; q < ns; ++q) {
+            tmp_slot[q] = obs_slot[perm[q]];
+            tmp_cam[q] = hcam[perm[q]];
+          }
+          obs_slot.swap(tmp_slot);
+          hcam.swap(tmp_cam);
+          for (int64_t q = 0; q < ns; ++q) tmp_slot[q] = total[perm[q]];
+          total.swap(tmp_slot);
+          std::vector<int> pc2;
+          pc2.reserve(part_cam.size());
+          for (Chunk& q : chunks) {
+            std::vector<int> dense = compact_chunk_slots(tiles, q, obs_slot, part_cam);
+            // colour the dense numbering: color_chunk_slots reads the chunk's
+            // cameras from part_cam[part0, part0 + nslot)
+            Chunk qd = q;
+            qd.part0 = 0;
+            qd.nslot = (int)dense.size();
+            std::vector<int> cams = color_chunk_slots(tiles, qd, obs_slot, dense, group, passes);
+            q.part0 = (int)pc2.size();
+            q.nslot = (int)cams.size();
+            pc2.insert(pc2.end(), cams.begin(), cams.end());
+          }
+          part_cam.swap(pc2);
+        }
+        DBuf dperm, c2, f2, p2;
+        PTRY(dperm.alloc(ns * 4));
+        PTRY(c2.alloc(ns * 4));
+        PTRY(f2.alloc(ns * 4));
+        PTRY(p2.alloc(ns * 16));
+        PCK(cudaMemcpyAsync(dperm.p, total.data(), ns * 4, cudaMemcpyHostToDevice, s));
+        k_permute_slots<<<grid_for(ns, B), B, 0, s>>>(dperm.as<int>(), ns, c.cam_s.as<int>(), c.file_s.as<int>(),
+                                                     c.pix_s.as<double2>(), c2.as<int>(), f2.as<int>(),
+                                                     p2.as<double2>());
+        c.launches++;
+        PCK(cudaGetLastError());
+        PCK(cudaMemcpyAsync(c.cam_s.p, c2.p, ns * 4, cudaMemcpyDeviceToDevice, s));
+        PCK(cudaMemcpyAsync(c.file_s.p, f2.p, ns * 4, cudaMemcpyDeviceToDevice, s));
+        PCK(cudaMemcpyAsync(c.pix_s.p, p2.p, ns * 16, cudaMemcpyDeviceToDevice, s));
+        PCK(cudaStreamSynchronize(s));
+      }
     }
     if (getenv("POBA_SLOT_STATS")) {  // bank-conflict model: sum over quarters of the largest residue class
       int64_t wf = 0, ideal = 0;
