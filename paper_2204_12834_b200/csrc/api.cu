@@ -594,7 +594,7 @@ int poba_problem_info(poba_ctx* ctx, int64_t* info) {
   size_t bytes = 0;
   for (const DBuf* b : {&c.cam_file, &c.pt_file, &c.kpt, &c.order, &c.tiles, &c.tilek, &c.chunks, &c.cta_tiles,
                         &c.cam_s, &c.file_s, &c.pix_s, &c.lidx_s, &c.lm_slot0, &c.lm_k,
-                        &c.part_cam_off, &c.part_idx, &c.long_lm, &c.cperm, &c.cam_start, &c.cc_cam_off, &c.cc_cam, &c.cpos, &c.cmaj, &c.J,
+                        &c.part_cam_off, &c.part_idx, &c.long_lm, &c.cperm, &c.cam_start, &c.cc_cam_off, &c.cc_cam, &c.lm_c, &c.pix_c, &c.file_c, &c.J,
                         &c.Rz, &c.cams, &c.cams_prep, &c.cams_trial, &c.trial_prep, &c.U0, &c.bp, &c.Dp, &c.Uinv,
                         &c.Ud, &c.bt, &c.tvec, &c.xvec, &c.rvec, &c.cc_part, &c.partials, &c.points, &c.V0, &c.bl,
                         &c.Dl, &c.Vinv, &c.Vd, &c.dl, &c.ltmp, &c.ctmp, &c.ctmp2})

@@ -20,7 +20,7 @@ namespace {
 #ifndef POBA_LIN_COOP_PREP
 #define POBA_LIN_COOP_PREP 1
 #endif
-constexpr int kLinRec = 11;  // double2 per staged camera-major record (10 used)
+constexpr int kLinRec = 9;  // double2 per staged camera record (8 used; 144-B stride)
 constexpr int kLinRecSmem = kBlockTiles * kTile * kLinRec * 16;
 
 
@@ -160,11 +160,10 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
            const double* __restrict__ prep, const double* __restrict__ points, const double* __restrict__ ejp,
            const double* __restrict__ ejl, const double* __restrict__ eres, void* __restrict__ J,
            double2* __restrict__ Rz, double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
-           const int* __restrict__ cpos, double2* __restrict__ cmaj, unsigned long long* __restrict__ n_invalid) {
+           unsigned long long* __restrict__ n_invalid) {
   __shared__ double contrib_all[kBlockTiles][kTile * 9];
   __shared__ int lstart_all[kBlockTiles][kTile + 1];
-  // per warp: the tile's camera-major records (J_p pairs + residual, 176-B
-  // stride so that 16-B accesses of eight consecutive lanes hit distinct banks)
+  // per warp: the tile's 32 camera records, staged for the cooperative gather
   extern __shared__ __align__(16) double2 lin_rec[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = tile0 + blockIdx.x * kBlockTiles + w;
@@ -175,7 +174,6 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   // per-slot loads first, all independent of the tile descriptor (slot arrays
   // cover the padding too), so their latencies overlap
   const int cam_o = cam_s[o];
-  const int cpos_o = cpos[o];
   const int li_o = lidx_s[o];
   const Tile t = tiles[ti];
   const bool is_long = t.flags & kTileLong;
@@ -212,7 +210,6 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
         cp[2 * k + 1] = v.y;
       }
     }
-    __syncwarp();  // the stage is reused for the camera-major records below
 #else
     if (lane < t.n) load_prep(prep, my_cam, cp);
 #endif
@@ -256,12 +253,6 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
     m.r0 = stored<F32>(m.r0);
     m.r1 = stored<F32>(m.r1);
     Rz[o] = make_double2(m.r0, m.r1);
-    {  // this observation's camera-major record, staged for the cooperative write below
-      double2* rec = lin_rec + (w * kTile + lane) * kLinRec;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) rec[j] = make_double2(m.jp0[j], m.jp1[j]);
-      rec[9] = make_double2(m.r0, m.r1);
-    }
     double* cc = contrib + lane * 9;
     cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
     cc[1] = m.jl0[0] * m.jl0[1] + m.jl1[0] * m.jl1[1];
@@ -279,17 +270,6 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   }
   if (lane == 0) lstart[t.nlm] = t.n;
   __syncwarp();
-  {  // camera-major copy of J_p and r for the U0 / b_p pass: each 160-B record
-     // is written by ten lanes as one contiguous run (three records per step)
-    const int my_pos = lane < t.n ? cpos_o : 0;
-    const int sub = lane / 10, piece = lane - sub * 10;
-    const double2* rec = lin_rec + w * kTile * kLinRec;
-    for (int i0 = 0; i0 < t.n; i0 += 3) {
-      const int i = i0 + sub;
-      const int pos = __shfl_sync(0xffffffffu, my_pos, i & 31);
-      if (sub < 3 && i < t.n) cmaj[(int64_t)pos * 10 + piece] = rec[i * kLinRec + piece];
-    }
-  }
   const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
   if (lane == 0 && nbad) atomicAdd(n_invalid, (unsigned long long)nbad);
   __syncwarp();
@@ -343,41 +323,60 @@ __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restric
 }
 
 
-// U0 (packed upper 45) and b_p (9) partial sums over chunks of <= 128 observations
-// of one camera, walked in camera-major order; fixed warp-butterfly reduction.
-// (Variants staging each group of 32 records through shared memory -- with
-// coalesced loads, or double-buffered with cp.async -- were slower; see
-// profiles/r01e_linearize_ab.md.)
+// U0 (packed upper 45) and b_p (9) partial sums over chunks of <= kCamChunk
+// observations of one camera, walked in camera-major order; fixed
+// warp-butterfly reduction.  Each observation's J_p and residual are
+// RECOMPUTED here from the camera record (one per warp), the landmark's point
+// and the pixel -- the same evaluate_obs (and fp32 rounding at precision 32)
+// that produced the stored rows -- instead of being written camera-major by
+// the tile pass and read back (160 B per observation each way).
+template <bool kExplicit, bool F32>
 __global__ void __launch_bounds__(kCamReduceThreads)
 k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cc_cam, const int* __restrict__ cam_start,
-                   const double2* __restrict__ cmaj, int n_cc, double* __restrict__ out) {
+                   int n_cc, const double* __restrict__ prep, const double* __restrict__ points,
+                   const int* __restrict__ lm_c, const double2* __restrict__ pix_c, const int* __restrict__ file_c,
+                   const double* __restrict__ ejp, const double* __restrict__ eres, double* __restrict__ out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_cc) return;
   const int cam = cc_cam[warp];
   const int p0 = cam_start[cam] + (warp - cc_cam_off[cam]) * kCamChunk;
   const int p1 = min(p0 + kCamChunk, cam_start[cam + 1]);
+  double cp[16];
+  if (!kExplicit) load_prep(prep, cam, cp);
   double acc[54];
 #pragma unroll
   for (int q = 0; q < 54; ++q) acc[q] = 0.0;
-  auto fold = [&](const double2* cm) {  // one record: 45 products of J_p, 9 of J_p with r
+  for (int p = p0 + lane; p < p1; p += 32) {
+    ObsModel m;
+    if (kExplicit) {
+      const int64_t f = file_c[p];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        m.jp0[j] = ejp[f * 18 + j];
+        m.jp1[j] = ejp[f * 18 + 9 + j];
+      }
+      m.r0 = eres[f * 2];
+      m.r1 = eres[f * 2 + 1];
+    } else {
+      const int64_t lm = lm_c[p];
+      evaluate_obs<true>(cp, points[lm * 3], points[lm * 3 + 1], points[lm * 3 + 2], __ldcs(pix_c + p), m);
+    }
     double a[9], b[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const double2 v = __ldcs(cm + j);
-      a[j] = v.x;
-      b[j] = v.y;
+      a[j] = stored<F32>(m.jp0[j]);
+      b[j] = stored<F32>(m.jp1[j]);
     }
-    const double2 r = __ldcs(cm + 9);
+    const double r0 = stored<F32>(m.r0), r1 = stored<F32>(m.r1);
     int q = 0;
 #pragma unroll
     for (int i = 0; i < 9; ++i)
 #pragma unroll
       for (int j = i; j < 9; ++j) acc[q++] += a[i] * a[j] + b[i] * b[j];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) acc[45 + i] += a[i] * r.x + b[i] * r.y;
-  };
-  for (int p = p0 + lane; p < p1; p += 32) fold(cmaj + (int64_t)p * 10);
+    for (int i = 0; i < 9; ++i) acc[45 + i] += a[i] * r0 + b[i] * r1;
+  }
 #pragma unroll
   for (int q = 0; q < 54; ++q) {
     double v = acc[q];
@@ -502,7 +501,6 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   }
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 32);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
-  PTRY(c.cmaj.alloc((size_t)std::max<int64_t>(c.n_obs_l, 1) * 160));
   const bool f32 = c.precision == 32;
   auto lin = [&](auto kern, const double* prep, const double* pts, const double* a, const double* b,
                  const double* r, int t0, int t1) {
@@ -511,7 +509,7 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
     kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, kLinRecSmem, s>>>(
         c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
         c.lidx_s.as<uint8_t>(), prep, pts, a, b, r, c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
-        c.Dl.as<double>(), c.cpos.as<int>(), c.cmaj.as<double2>(), d_bad);
+        c.Dl.as<double>(), d_bad);
     c.launches++;
   };
   auto lin_range = [&](int t0, int t1) {
@@ -550,9 +548,19 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   // camera side: U0 / b_p via camera-major chunks, then a fixed-order merge
   if (c.n_cchunks) {
     const unsigned g = grid_for((int64_t)c.n_cchunks * 32, kCamReduceThreads);
-    k_cam_chunk_reduce<<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_cam.as<int>(),
-                                                      c.cam_start.as<int>(), c.cmaj.as<double2>(), c.n_cchunks,
-                                                      c.cc_part.as<double>());
+    auto reduce = [&](auto kern) {
+      kern<<<g, kCamReduceThreads, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_cam.as<int>(), c.cam_start.as<int>(),
+                                           c.n_cchunks, c.cams_prep.as<double>(), c.points.as<double>(),
+                                           c.lm_c.as<int>(), c.pix_c.as<double2>(), c.file_c.as<int>(),
+                                           ejp.as<double>(), eres.as<double>(), c.cc_part.as<double>());
+    };
+    if (expl) {
+      if (f32) reduce(k_cam_chunk_reduce<true, true>);
+      else reduce(k_cam_chunk_reduce<true, false>);
+    } else {
+      if (f32) reduce(k_cam_chunk_reduce<false, true>);
+      else reduce(k_cam_chunk_reduce<false, false>);
+    }
     c.launches++;
   }
   k_cam_merge54<<<grid_for(c.n_cam * 32, 256), 256, 0, s>>>(c.cc_cam_off.as<int>(), c.cc_part.as<double>(),

@@ -297,8 +297,9 @@ struct Ctx {
   // camera-major reduction chunks
   int n_cchunks = 0;
   DBuf cperm;        // int32 [n_obs_l] slots sorted by (camera, slot)
-  DBuf cpos;         // int32 [n_slots] position of each slot in cperm
-  DBuf cmaj;         // double2 [n_obs_l][10] J_p column pairs + residual, camera-major (U0 / b_p pass)
+  DBuf lm_c;         // int32 [n_obs_l] store landmark of each camera-major position (U0 / b_p pass)
+  DBuf pix_c;        // double2 [n_obs_l] its pixel
+  DBuf file_c;       // int32 [n_obs_l] its file index (explicit-Jacobian systems)
   DBuf cam_start;    // int32 [n_cam+1] camera -> first position in cperm
   DBuf cc_cam_off;   // int32 [n_cam+1] camera -> cchunk range
   DBuf cc_cam;       // int32 [n_cchunks] cchunk -> camera

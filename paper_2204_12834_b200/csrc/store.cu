@@ -162,10 +162,21 @@ __global__ void k_low32(const uint64_t* __restrict__ key, int64_t n, int* __rest
   if (i < n) out[i] = (int)(key[i] & 0xffffffffu);
 }
 
-__global__ void k_inverse_perm(const int* __restrict__ perm, int64_t n, int* __restrict__ inv) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) inv[perm[i]] = (int)i;
+// the U0 / b_p pass walks observations camera-major and recomputes each one's
+// J_p and residual: its landmark (store index), pixel and file index, in that order
+__global__ void k_cam_major_gather(const int* __restrict__ cperm, int64_t n, const Tile* __restrict__ tiles,
+                                   const uint8_t* __restrict__ lidx_s, const double2* __restrict__ pix_s,
+                                   const int* __restrict__ file_s, int* __restrict__ lm_c, double2* __restrict__ pix_c,
+                                   int* __restrict__ file_c) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int slot = cperm[p];
+  const Tile t = tiles[slot >> 5];
+  lm_c[p] = t.lm0 + ((t.flags & kTileLong) ? 0 : lidx_s[slot]);
+  if (pix_c) pix_c[p] = pix_s[slot];
+  file_c[p] = file_s[slot];
 }
+
 
 __global__ void k_cam_degree(const uint64_t* __restrict__ key, int64_t n, int* __restrict__ deg) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1012,8 +1023,13 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PTRY(sort_keys(c, ka.as<uint64_t>(), kb.as<uint64_t>(), ns, 64));
     PTRY(c.cperm.alloc(nl * 4));
     k_low32<<<grid_for(nl, B), B, 0, s>>>(kb.as<uint64_t>(), nl, c.cperm.as<int>());
-    PTRY(c.cpos.alloc(ns * 4));
-    k_inverse_perm<<<grid_for(nl, B), B, 0, s>>>(c.cperm.as<int>(), nl, c.cpos.as<int>());
+    PTRY(c.lm_c.alloc(std::max<int64_t>(nl, 1) * 4));
+    PTRY(c.file_c.alloc(std::max<int64_t>(nl, 1) * 4));
+    if (h_pix) PTRY(c.pix_c.alloc(std::max<int64_t>(nl, 1) * 16));
+    k_cam_major_gather<<<grid_for(nl, B), B, 0, s>>>(c.cperm.as<int>(), nl, c.tiles.as<Tile>(),
+                                                    c.lidx_s.as<uint8_t>(), c.pix_s.as<double2>(),
+                                                    c.file_s.as<int>(), c.lm_c.as<int>(),
+                                                    h_pix ? c.pix_c.as<double2>() : nullptr, c.file_c.as<int>());
     c.launches++;
     DBuf deg, ccnt;
     PTRY(deg.alloc((n_cam + 1) * 4));
