@@ -141,7 +141,8 @@ int local_collective(Ctx& c, int kind, const double* d_src, double* d_dst, size_
   for (int r = 0; r < g.n; ++r) rp.p[r] = g.src[r];
   if (kind == 2) {
     for (int r = 0; r < g.n; ++r)
-      PCK(cudaMemcpyAsync(d_dst + r * n, rp.p[r], n * 8, cudaMemcpyDeviceToDevice, c.stream));
+      if (d_dst + r * n != rp.p[r])  // in place: this rank's own slice is already there
+        PCK(cudaMemcpyAsync(d_dst + r * n, rp.p[r], n * 8, cudaMemcpyDeviceToDevice, c.stream));
   } else if (kind == 3) {
     for (int r = 0; r < g.n; ++r)
       PCK(cudaMemcpyAsync(d_dst + r * n, rp.p[r] + (size_t)c.rank * n, n * 8, cudaMemcpyDeviceToDevice, c.stream));
@@ -218,6 +219,14 @@ int allreduce_max(Ctx& c, double* d_buf, size_t n) {
   if (c.group) return local_collective(c, 1, d_buf, d_buf, n);
   PNCCL(AllReduce(d_buf, d_buf, n, ncclFloat64, ncclMax, c.comm, c.stream));
   return POBA_OK;
+}
+
+// sharded contexts: every rank updated only its slice of a per-camera vector
+// (x, b_tilde) -- all-gather the slices (rows of `width` doubles), in place
+int gather_cam_slices(Ctx& c, double* d_vec, int width) {
+  if (c.nranks <= 1) return POBA_OK;
+  const size_t per = (size_t)c.cam_ls * width;
+  return allgather(c, d_vec + (size_t)c.rank * per, d_vec, per);
 }
 
 int allgather(Ctx& c, const double* d_src, double* d_dst, size_t n) {

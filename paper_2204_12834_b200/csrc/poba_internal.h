@@ -243,6 +243,7 @@ struct Ctx {
   LocalGroup* group = nullptr;  // set instead of comm for in-process virtual ranks
   DBuf coll_tmp;                // local-group collective result scratch
   DBuf xch_send, xch_recv;      // rank-ordered all-reduce: padded slices out / in
+  int64_t cam_ls = 0;           // sharded: cameras per rank slice of the camera step (>= 4)
   int n_sm = 148;
   int64_t launches = 0;
 
@@ -418,6 +419,8 @@ int allgather(Ctx& c, const double* d_src, double* d_dst, size_t n);
 int exchange_slices(Ctx& c, const double* d_src, double* d_dst, size_t per);
 // rank-ordered, run-to-run bitwise deterministic sum (allreduce_sum forwards here)
 int allreduce_ordered(Ctx& c, double* d_buf, size_t n);
+// sharded: all-gather a per-camera vector whose rank slices were updated locally
+int gather_cam_slices(Ctx& c, double* d_vec, int width);
 int time_terms_device(Ctx& c, int reps, double* ms_per_term, double* ms_term_kernel, int* launches);
 int set_precision_device(Ctx& c, int bits);
 int series_clustered_device(Ctx& c, const int64_t* h_cluster_of_cam, int n_clusters, double eps, int max_order,

@@ -528,20 +528,82 @@ struct CamArgs {
   int order;
   double eps;
   int check_stop;
+  // sliced camera step (sharded contexts): this rank's cameras [c0, c1), the
+  // R received slices (ls cameras x 9 each) of the ranks' partial sums
+  const double* recv;
+  int nranks, ls, c0, c1;
 };
 
-template <int MODE, bool kFromPartials>
+enum CamSrc { kSrcPartials = 0, kSrcFull = 1, kSrcSlices = 2 };
+
+// stop logic of the series at one order from the reduced norms
+// (power_series.py:29-42, 62-77); one thread
+template <int MODE>
+__device__ void series_stop(const CamArgs& a, double DD, double XX, double NF, double NZ) {
+  SeriesState* st = a.st;
+  if (MODE == kCamBt) {
+    if (NZ == 0.0) {  // zero right-hand side (power_series.py:64-65)
+      st->stopped = 1;
+      st->converged = 1;
+      st->order_used = 0;
+      st->any_nonzero = -1;  // marks the zero-rhs shortcut
+    } else if (NF > 0.0) {
+      st->stopped = 1;
+      st->error = POBA_ENONFINITE;
+      st->error_order = 0;
+    }
+  } else {
+    const int i = a.order;
+    if (NF > 0.0) {
+      st->stopped = 1;
+      st->error = POBA_ENONFINITE;
+      st->error_order = i;
+    } else {
+      st->order_used = i;
+      if (a.check_stop) {
+        if (XX == 0.0) {
+          st->stopped = 1;
+          st->error = POBA_EVANISH;
+          st->error_order = i;
+        } else {
+          const double ratio = (double)(i + 1) * sqrt(DD) / sqrt(XX);
+          if (a.ratios) a.ratios[i] = ratio;
+          if (ratio < a.eps) {
+            st->stopped = 1;
+            st->converged = 1;
+          }
+        }
+      }
+    }
+  }
+}
+
+// One warp per camera: the camera's reduced vector r (from the chunk partials,
+// a full vector, or -- sliced -- the rank-order sum of the R received slices),
+// then b_tilde / t = U^-1 r / x += t and the norms of the stop test.  The
+// norms are reduced in a fixed order (lanes, warps, blocks in the last block);
+// on a slice the last block leaves its four totals in the pad doubles of the
+// slice's first four t records (all-gathered with t), and k_stop finishes.
+template <int MODE, int SRC>
 __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
   __shared__ double red[8][4];
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cam = blockIdx.x * 8 + warp;
+  const int cam = (SRC == kSrcSlices ? a.c0 : 0) + blockIdx.x * 8 + warp;
+  const int cam_end = SRC == kSrcSlices ? a.c1 : a.n_cam;
   if (MODE == kCamTerm && a.st->stopped) return;
   double r[9];
 #pragma unroll
   for (int j = 0; j < 9; ++j) r[j] = 0.0;
-  if (cam < a.n_cam) {
-    if (kFromPartials) {
+  if (cam < cam_end) {
+    if (SRC == kSrcSlices) {  // rank-order sum of the received slices
+      const int64_t off = (int64_t)(cam - a.c0) * 9;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) r[j] = a.recv[off + j];
+      for (int rk = 1; rk < a.nranks; ++rk)
+#pragma unroll
+        for (int j = 0; j < 9; ++j) r[j] += a.recv[(int64_t)rk * a.ls * 9 + off + j];
+    } else if (SRC == kSrcPartials) {
       const int p0 = a.part_cam_off[cam], p1 = a.part_cam_off[cam + 1];
       for (int p = p0 + lane; p < p1; p += 32) {  // 80-B partial records: five 16-B loads
         POBA_DCHECK(a.part_idx[p] >= 0);
@@ -566,7 +628,7 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
     }
   }
   double dd = 0.0, xx = 0.0, nonfinite = 0.0, nonzero = 0.0;
-  if (cam < a.n_cam && lane < 9) {
+  if (cam < cam_end && lane < 9) {
     const int i = lane;
     const int64_t q = (int64_t)cam * 9 + i;
     if (MODE == kCamMerge) {
@@ -645,45 +707,26 @@ __global__ void __launch_bounds__(256) k_cam(const CamArgs a) {
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    SeriesState* st = a.st;
-    st->ticket = 0;
-    const double DD = tot[0][0], XX = tot[0][1], NF = tot[0][2], NZ = tot[0][3];
-    if (MODE == kCamBt) {
-      if (NZ == 0.0) {  // zero right-hand side (power_series.py:64-65)
-        st->stopped = 1;
-        st->converged = 1;
-        st->order_used = 0;
-        st->any_nonzero = -1;  // marks the zero-rhs shortcut
-      } else if (NF > 0.0) {
-        st->stopped = 1;
-        st->error = POBA_ENONFINITE;
-        st->error_order = 0;
-      }
+    a.st->ticket = 0;
+    if (SRC == kSrcSlices) {
+      for (int k = 0; k < 4; ++k) a.tvec[(int64_t)(a.c0 + k) * kTStride + 9] = tot[0][k];
     } else {
-      const int i = a.order;
-      if (NF > 0.0) {
-        st->stopped = 1;
-        st->error = POBA_ENONFINITE;
-        st->error_order = i;
-      } else {
-        st->order_used = i;
-        if (a.check_stop) {
-          if (XX == 0.0) {
-            st->stopped = 1;
-            st->error = POBA_EVANISH;
-            st->error_order = i;
-          } else {
-            const double ratio = (double)(i + 1) * sqrt(DD) / sqrt(XX);
-            if (a.ratios) a.ratios[i] = ratio;
-            if (ratio < a.eps) {
-              st->stopped = 1;
-              st->converged = 1;
-            }
-          }
-        }
-      }
+      series_stop<MODE>(a, tot[0][0], tot[0][1], tot[0][2], tot[0][3]);
     }
   }
+}
+
+// sliced camera step: the ranks' norm totals (pad doubles of each slice's first
+// four t records, all-gathered), summed in rank order -> the stop decision,
+// identical on every rank
+template <int MODE>
+__global__ void k_stop(const CamArgs a) {
+  if (threadIdx.x != 0) return;
+  if (MODE == kCamTerm && a.st->stopped) return;
+  double t4[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int rk = 0; rk < a.nranks; ++rk)
+    for (int k = 0; k < 4; ++k) t4[k] += a.tvec[((int64_t)rk * a.ls + k) * kTStride + 9];
+  series_stop<MODE>(a, t4[0], t4[1], t4[2], t4[3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -958,6 +1001,11 @@ CamArgs cam_args(Ctx& c, int order, double eps, bool check_stop) {
   a.order = order;
   a.eps = eps;
   a.check_stop = check_stop ? 1 : 0;
+  a.recv = nullptr;
+  a.nranks = c.nranks;
+  a.ls = (int)c.cam_ls;
+  a.c0 = 0;
+  a.c1 = (int)c.n_cam;
   return a;
 }
 
@@ -983,25 +1031,48 @@ int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool ch
   return POBA_OK;
 }
 
-// camera step after a term kernel: merge (+ all-reduce when sharded) + finalize
+// camera step after a term kernel.  One GPU: merge the chunk partials and
+// finalize in one kernel.  Sharded: merge this rank's partials, then either
+// (kCamMerge) the rank-ordered all-reduce of the full vector, or (series
+// terms, b_tilde) the SLICED step: exchange slices of the partial vector,
+// each rank finalizes only its cameras [c0, c1) (U^-1, x, norms), all-gather
+// of the t records (with the norm totals in their pad doubles), and k_stop.
+// Same NVLink bytes as an all-reduce; the camera work is 1/R per rank.
 int launch_cam(Ctx& c, int mode, int order, double eps, bool check_stop, const CamArgs* override_args = nullptr) {
   const unsigned nb = grid_for(c.n_cam, 8);
   CamArgs a = override_args ? *override_args : cam_args(c, order, eps, check_stop);
   if (c.nranks == 1) {
-    if (mode == kCamTerm) k_cam<kCamTerm, true><<<nb, 256, 0, c.stream>>>(a);
-    else if (mode == kCamBt) k_cam<kCamBt, true><<<nb, 256, 0, c.stream>>>(a);
-    else k_cam<kCamMerge, true><<<nb, 256, 0, c.stream>>>(a);
+    if (mode == kCamTerm) k_cam<kCamTerm, kSrcPartials><<<nb, 256, 0, c.stream>>>(a);
+    else if (mode == kCamBt) k_cam<kCamBt, kSrcPartials><<<nb, 256, 0, c.stream>>>(a);
+    else k_cam<kCamMerge, kSrcPartials><<<nb, 256, 0, c.stream>>>(a);
     c.launches++;
   } else {
-    k_cam<kCamMerge, true><<<nb, 256, 0, c.stream>>>(a);
+    k_cam<kCamMerge, kSrcPartials><<<nb, 256, 0, c.stream>>>(a);
     c.launches++;
-    PTRY(allreduce_sum(c, c.rvec.as<double>(), c.n_cam * 9));
-    if (mode == kCamTerm) {
-      k_cam<kCamTerm, false><<<nb, 256, 0, c.stream>>>(a);
-      c.launches++;
-    } else if (mode == kCamBt) {
-      k_cam<kCamBt, false><<<nb, 256, 0, c.stream>>>(a);
-      c.launches++;
+    if (mode == kCamMerge) {
+      PTRY(allreduce_sum(c, c.rvec.as<double>(), c.n_cam * 9));
+    } else {
+      const size_t per = (size_t)c.cam_ls * 9;
+      PTRY(c.xch_send.alloc(per * c.nranks * 8));
+      PTRY(c.xch_recv.alloc(per * c.nranks * 8));
+      double* snd = c.xch_send.as<double>();
+      if ((int64_t)per * c.nranks > c.n_cam * 9)
+        PCK(cudaMemsetAsync(snd + c.n_cam * 9, 0, (per * c.nranks - c.n_cam * 9) * 8, c.stream));
+      PCK(cudaMemcpyAsync(snd, c.rvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, c.stream));
+      PTRY(exchange_slices(c, snd, c.xch_recv.as<double>(), per));
+      a.recv = c.xch_recv.as<double>();
+      a.nranks = c.nranks;
+      a.ls = (int)c.cam_ls;
+      a.c0 = (int)std::min<int64_t>(c.n_cam, (int64_t)c.rank * c.cam_ls);
+      a.c1 = (int)std::min<int64_t>(c.n_cam, (int64_t)(c.rank + 1) * c.cam_ls);
+      const unsigned nbs = std::max(1u, grid_for(a.c1 - a.c0, 8));
+      if (mode == kCamTerm) k_cam<kCamTerm, kSrcSlices><<<nbs, 256, 0, c.stream>>>(a);
+      else k_cam<kCamBt, kSrcSlices><<<nbs, 256, 0, c.stream>>>(a);
+      const size_t rec = (size_t)c.cam_ls * kTStride;
+      PTRY(allgather(c, a.tvec + (size_t)c.rank * rec, a.tvec, rec));
+      if (mode == kCamTerm) k_stop<kCamTerm><<<1, 32, 0, c.stream>>>(a);
+      else k_stop<kCamBt><<<1, 32, 0, c.stream>>>(a);
+      c.launches += 2;
     }
   }
   PCK(cudaGetLastError());
@@ -1073,10 +1144,12 @@ int enqueue_series(Ctx& c, double eps, int max_order, bool forced) {
   // order 0: b_tilde and t0
   PTRY(launch_term(c, kModeBt, nullptr, c.bl.as<double>(), false));
   PTRY(launch_cam(c, kCamBt, 0, eps, false));
+  PTRY(gather_cam_slices(c, c.bt.as<double>(), 9));
   for (int i = 1; i <= max_order; ++i) {
     PTRY(launch_term(c, kModeTerm, c.tvec.as<double>(), nullptr, true));
     PTRY(launch_cam(c, kCamTerm, i, eps, !forced));
   }
+  PTRY(gather_cam_slices(c, c.xvec.as<double>(), 9));
   return POBA_OK;
 }
 
@@ -1102,7 +1175,7 @@ int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_use
       ng.ratios = c.ratios.p;
       const int64_t l0 = c.launches;
       if (c.nranks > 1) {  // collective scratch sized before capture (no allocation inside a graph)
-        const size_t per = ((size_t)c.n_cam * 9 + c.nranks - 1) / c.nranks;
+        const size_t per = std::max<size_t>(((size_t)c.n_cam * 9 + c.nranks - 1) / c.nranks, (size_t)c.cam_ls * 9);
         PTRY(c.xch_send.alloc(per * c.nranks * 8));
         PTRY(c.xch_recv.alloc(per * c.nranks * 8));
       }
@@ -1163,6 +1236,7 @@ int b_tilde_device(Ctx& c) {
   a.xvec = c.ctmp2.as<double>();
   a.st = c.state_aux.as<SeriesState>();
   PTRY(launch_cam(c, kCamBt, 0, 1.0, false, &a));
+  PTRY(gather_cam_slices(c, c.bt.as<double>(), 9));
   PCK(cudaStreamSynchronize(s));
   return POBA_OK;
 }
@@ -1190,6 +1264,7 @@ int series_apply_device(Ctx& c, const double* d_v, int order, double* d_out) {
     PTRY(launch_term(c, kModeTerm, c.tvec.as<double>(), nullptr, false));
     PTRY(launch_cam(c, kCamTerm, i, 1.0, false));
   }
+  PTRY(gather_cam_slices(c, c.xvec.as<double>(), 9));
   PCK(cudaMemcpyAsync(d_out, c.xvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, s));
   PCK(cudaStreamSynchronize(s));
   c.have_solution = false;

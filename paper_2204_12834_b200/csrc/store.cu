@@ -1061,9 +1061,14 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PCK(cudaStreamSynchronize(s));  // obs_slot is a local vector
   PTRY(alloc_store(c));
   const int64_t nc = n_cam, nlm1 = std::max<int64_t>(nlm, 1);
-  for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.bt, &c.xvec, &c.rvec})
-    PTRY(b->alloc(nc * 9 * 8));
-  for (DBuf* b : {&c.tvec, &c.ctmp, &c.ctmp2}) PTRY(b->alloc(nc * kTStride * 8));
+  // sharded: the camera step finalizes rank slices of cam_ls cameras (>= 4, the
+  // slice's first four t records carry its norm totals); per-camera vectors
+  // that are all-gathered by slices are padded to nranks * cam_ls rows
+  c.cam_ls = c.nranks > 1 ? std::max<int64_t>(4, (nc + c.nranks - 1) / c.nranks) : nc;
+  const int64_t ncp = c.nranks > 1 ? c.cam_ls * c.nranks : nc;
+  for (DBuf* b : {&c.cams, &c.cams_trial, &c.bp, &c.Dp, &c.rvec}) PTRY(b->alloc(nc * 9 * 8));
+  for (DBuf* b : {&c.bt, &c.xvec}) PTRY(b->alloc(ncp * 9 * 8));
+  for (DBuf* b : {&c.tvec, &c.ctmp, &c.ctmp2}) PTRY(b->alloc(ncp * kTStride * 8));
   for (DBuf* b : {&c.cams_prep, &c.trial_prep}) PTRY(b->alloc(nc * 16 * 8));
   for (DBuf* b : {&c.U0, &c.Uinv, &c.Ud}) PTRY(b->alloc(nc * 45 * 8));
   for (DBuf* b : {&c.points, &c.bl, &c.Dl, &c.dl, &c.ltmp}) PTRY(b->alloc(nlm1 * 3 * 8));
