@@ -44,6 +44,15 @@ for k, r in d["configs"].items():
     out.append(f"| {k} | m={st['max_order']}, ε={st['epsilon']}, ≤{st['max_outer_iterations']} its | "
                + " | ".join(cell(r, c[0]) for c in cols)
                + f" | {r['gpu_lm']['costs'][-1]:.10g} | {ref_final} | {diff} |")
+if any("setup_s" in r for r in d["configs"].values()):
+    out += ["", "## One-time device store build and time to 1% including it", "",
+            "`blocks.device_problem` cold (CUB sorts of the canonical order, host tile packing, upload of indices "
+            "and pixels); the reference sorts inside every `linearize` instead (blocks.py:308-309).", "",
+            "| config | store build s | PoBA GPU incl. build | PoBA-32 GPU incl. build | PoBA reference CPU |", "|---|---|---|---|---|"]
+    for k, r in d["configs"].items():
+        ti = r.get("time_to_1pct_incl_setup_s", {})
+        f = lambda v: "—" if v is None else f"{v:.4g}"
+        out.append(f"| {k} | {r.get('setup_s', float('nan')):.3f} | {f(ti.get('gpu'))} | {f(ti.get('gpu_poba32'))} | {f(ti.get('ref'))} |")
 broken = [k for k, r in d["configs"].items() if any(isinstance(v, dict) and "error" in v for v in r.values())]
 note = ("C4/C5 reference LM runs are estimated at hours (SURVEY §8(d)) and were not run; their f* comes from "
         "the GPU runs. ")

@@ -103,6 +103,12 @@ def main():
                "n_observations": problem.n_observations, "gen_s": gen_s,
                "lm_settings": {"max_outer_iterations": st.max_outer_iterations, "max_order": st.max_order,
                                "epsilon": st.epsilon, "initial_lambda": st.initial_lambda}}
+        # one-time device store build (CUB sorts, host tile packing, index/pixel upload):
+        # cold, before anything else touches the problem; added to the GPU times below
+        from paper_2204_12834_b200 import blocks
+        t = time.perf_counter()
+        blocks.device_problem(problem)
+        rec["setup_s"] = time.perf_counter() - t
         rec["series"] = series_throughput(problem, st.initial_lambda)
         rec["series_poba32"] = series_throughput(problem, st.initial_lambda, precision=32)
         rec["gpu_lm"] = gpu_lm(problem, st)
@@ -129,6 +135,10 @@ def main():
         thr = f0 - 0.99 * (f0 - f_star)
         rec["f0"], rec["f_star"], rec["threshold_1pct"] = f0, f_star, thr
         rec["time_to_1pct_s"] = {k: time_to(v, thr) for k, v in runs.items()}
+        # the reference re-sorts inside every linearize (blocks.py:308-309); the GPU path
+        # builds its store once per problem -- count that build against the GPU runs
+        rec["time_to_1pct_incl_setup_s"] = {k: (None if v is None else v + (rec["setup_s"] if k.startswith("gpu") else 0.0))
+                                            for k, v in rec["time_to_1pct_s"].items()}
         out["configs"][name] = rec
         s = rec["series"]
         print(f"{name}: obs {problem.n_observations} terms/s {s['terms_per_s']:.1f} kernel {s['kernel_gbs']:.0f} GB/s "
