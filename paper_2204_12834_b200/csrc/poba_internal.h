@@ -51,7 +51,14 @@ constexpr int kJPlanes = 12;      // Jacobian column pairs per row
 #ifndef POBA_TERM_WARPS
 #define POBA_TERM_WARPS 12
 #endif
-constexpr int kTermWarps = POBA_TERM_WARPS;  // warps per CTA of the term kernel (one CTA per SM)
+constexpr int kTermWarps = POBA_TERM_WARPS;  // warps per CTA of the term kernel
+#ifndef POBA_TERM_CTAS
+#define POBA_TERM_CTAS 1
+#endif
+// co-resident term-kernel CTAs per SM, each with its own tile range, accumulator table and apply-turn
+// ring.  1 is the measured optimum (profiles/r02a_term_cta_shapes.md: 2 x 6 warps and 3 x 4 warps are
+// 4-9% slower on C5 and double / triple the chunk partials).
+constexpr int kTermCtas = POBA_TERM_CTAS;
 constexpr int kPackWindow = 64;   // landmark lookahead of the tile packer
 constexpr int kTStride = 10;      // doubles per camera record of the term vector / partials (80 B, 16-B aligned)
 // Term-kernel shared memory: per warp one bulk-copy stage (the tile block, the
@@ -63,7 +70,8 @@ constexpr int kStVinv = kStDesc + 32;                            // V^-1 slice
 constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7072
 constexpr int kTRecBytes = kTStride * 8;                         // 80
 constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera-record table = 9632
-constexpr int kTermSmemMax = 227 * 1024;
+// one CTA: the 227-KB per-CTA limit; several: an equal share of the SM's 228 KB less the 1 KB reserved per CTA
+constexpr int kTermSmemMax = kTermCtas == 1 ? 227 * 1024 : (228 * 1024) / kTermCtas - 1024;
 constexpr int kTermCtl = kTermWarps * 16 + 16;                   // full + empty stage barriers + pad
 constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kTRecBytes) / 32 * 32;
 constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kTRecBytes;

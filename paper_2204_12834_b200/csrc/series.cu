@@ -252,7 +252,7 @@ struct TermArgs {
 // After the last tile of a chunk its warp writes the table out once (one 80-B
 // partial per (chunk, camera)) and clears it before passing the turn on.
 template <int MODE, bool F32>
-__global__ void __launch_bounds__(kTermWarps * 32, 1) k_term(const TermArgs a) {
+__global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermArgs a) {
   extern __shared__ __align__(128) uint8_t smraw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (a.check_stop && a.st->stopped) return;
@@ -952,12 +952,14 @@ int configure_term(Ctx& c) {
   int dev = 0;
   PCK(cudaGetDevice(&dev));
   if (done_dev != dev) {
-    PCK(cudaFuncSetAttribute(k_term<kModeTerm, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
-    PCK(cudaFuncSetAttribute(k_term<kModeBt, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
-    PCK(cudaFuncSetAttribute(k_term<kModeW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
-    PCK(cudaFuncSetAttribute(k_term<kModeTerm, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
-    PCK(cudaFuncSetAttribute(k_term<kModeBt, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
-    PCK(cudaFuncSetAttribute(k_term<kModeW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    const void* fns[] = {(const void*)k_term<kModeTerm, false>, (const void*)k_term<kModeBt, false>,
+                         (const void*)k_term<kModeW, false>,    (const void*)k_term<kModeTerm, true>,
+                         (const void*)k_term<kModeBt, true>,    (const void*)k_term<kModeW, true>};
+    for (const void* f : fns) {
+      PCK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+      // all of the SM's unified L1 as shared memory (needed for kTermCtas > 1 to be co-resident)
+      PCK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    }
     done_dev = dev;
   }
   return POBA_OK;

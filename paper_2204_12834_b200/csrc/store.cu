@@ -814,7 +814,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   {
     std::vector<int> hcam(ns);
     PTRY(poba::copy_sync(c, hcam.data(), c.cam_s.p, ns * 4, cudaMemcpyDeviceToHost));
-    const int n_cta = std::max(1, std::min(c.n_sm, (c.n_tiles + kTermWarps - 1) / kTermWarps));
+    const int n_cta = std::max(1, std::min(c.n_sm * kTermCtas, (c.n_tiles + kTermWarps - 1) / kTermWarps));
     std::vector<int64_t> cum(c.n_tiles + 1, 0);
     for (int i = 0; i < c.n_tiles; ++i) cum[i + 1] = cum[i] + tiles[i].n;
     std::vector<int2> cta(n_cta);
