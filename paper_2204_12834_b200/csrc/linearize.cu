@@ -33,6 +33,15 @@ constexpr double kClampHi = 1e6;      // blocks.py:37
 #define POBA_CAM_REDUCE_THREADS 128
 #endif
 constexpr int kCamReduceThreads = POBA_CAM_REDUCE_THREADS;
+// blocks per SM the camera-major reduce is compiled for: 2 keeps all 54
+// accumulators + the prefetched operands in registers (252, no spills); 3 and 4
+// spill and measured slower (profiles/r02a_linearize_ab.md)
+#ifndef POBA_CAM_REDUCE_BLOCKS
+#define POBA_CAM_REDUCE_BLOCKS 2
+#endif
+#ifndef POBA_LIN_TILE_BLOCKS
+#define POBA_LIN_TILE_BLOCKS 2  // 3 (80 registers, spills) measured slower
+#endif
 
 // Rotation matrix of an axis-angle vector through the unit quaternion, the
 // same construction scipy uses (from_rotvec -> as_matrix).
@@ -149,12 +158,35 @@ __device__ __forceinline__ void evaluate_obs(const double* __restrict__ cp, doub
   m.jp0[8] = fs * s * p0; m.jp1[8] = fs * s * p1;
 }
 
+// A tile's 32 camera records (128 B each) gathered cooperatively, four records
+// per 16-B load instruction, through the warp's shared stage (144-B stride:
+// conflict-free 16-B reads by consecutive lanes) -- instead of every lane
+// walking its own record with eight uncoalesced loads.
+__device__ __forceinline__ void gather_prep(const double* __restrict__ prep, int my_cam, int n, int lane,
+                                            double2* __restrict__ pst, double* __restrict__ cp) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int r = 4 * k + (lane >> 3), piece = lane & 7;
+    const int cam = __shfl_sync(0xffffffffu, my_cam, r);
+    if (r < n) pst[r * 9 + piece] = __ldg(reinterpret_cast<const double2*>(prep + (int64_t)cam * 16) + piece);
+  }
+  __syncwarp();
+  if (lane < n) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2 v = pst[lane * 9 + k];
+      cp[2 * k] = v.x;
+      cp[2 * k + 1] = v.y;
+    }
+  }
+}
+
 // Store rows + per-observation V0/b_l contributions + per-landmark sums; one
 // warp per warp-tile, each landmark's observations in camera order (np.add.at's
 // sequential fold of blocks.py:394,396 runs over the same observations in the
 // same order).
 template <bool kExplicit, bool F32>
-__global__ void __launch_bounds__(kBlockTiles * kTile)
+__global__ void __launch_bounds__(kBlockTiles * kTile, POBA_LIN_TILE_BLOCKS)
 k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __restrict__ cam_s,
            const int* __restrict__ file_s, const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s,
            const double* __restrict__ prep, const double* __restrict__ points, const double* __restrict__ ejp,
@@ -175,41 +207,23 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   // cover the padding too), so their latencies overlap
   const int cam_o = cam_s[o];
   const int li_o = lidx_s[o];
+  double2 pix = make_double2(0.0, 0.0);
+  if (!kExplicit) pix = __ldcs(pix_s + o);  // streamed once; the slot array covers the padding
   const Tile t = tiles[ti];
   const bool is_long = t.flags & kTileLong;
   bool bad = false;
   double cp[16];  // this observation's camera record (R, t, f, k1, k2, pad)
   double X0 = 0.0, X1 = 0.0, X2 = 0.0;
-  double2 pix = make_double2(0.0, 0.0);
-  if (!kExplicit && lane < t.n) {  // point and pixel loads in flight during the camera gather
+  if (!kExplicit && lane < t.n) {  // point loads in flight during the camera gather
     const double* X = points + (int64_t)(t.lm0 + (is_long ? 0 : li_o)) * 3;
     X0 = X[0];
     X1 = X[1];
     X2 = X[2];
-    pix = pix_s[o];
   }
   if (!kExplicit) {
     const int my_cam = lane < t.n ? cam_o : 0;
 #if POBA_LIN_COOP_PREP
-    // the tile's 32 camera records (128 B each) gathered cooperatively, four
-    // records per 16-B load instruction, through the warp's shared stage
-    // (144-B stride: conflict-free 16-B reads by consecutive lanes)
-    double2* pst = lin_rec + w * kTile * kLinRec;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int r = 4 * k + (lane >> 3), piece = lane & 7;
-      const int cam = __shfl_sync(0xffffffffu, my_cam, r);
-      if (r < t.n) pst[r * 9 + piece] = __ldg(reinterpret_cast<const double2*>(prep + (int64_t)cam * 16) + piece);
-    }
-    __syncwarp();
-    if (lane < t.n) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double2 v = pst[lane * 9 + k];
-        cp[2 * k] = v.x;
-        cp[2 * k + 1] = v.y;
-      }
-    }
+    gather_prep(prep, my_cam, t.n, lane, lin_rec + w * kTile * kLinRec, cp);
 #else
     if (lane < t.n) load_prep(prep, my_cam, cp);
 #endif
@@ -331,7 +345,7 @@ __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restric
 // that produced the stored rows -- instead of being written camera-major by
 // the tile pass and read back (160 B per observation each way).
 template <bool kExplicit, bool F32>
-__global__ void __launch_bounds__(kCamReduceThreads)
+__global__ void __launch_bounds__(kCamReduceThreads, POBA_CAM_REDUCE_BLOCKS)
 k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ cc_cam, const int* __restrict__ cam_start,
                    int n_cc, const double* __restrict__ prep, const double* __restrict__ points,
                    const int* __restrict__ lm_c, const double2* __restrict__ pix_c, const int* __restrict__ file_c,
@@ -347,6 +361,23 @@ k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ c
   double acc[54];
 #pragma unroll
   for (int q = 0; q < 54; ++q) acc[q] = 0.0;
+  // software pipeline over this lane's observations: the landmark index is
+  // loaded two steps ahead and the point + pixel one step ahead, so the two
+  // dependent load latencies overlap a whole step of arithmetic
+  double nX0 = 0.0, nX1 = 0.0, nX2 = 0.0;
+  double2 npx = make_double2(0.0, 0.0);
+  int lm_n2 = 0;
+  if (!kExplicit) {
+    const int pf = p0 + lane;
+    if (pf < p1) {
+      const int64_t lm = lm_c[pf];
+      nX0 = points[lm * 3];
+      nX1 = points[lm * 3 + 1];
+      nX2 = points[lm * 3 + 2];
+      npx = __ldcs(pix_c + pf);
+    }
+    if (pf + 32 < p1) lm_n2 = lm_c[pf + 32];
+  }
   for (int p = p0 + lane; p < p1; p += 32) {
     ObsModel m;
     if (kExplicit) {
@@ -359,8 +390,17 @@ k_cam_chunk_reduce(const int* __restrict__ cc_cam_off, const int* __restrict__ c
       m.r0 = eres[f * 2];
       m.r1 = eres[f * 2 + 1];
     } else {
-      const int64_t lm = lm_c[p];
-      evaluate_obs<true>(cp, points[lm * 3], points[lm * 3 + 1], points[lm * 3 + 2], __ldcs(pix_c + p), m);
+      const double X0 = nX0, X1 = nX1, X2 = nX2;
+      const double2 px = npx;
+      if (p + 32 < p1) {
+        const int64_t lm = lm_n2;
+        nX0 = points[lm * 3];
+        nX1 = points[lm * 3 + 1];
+        nX2 = points[lm * 3 + 2];
+        npx = __ldcs(pix_c + p + 32);
+      }
+      if (p + 64 < p1) lm_n2 = lm_c[p + 64];
+      evaluate_obs<true>(cp, X0, X1, X2, px, m);
     }
     double a[9], b[9];
 #pragma unroll
@@ -422,25 +462,39 @@ k_cost_tile(const Tile* __restrict__ tiles, int n_tiles, const int* __restrict__
             const double* __restrict__ points, const double* __restrict__ dl, double* __restrict__ block_sum,
             unsigned long long* __restrict__ n_invalid) {
   __shared__ double wsum[kBlockTiles];
+  extern __shared__ __align__(16) double2 lin_rec[];  // per warp: the tile's camera records (gather_prep)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ti = blockIdx.x * kBlockTiles + w;
   double v = 0.0;
   bool bad = false;
   if (ti < n_tiles) {
+    const int64_t o = (int64_t)ti * kTile + lane;
+    // per-slot loads first (the slot arrays cover the padding), then the descriptor's dependants
+    const int cam_o = cam_s[o];
+    const int li_o = lidx_s[o];
+    const double2 pix = __ldcs(pix_s + o);
     const Tile t = tiles[ti];
+    // point (and trial increment) loads in flight during the camera gather
+    double X0 = 0.0, X1 = 0.0, X2 = 0.0, d0 = 0.0, d1 = 0.0, d2 = 0.0;
     if (lane < t.n) {
-      const int64_t o = (int64_t)ti * kTile + lane;
-      const int lm = t.lm0 + ((t.flags & kTileLong) ? 0 : lidx_s[o]);
-      double X0 = points[(int64_t)lm * 3], X1 = points[(int64_t)lm * 3 + 1], X2 = points[(int64_t)lm * 3 + 2];
+      const int64_t lm = t.lm0 + ((t.flags & kTileLong) ? 0 : li_o);
+      X0 = points[lm * 3];
+      X1 = points[lm * 3 + 1];
+      X2 = points[lm * 3 + 2];
       if (dl) {
-        X0 += dl[(int64_t)lm * 3];
-        X1 += dl[(int64_t)lm * 3 + 1];
-        X2 += dl[(int64_t)lm * 3 + 2];
+        d0 = dl[lm * 3];
+        d1 = dl[lm * 3 + 1];
+        d2 = dl[lm * 3 + 2];
       }
+    }
+    double cp[16];
+    gather_prep(prep, lane < t.n ? cam_o : 0, t.n, lane, lin_rec + w * kTile * kLinRec, cp);
+    if (lane < t.n) {
+      X0 += d0;
+      X1 += d1;
+      X2 += d2;
       ObsModel m;
-      double cp[16];
-      load_prep(prep, cam_s[o], cp);
-      evaluate_obs<false>(cp, X0, X1, X2, pix_s[o], m);
+      evaluate_obs<false>(cp, X0, X1, X2, pix, m);
       bad = !m.valid;
       v = m.r0 * m.r0 + m.r1 * m.r1;
     }
@@ -597,7 +651,8 @@ int cost_device(Ctx& c, bool trial, double* cost, int64_t* n_invalid) {
   PTRY(c.scratch_c.alloc((nb + 8) * 8));
   unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(c.flag.as<char>() + 40);
   PCK(cudaMemsetAsync(d_bad, 0, 8, s));
-  k_cost_tile<<<nb, kBlockTiles * kTile, 0, s>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(),
+  cudaFuncSetAttribute(k_cost_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kLinRecSmem);
+  k_cost_tile<<<nb, kBlockTiles * kTile, kLinRecSmem, s>>>(c.tiles.as<Tile>(), c.n_tiles, c.cam_s.as<int>(),
                                                  c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(),
                                                  c.trial_prep.as<double>(), c.points.as<double>(),
                                                  trial ? c.dl.as<double>() : nullptr, c.scratch_c.as<double>(), d_bad);

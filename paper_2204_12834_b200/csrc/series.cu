@@ -759,6 +759,19 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
   if (t.flags & kTileLong) return;  // handled by k_wt_long
   double* wbuf = wbuf_all[w];
   int* lstart = lstart_all[w];
+  // this lane's landmark operands (V^-1, b_l) requested as soon as the tile
+  // descriptor is here, so they travel together with the camera records
+  // instead of after the landmark sums
+  double vi[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, blv[3] = {0.0, 0.0, 0.0};
+  if (OUT != kOutWt && lane < t.nlm) {
+    const int64_t lm = t.lm0 + lane;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) vi[k] = Vinv[lm * 6 + k];
+    if (OUT == kOutBack) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) blv[k] = bl[lm * 3 + k];
+    }
+  }
   if (lane < t.n) {
     const double2* tv = reinterpret_cast<const double2*>(tin + (int64_t)cam * kTStride);
     double tc[10];
@@ -792,10 +805,10 @@ k_wt_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __
     if (OUT == kOutWt) {
       z[0] = y[0]; z[1] = y[1]; z[2] = y[2];
     } else if (OUT == kOutZ) {
-      sym3_mv(Vinv + (int64_t)lm * 6, y, z);
+      sym3_mv(vi, y, z);
     } else {
-      const double yb[3] = {bl[lm * 3] + y[0], bl[lm * 3 + 1] + y[1], bl[lm * 3 + 2] + y[2]};
-      sym3_mv(Vinv + (int64_t)lm * 6, yb, z);
+      const double yb[3] = {blv[0] + y[0], blv[1] + y[1], blv[2] + y[2]};
+      sym3_mv(vi, yb, z);
       z[0] = -z[0]; z[1] = -z[1]; z[2] = -z[2];
       if (z[0] != 0.0 || z[1] != 0.0 || z[2] != 0.0) atomicOr(nonzero_flag, 1);
     }

@@ -5,7 +5,7 @@ PROBS=${*:-"mixed c1 c3:0.1"}
 for t in memcheck racecheck synccheck initcheck; do
   for p in $PROBS; do
     log=gpurun_out/sanitize_${t}_${p/:/_}.log
-    timeout 900 compute-sanitizer --tool $t --error-exitcode 9 --print-limit 20 python tools/sanitize.py $p > $log 2>&1
+    timeout ${SAN_TIMEOUT:-900} compute-sanitizer --tool $t --error-exitcode 9 --print-limit 20 python tools/sanitize.py $p > $log 2>&1
     echo "$t $p rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|sanitize workload ok' $log | tr '\n' ' ')"
   done
 done

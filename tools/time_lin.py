@@ -15,7 +15,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 tag = sys.argv[3] if len(sys.argv) > 3 else os.environ.get("POBA_LIB", "default")
 prec = int(sys.argv[4]) if len(sys.argv) > 4 else 64
-p = configs.make_config(name, scale, seed=0)
+import _cfg
+p = _cfg.load(name, scale)
 dp = blocks.DeviceProblem(p.cam_indices, p.pt_indices, p.pixels, p.n_cameras, p.n_points)
 dev = dp.dev
 dev.set_points(p.points)

@@ -21,7 +21,8 @@ from paper_2204_12834_b200 import configs
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
-p = configs.make_config(name, scale)
+import _cfg
+p = _cfg.load(name, scale)
 st = configs.LM_SETTINGS.get(name, configs.LmSettings())
 cams = torch.from_numpy(p.camera_params).pin_memory().numpy()
 pts = torch.from_numpy(p.points).pin_memory().numpy()
