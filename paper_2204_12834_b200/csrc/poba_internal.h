@@ -90,7 +90,9 @@ static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinati
 
 // metadata word of a slot: chunk slot (bits 0-10), landmark index in the tile
 // (11-15; 0 for a long landmark's sub-tile), first (16-20) and last (21-25)
-// lane of the landmark's run
+// lane of the landmark's run, apply lane (26-30: the lane whose camera
+// contribution this lane adds to the accumulator table, 31: this lane applies;
+// carried in the slot word's upper bits, see store.cu)
 __host__ __device__ __forceinline__ uint32_t pack_meta(int slot, int li, int first, int last) {
   return (uint32_t)slot | ((uint32_t)li << 11) | ((uint32_t)first << 16) | ((uint32_t)last << 21);
 }
@@ -98,6 +100,8 @@ __host__ __device__ __forceinline__ int meta_slot(uint32_t m) { return (int)(m &
 __host__ __device__ __forceinline__ int meta_li(uint32_t m) { return (int)((m >> 11) & 0x1fu); }
 __host__ __device__ __forceinline__ int meta_first(uint32_t m) { return (int)((m >> 16) & 0x1fu); }
 __host__ __device__ __forceinline__ int meta_last(uint32_t m) { return (int)((m >> 21) & 0x1fu); }
+__host__ __device__ __forceinline__ int meta_apply_src(uint32_t m) { return (int)((m >> 26) & 0x1fu); }
+__host__ __device__ __forceinline__ bool meta_apply_on(uint32_t m) { return (m >> 31) != 0u; }
 template <bool F32>
 constexpr int tile_block_bytes() { return F32 ? kTileBlockF32 : kTileBlock; }
 // bytes of a tile's bulk copy: metadata + planes up to plane 11's last valid

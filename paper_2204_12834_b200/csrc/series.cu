@@ -348,8 +348,9 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
     const bool valid = lane < t.n;
     const bool is_long = t.flags & kTileLong;
     int slot = 0, li = 0, first = lane, last = lane;
-    if (valid) {  // slot, landmark run: the tile's metadata word of this lane
-      const uint32_t mv = reinterpret_cast<const uint32_t*>(stg)[lane];
+    // the tile's metadata word of this lane (padding lanes carry an apply lane too)
+    const uint32_t mv = reinterpret_cast<const uint32_t*>(stg)[lane];
+    if (valid) {  // slot, landmark run
       slot = meta_slot(mv);
       li = meta_li(mv);
       POBA_DCHECK(slot < t.nslot && li < kTileLm && t.lm0 + li < a.n_lm);
@@ -489,10 +490,17 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
       }
     }
     if (q > 0) apply_held();
+    // hand each distinct camera's contribution to its apply lane (host-planned
+    // permutation: the slots of a quarter differ mod 8, so the 16-B accumulator
+    // accesses of a quarter do not collide); shuffles instead of bank replays
+    {
+      const int from = meta_apply_src(mv);
 #pragma unroll
-    for (int j = 0; j < 9; ++j) hg[j] = g[j];
-    h_slot = slot;
-    h_apply = apply;
+      for (int j = 0; j < 9; ++j) hg[j] = __shfl_sync(0xffffffffu, g[j], from);
+      h_slot = __shfl_sync(0xffffffffu, slot, from);
+      h_apply = meta_apply_on(mv);
+      POBA_DCHECK(!h_apply || __shfl_sync(0xffffffffu, (int)apply, from));
+    }
     h_ti = ti;
     h_flags = t.flags;
     h_part0 = t.part0;

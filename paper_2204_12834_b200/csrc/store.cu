@@ -146,7 +146,8 @@ __global__ void k_pack_meta(const Tile* __restrict__ tiles, const int* __restric
   const unsigned above = heads & ~((2u << lane) - 1u);
   const int last = (above ? __ffs(above) - 1 : t.n) - 1;
   const int first = 31 - __clz(heads & ((2u << lane) - 1u));
-  *meta_ptr<F32>(J, s) = valid ? pack_meta(slot_s[s], li, first, last) : 0u;
+  // slot_s carries the apply lane in bits 26-31 (every lane, padding included)
+  *meta_ptr<F32>(J, s) = valid ? pack_meta(slot_s[s], li, first, last) : ((uint32_t)slot_s[s] & 0xfc000000u);
 }
 
 __global__ void k_cam_slot_keys(const Tile* __restrict__ tiles, const int* __restrict__ cam_s,
@@ -809,6 +810,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   // numbered in first-appearance order; partial p = part0 + slot of a chunk
   // holds that camera's sum over the chunk.
   std::vector<int> obs_slot(ns, 0);
+  std::vector<uint8_t> obs_meta_hi(ns, 0);  // apply lane of each slot: source lane (bits 0-4), active (bit 5)
   std::vector<Chunk> chunks;
   std::vector<int> part_cam;  // camera of each partial
   {
@@ -869,8 +871,14 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     }
     for (const Chunk& q : chunks) tiles[q.tile1 - 1].flags |= kTileChunkLast;
     if (!getenv("POBA_NO_SLOT_COLOR")) {
-      const char* g = getenv("POBA_SLOT_GROUP");  // A/B: lanes per colouring group (8 = one quarter, 16, 32)
-      const int group = (g && (atoi(g) == 16 || atoi(g) == 32)) ? atoi(g) : 8;
+      // lanes per colouring group: with the apply-lane permutation (below) a
+      // tile's cameras can be dealt to any quarter, so what matters is that no
+      // colour has more than four cameras in a TILE (group 32) and the order
+      // of lanes inside a run no longer matters (no lane-ordering rounds);
+      // without it the colouring works per quarter (group 8) as in round 1
+      const bool perm_on = !getenv("POBA_NO_APPLY_PERM");
+      const char* g = getenv("POBA_SLOT_GROUP");  // A/B override: 8, 16 or 32
+      const int group = (g && (atoi(g) == 8 || atoi(g) == 16 || atoi(g) == 32)) ? atoi(g) : (perm_on ? 32 : 8);
       const char* ps = getenv("POBA_SLOT_PASSES");  // A/B: local-search passes after the greedy colouring
       const int passes = ps ? std::max(0, atoi(ps)) : kSlotPasses;
       std::vector<int> pc;  // rebuilt camera of every partial (-1: hole)
@@ -885,7 +893,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
       // rounds of within-run lane ordering (host permutation of the tile's
       // slots, applied to the device slot arrays) and re-colouring
       const char* lr = getenv("POBA_LANE_ROUNDS");  // A/B: 0 disables
-      const int rounds = lr ? std::max(0, atoi(lr)) : kLaneRounds;
+      const int rounds = lr ? std::max(0, atoi(lr)) : (perm_on ? 0 : kLaneRounds);
       if (rounds > 0) {
         std::vector<uint8_t> hl(ns);
         PTRY(poba::copy_sync(c, hl.data(), c.lidx_s.p, ns, cudaMemcpyDeviceToHost));
@@ -942,17 +950,78 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
         PCK(cudaStreamSynchronize(s));
       }
     }
+    // Apply lanes.  The term kernel adds each distinct camera of a tile (held by
+    // its lowest lane after the duplicate pre-sum) to its accumulator record
+    // with 16-B accesses, served one eight-lane quarter at a time; lanes of a
+    // quarter whose slots agree mod 8 serialise.  Which lane performs a
+    // camera's access is free, so each tile carries a lane permutation: lane d
+    // pulls the contribution of lane src(d) with warp shuffles and applies it
+    // (bits 26-30 of its metadata word: src, bit 31: active).  The cameras of
+    // a colour class are spread over the four quarters, so a quarter holds two
+    // slots of one colour only if the tile has more than four of that colour.
+    if (!getenv("POBA_NO_APPLY_PERM")) {
+      std::vector<int> seen(n_cam, -1);
+      for (int ti = 0; ti < c.n_tiles; ++ti) {
+        const int64_t s0 = (int64_t)ti * kTile;
+        int by_col[8][kTile], n_col[8] = {};
+        for (int i = 0; i < tiles[ti].n; ++i) {
+          const int cam = hcam[s0 + i];
+          if (seen[cam] == ti) continue;  // not the camera's lowest lane
+          seen[cam] = ti;
+          const int col = obs_slot[s0 + i] & 7;
+          by_col[col][n_col[col]++] = i;
+        }
+        int order[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+        std::sort(order, order + 8, [&](int a, int b) { return n_col[a] != n_col[b] ? n_col[a] > n_col[b] : a < b; });
+        // a quarter costs its largest colour multiplicity: place each camera where
+        // that grows least (colours in decreasing size, so the doubles of a colour
+        // with more than four cameras land in quarters that already have a double)
+        int load[4] = {}, has[4][8] = {}, qmax[4] = {};
+        int src_of[kTile];
+        for (int d = 0; d < kTile; ++d) src_of[d] = -1;
+        for (int oc = 0; oc < 8; ++oc) {
+          const int col = order[oc];
+          for (int k = 0; k < n_col[col]; ++k) {
+            int best = -1, best_grow = 0;
+            for (int qq = 0; qq < 4; ++qq) {
+              if (load[qq] >= 8) continue;
+              const int grow = std::max(qmax[qq], has[qq][col] + 1) - qmax[qq];
+              if (best < 0 || grow < best_grow || (grow == best_grow && has[qq][col] < has[best][col]) ||
+                  (grow == best_grow && has[qq][col] == has[best][col] && load[qq] < load[best])) {
+                best = qq;
+                best_grow = grow;
+              }
+            }
+            src_of[best * 8 + load[best]] = by_col[col][k];
+            load[best]++;
+            has[best][col]++;
+            qmax[best] = std::max(qmax[best], has[best][col]);
+          }
+        }
+        for (int d = 0; d < kTile; ++d)
+          obs_meta_hi[s0 + d] = src_of[d] >= 0 ? (uint8_t)(src_of[d] | 32) : (uint8_t)d;
+      }
+    } else {
+      std::vector<int> seen(n_cam, -1);
+      for (int ti = 0; ti < c.n_tiles; ++ti) {
+        const int64_t s0 = (int64_t)ti * kTile;
+        for (int d = 0; d < kTile; ++d) obs_meta_hi[s0 + d] = (uint8_t)d;
+        for (int i = 0; i < tiles[ti].n; ++i) {
+          const int cam = hcam[s0 + i];
+          if (seen[cam] == ti) continue;
+          seen[cam] = ti;
+          obs_meta_hi[s0 + i] = (uint8_t)(i | 32);
+        }
+      }
+    }
     if (getenv("POBA_SLOT_STATS")) {  // bank-conflict model: sum over quarters of the largest residue class
       int64_t wf = 0, ideal = 0;
-      std::vector<int> last(c.n_cam, -1);
       for (int ti = 0; ti < c.n_tiles; ++ti) {
         const int64_t s0 = (int64_t)ti * kTile;
         int cnt[4][8] = {};
-        for (int i = 0; i < tiles[ti].n; ++i) {
-          const int cam = hcam[s0 + i];
-          if (last[cam] == ti) continue;
-          last[cam] = ti;
-          cnt[i / 8][obs_slot[s0 + i] & 7]++;
+        for (int d = 0; d < kTile; ++d) {
+          if (!(obs_meta_hi[s0 + d] & 32)) continue;
+          cnt[d / 8][obs_slot[s0 + (obs_meta_hi[s0 + d] & 31)] & 7]++;
         }
         for (int qq = 0; qq < 4; ++qq) {
           int mx = 0, tot = 0;
@@ -1057,6 +1126,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   PTRY(c.Rz.alloc((size_t)ns * 16));
   PCK(cudaMemsetAsync(c.Rz.p, 0, (size_t)ns * 16, s));
   PTRY(c.slot_s.alloc(ns * 4));
+  for (int64_t q = 0; q < ns; ++q) obs_slot[q] |= (int)((uint32_t)obs_meta_hi[q] << 26);  // metadata bits 26-31
   PCK(cudaMemcpyAsync(c.slot_s.p, obs_slot.data(), ns * 4, cudaMemcpyHostToDevice, s));
   PCK(cudaStreamSynchronize(s));  // obs_slot is a local vector
   PTRY(alloc_store(c));

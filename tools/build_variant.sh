@@ -11,8 +11,8 @@ OBJ=/tmp/libab_obj/$NAME
 mkdir -p "$OUT" "$OBJ"
 NVCC=/usr/local/cuda/bin/nvcc
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-FLAGS="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $EXTRA"
-SRC=$ROOT/paper_2204_12834_b200/csrc
+FLAGS="-I $ROOT/include $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $EXTRA"
+SRC=${POBA_SRC:-$ROOT/paper_2204_12834_b200/csrc}
 pids=()
 for f in "$SRC"/*.cu; do
   $NVCC $FLAGS -c "$f" -o "$OBJ/$(basename "$f" .cu).o" & pids+=($!)

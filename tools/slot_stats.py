@@ -9,6 +9,7 @@ from paper_2204_12834_b200 import blocks, configs  # noqa: E402
 
 for arg in sys.argv[1:] or ["c5:1.0"]:
     name, scale = (arg.split(":") + ["1.0"])[:2]
-    p = configs.make_config(name, float(scale), seed=0)
+    import _cfg
+    p = _cfg.load(name, float(scale))
     print(arg, p.n_observations, flush=True)
     blocks.DeviceProblem(p.cam_indices, p.pt_indices, p.pixels, p.n_cameras, p.n_points)

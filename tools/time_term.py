@@ -22,7 +22,11 @@ dev.set_points(p.points)
 dev.set_precision(prec)
 dev.linearize(p.camera_params)
 dev.damp(1e-4)
-x, order, _, _ = dev.series_solve(1e-300, 16)
+try:
+    x, order, _, _ = dev.series_solve(1e-300, 16)
+except Exception as e:  # ablation builds (tools only) may produce vanishing / non-finite iterates
+    print("series_solve:", e)
+    x = np.zeros(1)
 ts = [dev.time_terms(20) for _ in range(5)]
 print(f"{name} x{scale} {tag} fp{prec}: term kernel {1e3 * np.median([t[1] for t in ts]):8.1f} us, "
       f"term {1e3 * np.median([t[0] for t in ts]):8.1f} us, |x| {np.linalg.norm(x):.17g}")
