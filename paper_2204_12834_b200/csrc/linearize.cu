@@ -39,9 +39,15 @@ constexpr int kCamReduceThreads = POBA_CAM_REDUCE_THREADS;
 #ifndef POBA_CAM_REDUCE_BLOCKS
 #define POBA_CAM_REDUCE_BLOCKS 2
 #endif
-#ifndef POBA_LIN_TILE_BLOCKS
-#define POBA_LIN_TILE_BLOCKS 2  // 3 (80 registers, spills) measured slower
+// tile pass shape: warp-tiles per block x blocks per SM the kernel is compiled for
+#ifndef POBA_LIN_TILES
+#define POBA_LIN_TILES 8
 #endif
+#ifndef POBA_LIN_TILE_BLOCKS
+#define POBA_LIN_TILE_BLOCKS 2  // 8 x 3 (80 registers, spills) measured slower
+#endif
+constexpr int kLinTiles = POBA_LIN_TILES;
+constexpr int kLinTileSmem = kLinTiles * kTile * kLinRec * 16;
 
 // Rotation matrix of an axis-angle vector through the unit quaternion, the
 // same construction scipy uses (from_rotvec -> as_matrix).
@@ -186,19 +192,19 @@ __device__ __forceinline__ void gather_prep(const double* __restrict__ prep, int
 // sequential fold of blocks.py:394,396 runs over the same observations in the
 // same order).
 template <bool kExplicit, bool F32>
-__global__ void __launch_bounds__(kBlockTiles * kTile, POBA_LIN_TILE_BLOCKS)
+__global__ void __launch_bounds__(kLinTiles * kTile, POBA_LIN_TILE_BLOCKS)
 k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __restrict__ cam_s,
            const int* __restrict__ file_s, const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s,
            const double* __restrict__ prep, const double* __restrict__ points, const double* __restrict__ ejp,
            const double* __restrict__ ejl, const double* __restrict__ eres, void* __restrict__ J,
            double2* __restrict__ Rz, double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
            unsigned long long* __restrict__ n_invalid) {
-  __shared__ double contrib_all[kBlockTiles][kTile * 9];
-  __shared__ int lstart_all[kBlockTiles][kTile + 1];
+  __shared__ double contrib_all[kLinTiles][kTile * 9];
+  __shared__ int lstart_all[kLinTiles][kTile + 1];
   // per warp: the tile's 32 camera records, staged for the cooperative gather
   extern __shared__ __align__(16) double2 lin_rec[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ti = tile0 + blockIdx.x * kBlockTiles + w;
+  const int ti = tile0 + blockIdx.x * kLinTiles + w;
   if (ti >= tile_end) return;  // warps are independent: no block-wide barrier below
   double* contrib = contrib_all[w];
   int* lstart = lstart_all[w];
@@ -559,8 +565,8 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
   auto lin = [&](auto kern, const double* prep, const double* pts, const double* a, const double* b,
                  const double* r, int t0, int t1) {
     if (t1 <= t0) return;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLinRecSmem);
-    kern<<<grid_for(t1 - t0, kBlockTiles), kBlockTiles * kTile, kLinRecSmem, s>>>(
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kLinTileSmem);
+    kern<<<grid_for(t1 - t0, kLinTiles), kLinTiles * kTile, kLinTileSmem, s>>>(
         c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(), c.file_s.as<int>(), c.pix_s.as<double2>(),
         c.lidx_s.as<uint8_t>(), prep, pts, a, b, r, c.J.p, c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
         c.Dl.as<double>(), d_bad);

@@ -499,7 +499,10 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
       for (int j = 0; j < 9; ++j) hg[j] = __shfl_sync(0xffffffffu, g[j], from);
       h_slot = __shfl_sync(0xffffffffu, slot, from);
       h_apply = meta_apply_on(mv);
-      POBA_DCHECK(!h_apply || __shfl_sync(0xffffffffu, (int)apply, from));
+#ifdef POBA_DEVICE_CHECKS
+      const int src_applies = __shfl_sync(0xffffffffu, (int)apply, from);  // every lane takes part
+      POBA_DCHECK(!h_apply || src_applies);
+#endif
     }
     h_ti = ti;
     h_flags = t.flags;
