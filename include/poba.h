@@ -80,6 +80,11 @@ int poba_set_precision(poba_ctx* ctx, int bits);
 /* info[0..15]: n_groups, n_tiles, n_chunks, n_partials, obs_lo, obs_hi, lm_lo,
  * lm_hi, max_slots, n_long, device_bytes, k_max, n_cam, n_pt, n_obs, rank   */
 int poba_problem_info(poba_ctx* ctx, int64_t* info);
+/* Camera-side layout the store build chose for the fused term kernel (no
+ * reference counterpart; a measurement aid): *table = 1 when the chunk's term
+ * records are kept in a per-CTA shared-memory table (camera working set of a
+ * CTA range fits: C1-C4), 0 when every tile gathers its records (C5).        */
+int poba_term_layout(poba_ctx* ctx, int* table);
 /* order / cam_sorted / pt_sorted (n_obs each): bit-exact with the reference */
 int poba_get_ordering(poba_ctx* ctx, int64_t* order, int64_t* cam_sorted, int64_t* pt_sorted);
 /* k-groups (k ascending): group k, first canonical observation, #landmarks */

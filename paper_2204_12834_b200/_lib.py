@@ -40,6 +40,7 @@ _SIGS = {
     "poba_create_local": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(_P)]),
     "poba_set_problem": (ctypes.c_int, [_P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _I64P, _I64P, _DP]),
     "poba_problem_info": (ctypes.c_int, [_P, _I64P]),
+    "poba_term_layout": (ctypes.c_int, [_P, _IP]),
     "poba_get_ordering": (ctypes.c_int, [_P, _I64P, _I64P, _I64P]),
     "poba_get_groups": (ctypes.c_int, [_P, ctypes.c_int64, _I64P, _I64P, _I64P, _I64P]),
     "poba_linearize": (ctypes.c_int, [_P, _DP, _DP, _I64P]),
@@ -242,7 +243,11 @@ class Device:
         _check(self._lib.poba_problem_info(self._h, _i64(v)))
         keys = ("n_groups", "n_tiles", "n_chunks", "n_partials", "n_obs_local", "n_slots", "lm_lo", "lm_hi",
                 "max_slots", "n_long", "device_bytes", "k_max", "n_cam", "n_pt", "n_obs", "rank")
-        return dict(zip(keys, (int(x) for x in v)))
+        d = dict(zip(keys, (int(x) for x in v)))
+        t = ctypes.c_int(0)
+        _check(self._lib.poba_term_layout(self._h, ctypes.byref(t)))
+        d["term_layout"] = "table" if t.value else "gather"
+        return d
 
     def ordering(self):
         o = np.empty(self.n_obs, dtype=np.int64)

@@ -615,6 +615,14 @@ int poba_problem_info(poba_ctx* ctx, int64_t* info) {
   return POBA_OK;
 }
 
+int poba_term_layout(poba_ctx* ctx, int* table) {
+  CTX_CHECK(ctx);
+  NEED(table, "null output");
+  NEED(ctx->c.have_problem, "no problem");
+  *table = ctx->c.chunk_t ? 1 : 0;
+  return POBA_OK;
+}
+
 int poba_get_ordering(poba_ctx* ctx, int64_t* order, int64_t* cam_sorted, int64_t* pt_sorted) {
   CTX_CHECK(ctx);
   Ctx& c = ctx->c;

@@ -69,20 +69,38 @@ constexpr int kStDesc = kTileBlock;                              // 32-B tile de
 constexpr int kStVinv = kStDesc + 32;                            // V^-1 slice
 constexpr int kStageBytes = kStVinv + kTileLm * 48;              // 7072
 constexpr int kTRecBytes = kTStride * 8;                         // 80
-constexpr int kWarpSmem = kStageBytes + kTile * kTRecBytes;      // + camera-record table = 9632
+// Two layouts of the camera side, chosen per context when the store is built
+// (Ctx::chunk_t):
+//   gather (CT = false)  every warp gathers the 32 term records of its next
+//                        tile from L2 into a per-warp table; the accumulator
+//                        table gets all the remaining shared memory (1440 slots)
+//   table  (CT = true)   the term records of the chunk's cameras sit in a
+//                        second per-CTA table next to the accumulator table,
+//                        loaded once per chunk by all warps and read by slot
+//                        (no per-tile gather); 896 slots, so chunks are
+//                        smaller -- chosen when a CTA range's camera working
+//                        set still fits (C1-C4), not on C5
 // one CTA: the 227-KB per-CTA limit; several: an equal share of the SM's 228 KB less the 1 KB reserved per CTA
 constexpr int kTermSmemMax = kTermCtas == 1 ? 227 * 1024 : (228 * 1024) / kTermCtas - 1024;
 constexpr int kTermCtl = kTermWarps * 16 + 16;                   // full + empty stage barriers + pad
-constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kTRecBytes) / 32 * 32;
-constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kTRecBytes;
-static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
-static_assert(kAccSlots < 2048, "chunk slots must fit the 11-bit metadata field");
+template <bool CT>
+struct TermShape {
+  static constexpr int kWarpSmem = kStageBytes + (CT ? 0 : kTile * kTRecBytes);  // stage (+ per-warp record table)
+  static constexpr int kSlotBytes = CT ? 2 * kTRecBytes : kTRecBytes;           // accumulator (+ term record)
+  static constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kSlotBytes) / 32 * 32;
+  static constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kSlotBytes;
+  static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
+  static_assert(kAccSlots < 2048, "chunk slots must fit the 11-bit metadata field");
+  static_assert(kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
+};
 static_assert(kTermCtl % 16 == 0, "the accumulator table after the stage barriers must stay 16-B aligned");
-static_assert(kTermWarps >= 2 && kTermWarps <= 15, "the apply turn uses named barriers 1..kTermWarps (ring of >= 2)");
+static_assert(kTermWarps >= 2 && kTermWarps <= 14, "the apply turn uses named barriers 1..kTermWarps (ring of >= 2), the chunk barrier 15");
+static_assert(kStageBytes % 16 == 0, "bulk-copy destinations must be 16-B aligned");
+// the table layout is taken when it needs at most this many times the gather layout's chunk partials
+constexpr double kChunkTMaxGrowth = 3.0;  // C4: 2.1x the partials, kernel -6%; C5 x 0.3: 8x, kernel 2x slower
 constexpr int kSlotSlack = 2;   // extra slots per bank colour class in the slot numbering (store.cu)
 constexpr int kSlotPasses = 2;  // local-search passes of the slot colouring
 constexpr int kLaneRounds = 2;  // rounds of within-run lane ordering + re-colouring (store.cu)
-static_assert(kStageBytes % 16 == 0 && kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 
 // PoBA-32 (blocks.py:42-47): block storage may be fp32 (planes of float2);
 // every value read from it is widened to fp64 and all arithmetic and
@@ -257,6 +275,7 @@ struct Ctx {
   DBuf xch_send, xch_recv;      // rank-ordered all-reduce: padded slices out / in
   int64_t cam_ls = 0;           // sharded: cameras per rank slice of the camera step (>= 4)
   int n_sm = 148;
+  bool chunk_t = false;         // term-kernel camera-side layout of this store (TermShape<chunk_t>)
   int64_t launches = 0;
 
   // global sizes
@@ -304,6 +323,7 @@ struct Ctx {
   cudaEvent_t xfer_ev[2 * kXferPieces + 1] = {};
   DBuf part_cam_off; // int32 [n_cam+1] camera -> range in part_idx
   DBuf part_idx;     // int32 [n_partials] partial indices per camera, chunk order
+  DBuf part_cam;     // int32 [n_partials] camera of each partial (-1: hole of the slot numbering)
   DBuf long_lm;      // int32 [n_long] local landmarks with k > kTile
   std::vector<int> long_host;
   std::vector<Chunk> chunks_host;

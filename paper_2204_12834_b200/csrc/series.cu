@@ -219,7 +219,8 @@ __device__ __forceinline__ void turn_wait(int warp) {
 struct TermArgs {
   const TileK* tk;         // per warp-tile kernel descriptors
   const int2* cta_tiles;   // tile range of each CTA
-  const int* cam_s;        // camera of each slot (gathered two tiles ahead)
+  const int* cam_s;        // camera of each slot (gathered two tiles ahead; unused with kChunkT)
+  const int* part_cam;     // camera of each partial = of each chunk slot (kChunkT: fills the chunk's term-record table)
   const void* J;           // slot rows (double2, or float2 at precision 32)
   const double* tin;       // camera vector (kModeTerm)
   const double* lvec;      // b_l (kModeBt) or landmark input (kModeW)
@@ -251,8 +252,11 @@ struct TermArgs {
 //            pre-summed in lane order.
 // After the last tile of a chunk its warp writes the table out once (one 80-B
 // partial per (chunk, camera)) and clears it before passing the turn on.
-template <int MODE, bool F32>
+template <int MODE, bool F32, bool CT>
 __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermArgs a) {
+  constexpr int kWarpSmem = TermShape<CT>::kWarpSmem;
+  constexpr int kAccSlots = TermShape<CT>::kAccSlots;
+  constexpr bool kChunkT = CT;
   extern __shared__ __align__(128) uint8_t smraw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (a.check_stop && a.st->stopped) return;
@@ -261,6 +265,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
   uint64_t* stage_bar = reinterpret_cast<uint64_t*>(ctl);  // [kTermWarps] full (copy landed)
   uint64_t* free_bar = stage_bar + kTermWarps;             // [kTermWarps] empty (all lanes read it)
   double2* acc = reinterpret_cast<double2*>(ctl + kTermCtl);                              // [kAccSlots][5]
+  double2* ttc = acc + kAccSlots * 5;  // kChunkT: [kAccSlots][5] term records of the current chunk's cameras
   for (int k = threadIdx.x; k < kAccSlots * 5; k += blockDim.x) acc[k] = make_double2(0.0, 0.0);
   if (threadIdx.x == 0) {
     for (int w = 0; w < kTermWarps; ++w) {
@@ -274,7 +279,10 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
   if (t_first >= range.y) return;
   const int nq = (range.y - t_first + kTermWarps - 1) / kTermWarps;
   uint8_t* stg = smraw + wid * kWarpSmem;
-  double2* ttab = reinterpret_cast<double2*>(stg + kStageBytes);  // [32 observations][5] camera records
+  double2* ttab = reinterpret_cast<double2*>(stg + kStageBytes);  // [32 observations][5] camera records (!kChunkT)
+  constexpr bool kGather = MODE == kModeTerm && !kChunkT;  // per-tile record gather
+  constexpr bool kTable = MODE == kModeTerm && kChunkT;    // per-chunk record table
+  int cur_part0 = -1;
   uint64_t* sbar = &stage_bar[wid];
   uint64_t* fbar = &free_bar[wid];
   const uint64_t pol = policy_evict_first();
@@ -303,7 +311,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
   }
   double2 tp[5];  // camera-record pieces of the next tile, in flight (five lanes per 80-B record)
   int cam_next = 0;
-  if (MODE == kModeTerm) {
+  if (kGather) {
     gather(a.cam_s[(int64_t)t_first * kTile + lane], tp);
 #pragma unroll
     for (int r = 0; r < 5; ++r) ttab[32 * r + lane] = tp[r];
@@ -345,6 +353,21 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
     const int ti = t_first + q * kTermWarps;
     mbar_wait(sbar, (uint32_t)(q & 1));
     const TileK t = *reinterpret_cast<const TileK*>(stg + kStDesc);
+    if (kTable && t.part0 != cur_part0) {
+      // first round of a chunk (chunks start at rounds, so every warp that has
+      // a tile in this round is here): once all of them are past their reads
+      // of the previous chunk's records, they load the new chunk's together
+      const int nact = min(kTermWarps, range.y - range.x - q * kTermWarps);
+      asm volatile("bar.sync 15, %0;" ::"r"(nact * 32) : "memory");
+      for (int k = wid * 32 + lane; k < t.nslot * 5; k += nact * 32) {
+        const int cam = a.part_cam[t.part0 + k / 5];
+        POBA_DCHECK(cam < a.n_cam);
+        ttc[k] = cam >= 0 ? __ldg(reinterpret_cast<const double2*>(a.tin + (int64_t)cam * kTStride) + k % 5)
+                          : make_double2(0.0, 0.0);
+      }
+      asm volatile("bar.sync 15, %0;" ::"r"(nact * 32) : "memory");
+      cur_part0 = t.part0;
+    }
     const bool valid = lane < t.n;
     const bool is_long = t.flags & kTileLong;
     int slot = 0, li = 0, first = lane, last = lane;
@@ -393,7 +416,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
     __syncwarp();
     if (lane == 0) mbar_arrive(fbar);
     // the next tile's camera records, in flight during this tile's math
-    if (MODE == kModeTerm && q + 1 < nq) {
+    if (kGather && q + 1 < nq) {
       gather(cam_next, tp);
       cam_next = (q + 2 < nq) ? a.cam_s[(int64_t)(ti + 2 * kTermWarps) * kTile + lane] : 0;
     }
@@ -401,9 +424,10 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
     // at the end of the previous tile)
     double tc[10];
     if (MODE == kModeTerm) {
+      const double2* rec = kChunkT ? ttc + slot * 5 : ttab + lane * 5;
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
-        const double2 v = ttab[lane * 5 + p];
+        const double2 v = rec[p];
         tc[2 * p] = v.x;
         tc[2 * p + 1] = v.y;
       }
@@ -508,7 +532,7 @@ __global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermA
     h_flags = t.flags;
     h_part0 = t.part0;
     h_nslot = t.nslot;
-    if (MODE == kModeTerm && q + 1 < nq) {
+    if (kGather && q + 1 < nq) {
 #pragma unroll
       for (int r = 0; r < 5; ++r) ttab[32 * r + lane] = tp[r];
     }
@@ -976,14 +1000,22 @@ int configure_term(Ctx& c) {
   int dev = 0;
   PCK(cudaGetDevice(&dev));
   if (done_dev != dev) {
-    const void* fns[] = {(const void*)k_term<kModeTerm, false>, (const void*)k_term<kModeBt, false>,
-                         (const void*)k_term<kModeW, false>,    (const void*)k_term<kModeTerm, true>,
-                         (const void*)k_term<kModeBt, true>,    (const void*)k_term<kModeW, true>};
-    for (const void* f : fns) {
-      PCK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kTermSmem));
+    auto setup = [](const void* f, int smem) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
       // all of the SM's unified L1 as shared memory (needed for kTermCtas > 1 to be co-resident)
-      PCK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    }
+      return cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    };
+#define POBA_TERM_SETUP(CT)                                                                          \
+  PCK(setup((const void*)k_term<kModeTerm, false, CT>, TermShape<CT>::kTermSmem));                   \
+  PCK(setup((const void*)k_term<kModeBt, false, CT>, TermShape<CT>::kTermSmem));                     \
+  PCK(setup((const void*)k_term<kModeW, false, CT>, TermShape<CT>::kTermSmem));                      \
+  PCK(setup((const void*)k_term<kModeTerm, true, CT>, TermShape<CT>::kTermSmem));                    \
+  PCK(setup((const void*)k_term<kModeBt, true, CT>, TermShape<CT>::kTermSmem));                      \
+  PCK(setup((const void*)k_term<kModeW, true, CT>, TermShape<CT>::kTermSmem));
+    POBA_TERM_SETUP(false)
+    POBA_TERM_SETUP(true)
+#undef POBA_TERM_SETUP
     done_dev = dev;
   }
   return POBA_OK;
@@ -994,6 +1026,7 @@ TermArgs term_args(Ctx& c, const double* tin, const double* lvec, bool check_sto
   a.tk = c.tilek.as<TileK>();
   a.cta_tiles = c.cta_tiles.as<int2>();
   a.cam_s = c.cam_s.as<int>();
+  a.part_cam = c.part_cam.as<int>();
   a.J = c.J.p;
   a.tin = tin;
   a.lvec = lvec;
@@ -1035,23 +1068,29 @@ CamArgs cam_args(Ctx& c, int order, double eps, bool check_stop) {
   return a;
 }
 
-int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool check_stop) {
-  PTRY(configure_term(c));
-  const TermArgs a = term_args(c, tin, lvec, check_stop);
-  const size_t smem = kTermSmem;
+template <bool CT>
+void launch_term_shape(Ctx& c, int mode, const TermArgs& a) {
+  const size_t smem = TermShape<CT>::kTermSmem;
   const unsigned grid = (unsigned)c.n_cta;
   const bool f32 = c.precision == 32;
   if (mode == kModeTerm) {
-    launch_wt_long<kOutZ>(c, tin, kTStride, nullptr, c.ltmp.as<double>(), nullptr, check_stop);
-    if (f32) k_term<kModeTerm, true><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
-    else k_term<kModeTerm, false><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeTerm, true, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeTerm, false, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   } else if (mode == kModeBt) {
-    if (f32) k_term<kModeBt, true><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
-    else k_term<kModeBt, false><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeBt, true, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeBt, false, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   } else {
-    if (f32) k_term<kModeW, true><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
-    else k_term<kModeW, false><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeW, true, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeW, false, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
   }
+}
+
+int launch_term(Ctx& c, int mode, const double* tin, const double* lvec, bool check_stop) {
+  PTRY(configure_term(c));
+  const TermArgs a = term_args(c, tin, lvec, check_stop);
+  if (mode == kModeTerm) launch_wt_long<kOutZ>(c, tin, kTStride, nullptr, c.ltmp.as<double>(), nullptr, check_stop);
+  if (c.chunk_t) launch_term_shape<true>(c, mode, a);
+  else launch_term_shape<false>(c, mode, a);
   c.launches++;
   PCK(cudaGetLastError());
   return POBA_OK;

@@ -832,6 +832,62 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
       prev = e;
     }
     std::vector<int> stamp(n_cam, -1), tstamp(n_cam, -1), slot_of(n_cam, 0);
+    // Camera-side layout of the term kernel (TermShape).  With the table layout
+    // a chunk's term records are loaded into shared memory by all warps of the
+    // CTA at a round boundary (a round = kTermWarps consecutive tiles, one per
+    // warp), so chunks start only at rounds of the CTA's range, and the table
+    // has fewer slots.  It is taken when the camera working set of the CTA
+    // ranges still fits: at most kChunkTMaxGrowth times the gather layout's
+    // partials (dry run of the chunk cut for both); POBA_TERM_CHUNK_T=0/1 forces.
+    auto count_partials = [&](int cap, int align) -> int64_t {
+      std::vector<int> st(n_cam, -1), ts(n_cam, -1);
+      int64_t total = 0;
+      int chn = 0;
+      for (int b = 0; b < n_cta; ++b) {
+        int cnt = 0;
+        bool open = false;
+        for (int ti = cta[b].x; ti < cta[b].y; ++ti) {
+          const bool may_cut = (ti - cta[b].x) % align == 0;
+          if (may_cut || !open) {
+            int fresh = 0;
+            for (int tj = ti; tj < std::min(ti + align, cta[b].y); ++tj)
+              for (int i = 0; i < tiles[tj].n; ++i) {
+                const int cam = hcam[(int64_t)tj * kTile + i];
+                if (ts[cam] == ti) continue;
+                ts[cam] = ti;
+                if (!open || st[cam] != chn) ++fresh;
+              }
+            if (!open || cnt + fresh > cap) {
+              if (open) ++chn;
+              open = true;
+              cnt = 0;
+            }
+          }
+          for (int i = 0; i < tiles[ti].n; ++i) {
+            const int cam = hcam[(int64_t)ti * kTile + i];
+            if (st[cam] != chn) {
+              st[cam] = chn;
+              ++cnt;
+              ++total;
+            }
+          }
+        }
+        if (open) ++chn;
+      }
+      return total;
+    };
+    const int cap_gather = TermShape<false>::kAccSlots - 8 * kSlotSlack;
+    const int cap_table = TermShape<true>::kAccSlots - 8 * kSlotSlack;
+    const char* force = getenv("POBA_TERM_CHUNK_T");
+    if (force) {
+      c.chunk_t = atoi(force) != 0;
+    } else {
+      const int64_t pg = count_partials(cap_gather, 1), pt = count_partials(cap_table, kTermWarps);
+      c.chunk_t = (double)pt <= kChunkTMaxGrowth * (double)pg;
+    }
+    const int align = c.chunk_t ? kTermWarps : 1;
+    const int cap_slots = c.chunk_t ? cap_table : cap_gather;
+    std::vector<int> rstamp(n_cam, -1);
     for (int b = 0; b < n_cta; ++b) {
       int ch = -1, cnt = 0;
       for (int ti = cta[b].x; ti < cta[b].y; ++ti) {
@@ -848,7 +904,18 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
           tstamp[cam] = ti;
           if (ch < 0 || stamp[cam] != ch) ++fresh;
         }
-        if (ch < 0 || cnt + fresh > kAccSlots - 8 * kSlotSlack) {
+        const bool may_cut = (ti - cta[b].x) % align == 0;
+        if (align > 1 && may_cut) {  // new cameras of the whole round
+          fresh = 0;
+          for (int tj = ti; tj < std::min(ti + align, cta[b].y); ++tj)
+            for (int i = 0; i < tiles[tj].n; ++i) {
+              const int cam = hcam[(int64_t)tj * kTile + i];
+              if (rstamp[cam] == ti) continue;
+              rstamp[cam] = ti;
+              if (ch < 0 || stamp[cam] != ch) ++fresh;
+            }
+        }
+        if (ch < 0 || (may_cut && cnt + fresh > cap_slots)) {
           if (ch >= 0) chunks.back().tile1 = ti;
           chunks.push_back(Chunk{ti, ti, (int)part_cam.size(), 0});
           ch = (int)chunks.size() - 1;
@@ -1081,6 +1148,8 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     PTRY(poba::copy_sync(c, c.part_idx.p, idx.data(), std::max(n_u, 1) * 4, cudaMemcpyHostToDevice));
     PTRY(c.part_cam_off.alloc((n_cam + 1) * 4));
     PTRY(poba::copy_sync(c, c.part_cam_off.p, off.data(), (n_cam + 1) * 4, cudaMemcpyHostToDevice));
+    PTRY(c.part_cam.alloc(std::max(n_u, 1) * 4));
+    if (n_u) PTRY(poba::copy_sync(c, c.part_cam.p, part_cam.data(), (size_t)n_u * 4, cudaMemcpyHostToDevice));
   }
   DBuf ka, kb;
   PTRY(ka.alloc(ns * 8));
