@@ -32,13 +32,22 @@ for i, n in names.items():
 cfg = sys.argv[2] if len(sys.argv) > 2 else "c5"
 N = {"c5": (29084796, 4500000, 13700), "c4": (10317376, 1000000, 1100), "c3": (878990, 160000, 1200)}[cfg]
 no, nl, nc = N
-ALG = {  # algorithmic bytes per launch
-    "k_term<0, 0>": 196 * no + 48 * nl + 72 * nc, "k_term<1, 0>": 196 * no + 72 * nl + 72 * nc,
+ALG = {  # algorithmic bytes per launch, keyed by kernel name prefix
+    "k_term<0, 0": 196 * no + 48 * nl + 72 * nc, "k_term<1, 0": 196 * no + 72 * nl + 72 * nc,
     "k_lin_tile<0, 0>": (196 + 16 + 16 + 4 + 1) * no + (24 + 96) * nl,
-    "k_cam_chunk_reduce<0, 0>": (16 + 4) * no + 54 * 8 * nc, "k_cam_major_gather": 0,
+    "k_cam_chunk_reduce<0, 0>": (16 + 4) * no + 54 * 8 * nc,
     "k_wt_tile<2, 0>": 196 * no + (48 + 24 + 24) * nl, "k_cost_tile": (16 + 4 + 1) * no + 48 * nl,
     "k_damp_v": (48 + 24 + 48 + 48) * nl, "k_damp_u": (360 + 72 + 360 + 360) * nc,
 }
+
+
+def alg_of(name):
+    for k, v in ALG.items():
+        if name.startswith(k):
+            return v
+    return None
+
+
 peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"]
 print(f"| kernel | launches per pass | us per pass (ncu, cold, summed over its launches) | DRAM read MB | DRAM write MB | "
       f"DRAM GB/s | algorithmic MB | algorithmic GB/s | frac of {peak:.0f} | LSU pipe % | warps active % |")
@@ -51,7 +60,7 @@ for n, m in sorted(agg.items(), key=lambda x: -x[1].get("gpu__time_duration.sum"
     t = m.get("gpu__time_duration.sum", 0.0) / PASSES  # ms per pass
     rd, wr = m.get("dram__bytes_read.sum", 0.0) / PASSES, m.get("dram__bytes_write.sum", 0.0) / PASSES
     lp = k / PASSES
-    alg = ALG.get(n)
+    alg = alg_of(n)
     if alg and n.startswith("k_term") or n.startswith("k_cam<"):
         # launched several times per pass on the same data: per-launch figures
         t, rd, wr, lp_note = t / lp, rd / lp, wr / lp, f"{lp:g} (per launch)"
