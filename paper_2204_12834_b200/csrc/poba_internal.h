@@ -82,19 +82,22 @@ constexpr int kTRecBytes = kTStride * 8;                         // 80
 //                        set still fits (C1-C4), not on C5
 // one CTA: the 227-KB per-CTA limit; several: an equal share of the SM's 228 KB less the 1 KB reserved per CTA
 constexpr int kTermSmemMax = kTermCtas == 1 ? 227 * 1024 : (228 * 1024) / kTermCtas - 1024;
-constexpr int kTermCtl = kTermWarps * 16 + 16;                   // full + empty stage barriers + pad
+#ifndef POBA_TERM_WARPS_TABLE
+#define POBA_TERM_WARPS_TABLE 14  // the table layout needs 145 registers per thread (gather: 162), so 14 warps fit
+#endif
 template <bool CT>
 struct TermShape {
+  static constexpr int kWarps = CT ? POBA_TERM_WARPS_TABLE : kTermWarps;        // warps per CTA
+  static constexpr int kCtl = kWarps * 16 + 16;                                 // full + empty stage barriers + pad
   static constexpr int kWarpSmem = kStageBytes + (CT ? 0 : kTile * kTRecBytes);  // stage (+ per-warp record table)
   static constexpr int kSlotBytes = CT ? 2 * kTRecBytes : kTRecBytes;           // accumulator (+ term record)
-  static constexpr int kAccSlots = ((kTermSmemMax - kTermWarps * kWarpSmem - kTermCtl) / kSlotBytes) / 32 * 32;
-  static constexpr int kTermSmem = kTermWarps * kWarpSmem + kTermCtl + kAccSlots * kSlotBytes;
+  static constexpr int kAccSlots = ((kTermSmemMax - kWarps * kWarpSmem - kCtl) / kSlotBytes) / 32 * 32;
+  static constexpr int kTermSmem = kWarps * kWarpSmem + kCtl + kAccSlots * kSlotBytes;
   static_assert(kTermSmem <= kTermSmemMax, "term kernel shared memory over budget");
   static_assert(kAccSlots < 2048, "chunk slots must fit the 11-bit metadata field");
-  static_assert(kWarpSmem % 16 == 0, "bulk-copy destinations must be 16-B aligned");
+  static_assert(kWarpSmem % 16 == 0 && kCtl % 16 == 0, "bulk-copy destinations and the tables must be 16-B aligned");
+  static_assert(kWarps >= 2 && kWarps <= 14, "the apply turn uses named barriers 1..kWarps (ring of >= 2), the chunk barrier 15");
 };
-static_assert(kTermCtl % 16 == 0, "the accumulator table after the stage barriers must stay 16-B aligned");
-static_assert(kTermWarps >= 2 && kTermWarps <= 14, "the apply turn uses named barriers 1..kTermWarps (ring of >= 2), the chunk barrier 15");
 static_assert(kStageBytes % 16 == 0, "bulk-copy destinations must be 16-B aligned");
 // the table layout is taken when it needs at most this many times the gather layout's chunk partials
 constexpr double kChunkTMaxGrowth = 3.0;  // C4: 2.1x the partials, kernel -6%; C5 x 0.3: 8x, kernel 2x slower

@@ -253,7 +253,9 @@ struct TermArgs {
 // After the last tile of a chunk its warp writes the table out once (one 80-B
 // partial per (chunk, camera)) and clears it before passing the turn on.
 template <int MODE, bool F32, bool CT>
-__global__ void __launch_bounds__(kTermWarps * 32, kTermCtas) k_term(const TermArgs a) {
+__global__ void __launch_bounds__(TermShape<CT>::kWarps * 32, kTermCtas) k_term(const TermArgs a) {
+  constexpr int kTermWarps = TermShape<CT>::kWarps;  // (shadows the gather layout's global constant)
+  constexpr int kTermCtl = TermShape<CT>::kCtl;
   constexpr int kWarpSmem = TermShape<CT>::kWarpSmem;
   constexpr int kAccSlots = TermShape<CT>::kAccSlots;
   constexpr bool kChunkT = CT;
@@ -1074,14 +1076,14 @@ void launch_term_shape(Ctx& c, int mode, const TermArgs& a) {
   const unsigned grid = (unsigned)c.n_cta;
   const bool f32 = c.precision == 32;
   if (mode == kModeTerm) {
-    if (f32) k_term<kModeTerm, true, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
-    else k_term<kModeTerm, false, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeTerm, true, CT><<<grid, TermShape<CT>::kWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeTerm, false, CT><<<grid, TermShape<CT>::kWarps * 32, smem, c.stream>>>(a);
   } else if (mode == kModeBt) {
-    if (f32) k_term<kModeBt, true, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
-    else k_term<kModeBt, false, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeBt, true, CT><<<grid, TermShape<CT>::kWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeBt, false, CT><<<grid, TermShape<CT>::kWarps * 32, smem, c.stream>>>(a);
   } else {
-    if (f32) k_term<kModeW, true, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
-    else k_term<kModeW, false, CT><<<grid, kTermWarps * 32, smem, c.stream>>>(a);
+    if (f32) k_term<kModeW, true, CT><<<grid, TermShape<CT>::kWarps * 32, smem, c.stream>>>(a);
+    else k_term<kModeW, false, CT><<<grid, TermShape<CT>::kWarps * 32, smem, c.stream>>>(a);
   }
 }
 

@@ -816,6 +816,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
   {
     std::vector<int> hcam(ns);
     PTRY(poba::copy_sync(c, hcam.data(), c.cam_s.p, ns * 4, cudaMemcpyDeviceToHost));
+    // (sized with the gather layout's warp count; only problems smaller than one round per SM differ)
     const int n_cta = std::max(1, std::min(c.n_sm * kTermCtas, (c.n_tiles + kTermWarps - 1) / kTermWarps));
     std::vector<int64_t> cum(c.n_tiles + 1, 0);
     for (int i = 0; i < c.n_tiles; ++i) cum[i + 1] = cum[i] + tiles[i].n;
@@ -882,10 +883,10 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     if (force) {
       c.chunk_t = atoi(force) != 0;
     } else {
-      const int64_t pg = count_partials(cap_gather, 1), pt = count_partials(cap_table, kTermWarps);
+      const int64_t pg = count_partials(cap_gather, 1), pt = count_partials(cap_table, TermShape<true>::kWarps);
       c.chunk_t = (double)pt <= kChunkTMaxGrowth * (double)pg;
     }
-    const int align = c.chunk_t ? kTermWarps : 1;
+    const int align = c.chunk_t ? TermShape<true>::kWarps : 1;
     const int cap_slots = c.chunk_t ? cap_table : cap_gather;
     std::vector<int> rstamp(n_cam, -1);
     for (int b = 0; b < n_cta; ++b) {
@@ -1127,7 +1128,7 @@ int build_structure(Ctx& c, const int64_t* h_cam, const int64_t* h_pt, const dou
     }
     for (int i = 0; i < c.n_tiles; ++i) {
       const Chunk& ch = chunks[tiles[i].chunk];
-      const int nx = i + kTermWarps;
+      const int nx = i + (c.chunk_t ? TermShape<true>::kWarps : TermShape<false>::kWarps);  // same warp's next tile
       const bool has = nx < cta_end[i];
       tk[i] = TileK{tiles[i].n, tiles[i].lm0, tiles[i].nlm, tiles[i].flags, ch.part0, ch.nslot,
                     has ? (tiles[nx].n | (tiles[nx].nlm << 8)) : 0, has ? tiles[nx].lm0 : 0};
