@@ -83,7 +83,7 @@ constexpr int kTRecBytes = kTStride * 8;                         // 80
 // one CTA: the 227-KB per-CTA limit; several: an equal share of the SM's 228 KB less the 1 KB reserved per CTA
 constexpr int kTermSmemMax = kTermCtas == 1 ? 227 * 1024 : (228 * 1024) / kTermCtas - 1024;
 #ifndef POBA_TERM_WARPS_TABLE
-#define POBA_TERM_WARPS_TABLE 14  // the table layout needs 145 registers per thread (gather: 162), so 14 warps fit
+#define POBA_TERM_WARPS_TABLE 12  // 13 / 14 warps fit its 145 registers but measured 12% slower on C4 and C3 (smaller table, 128-register build)
 #endif
 template <bool CT>
 struct TermShape {
