@@ -307,7 +307,9 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
   }
 }
 
-// V0/b_l of landmarks longer than a tile, straight from the stored rows
+// V0/b_l of landmarks longer than a tile, straight from the stored rows: one
+// warp per landmark, lanes stride its observations (each lane folds its own in
+// order), fixed-shape butterfly across lanes
 template <bool F32>
 __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restrict__ lm_slot0,
                            const int* __restrict__ lm_k, const void* __restrict__ J,
@@ -315,30 +317,34 @@ __global__ void k_lin_long(const int* __restrict__ long_lm, const int* __restric
                            double* __restrict__ bl, double* __restrict__ Dl) {
   const int lm = long_lm[blockIdx.x];
   const int o0 = lm_slot0[lm], o1 = o0 + lm_k[lm];
-  const int comp = threadIdx.x;  // 9 threads
-  if (comp >= 9) return;
-  double acc = 0.0;
-  for (int o = o0; o < o1; ++o) {
+  const int lane = threadIdx.x;  // 32 threads
+  double acc[9] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int o = o0 + lane; o < o1; o += 32) {
     const double2 a = jload<F32>(J, o, 9), b = jload<F32>(J, o, 10), c = jload<F32>(J, o, 11);
     const double2 r = Rz[o];
-    double v;
-    switch (comp) {
-      case 0: v = a.x * a.x + a.y * a.y; break;
-      case 1: v = a.x * b.x + a.y * b.y; break;
-      case 2: v = a.x * c.x + a.y * c.y; break;
-      case 3: v = b.x * b.x + b.y * b.y; break;
-      case 4: v = b.x * c.x + b.y * c.y; break;
-      case 5: v = c.x * c.x + c.y * c.y; break;
-      case 6: v = a.x * r.x + a.y * r.y; break;
-      case 7: v = b.x * r.x + b.y * r.y; break;
-      default: v = c.x * r.x + c.y * r.y; break;
-    }
-    acc += v;
+    acc[0] += a.x * a.x + a.y * a.y;
+    acc[1] += a.x * b.x + a.y * b.y;
+    acc[2] += a.x * c.x + a.y * c.y;
+    acc[3] += b.x * b.x + b.y * b.y;
+    acc[4] += b.x * c.x + b.y * c.y;
+    acc[5] += c.x * c.x + c.y * c.y;
+    acc[6] += a.x * r.x + a.y * r.y;
+    acc[7] += b.x * r.x + b.y * r.y;
+    acc[8] += c.x * r.x + c.y * r.y;
   }
-  if (comp < 6) V0[(int64_t)lm * 6 + comp] = acc; else bl[(int64_t)lm * 3 + comp - 6] = acc;
-  if (comp == 0 || comp == 3 || comp == 5) {
-    const double c2 = fmin(fmax(acc, kClampLo * kClampLo), kClampHi * kClampHi);
-    Dl[(int64_t)lm * 3 + (comp == 0 ? 0 : comp == 3 ? 1 : 2)] = sqrt(c2);
+#pragma unroll
+  for (int q = 0; q < 9; ++q)
+#pragma unroll
+    for (int s = 16; s; s >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], s);
+  if (lane == 0) {
+#pragma unroll
+    for (int comp = 0; comp < 9; ++comp) {
+      if (comp < 6) V0[(int64_t)lm * 6 + comp] = acc[comp]; else bl[(int64_t)lm * 3 + comp - 6] = acc[comp];
+      if (comp == 0 || comp == 3 || comp == 5) {
+        const double c2 = fmin(fmax(acc[comp], kClampLo * kClampLo), kClampHi * kClampHi);
+        Dl[(int64_t)lm * 3 + (comp == 0 ? 0 : comp == 3 ? 1 : 2)] = sqrt(c2);
+      }
+    }
   }
 }
 
