@@ -46,6 +46,9 @@ constexpr int kCamReduceThreads = POBA_CAM_REDUCE_THREADS;
 #ifndef POBA_LIN_TILE_BLOCKS
 #define POBA_LIN_TILE_BLOCKS 2  // 8 x 3 (80 registers, spills) measured slower
 #endif
+#ifndef POBA_LIN_PIPE_BLOCKS
+#define POBA_LIN_PIPE_BLOCKS 3  // blocks of 4 warps per SM the pipelined tile pass is compiled for
+#endif
 constexpr int kLinTiles = POBA_LIN_TILES;
 constexpr int kLinTileSmem = kLinTiles * kTile * kLinRec * 16;
 
@@ -305,6 +308,161 @@ k_lin_tile(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* _
       Dl[(int64_t)lm * 3 + (comp == 0 ? 0 : comp == 3 ? 1 : 2)] = sqrt(c2);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Software-pipelined tile pass (state path).  Same arithmetic as k_lin_tile,
+// but the warps are persistent and keep two tiles of loads in flight behind
+// the tile they compute: at tile i a warp issues the per-slot loads (camera,
+// landmark index, pixel) and the descriptor of tile i + 2, then -- with tile
+// i + 1's of those now landed -- that tile's point loads and its 32 camera
+// records (cp.async, 16 B x 8 per lane, into the other half of a two-deep
+// shared stage), and only then evaluates tile i.  k_lin_tile's warp waits two
+// dependent load waves per tile; this one waits none in steady state.
+// ---------------------------------------------------------------------------
+constexpr int kPipeWarps = 4;                       // warps per block
+constexpr int kPipeRecBytes = kTile * kLinRec * 16;  // one tile's staged camera records (4608 B)
+constexpr int kPipeSmem = kPipeWarps * 2 * kPipeRecBytes;
+
+struct LinW1 {  // first load wave of a tile: per-slot values + descriptor
+  int cam, li;
+  double2 pix;
+  Tile t;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+template <bool F32>
+__global__ void __launch_bounds__(kPipeWarps * kTile, POBA_LIN_PIPE_BLOCKS)
+k_lin_tile_pipe(const Tile* __restrict__ tiles, int tile0, int tile_end, const int* __restrict__ cam_s,
+                const double2* __restrict__ pix_s, const uint8_t* __restrict__ lidx_s,
+                const double* __restrict__ prep, const double* __restrict__ points, void* __restrict__ J,
+                double2* __restrict__ Rz, double* __restrict__ V0, double* __restrict__ bl, double* __restrict__ Dl,
+                unsigned long long* __restrict__ n_invalid) {
+  __shared__ double contrib_all[kPipeWarps][kTile * 9];
+  __shared__ int lstart_all[kPipeWarps][kTile + 1];
+  extern __shared__ __align__(16) double2 pipe_rec[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int stride = gridDim.x * kPipeWarps;
+  int ti = tile0 + blockIdx.x * kPipeWarps + w;  // consecutive warps take consecutive tiles
+  if (ti >= tile_end) return;                   // warps are independent: no block-wide barrier below
+  double* contrib = contrib_all[w];
+  int* lstart = lstart_all[w];
+  double2* const stage0 = pipe_rec + (w * 2) * kTile * kLinRec;  // two-deep record stage of this warp
+  auto stage = [&](int h) { return stage0 + h * kTile * kLinRec; };
+
+  auto wave1 = [&](int tj, LinW1& r) {  // clamped past the end: loads stay in range, the results unused
+    const int tt = min(tj, tile_end - 1);
+    const int64_t o = (int64_t)tt * kTile + lane;
+    r.cam = cam_s[o];
+    r.li = lidx_s[o];
+    r.pix = __ldcs(pix_s + o);
+    r.t = tiles[tt];
+  };
+  auto wave2 = [&](const LinW1& r, double2* pst, double& X0, double& X1, double& X2) {
+    X0 = X1 = X2 = 0.0;
+    if (lane < r.t.n) {
+      const double* X = points + (int64_t)(r.t.lm0 + ((r.t.flags & kTileLong) ? 0 : r.li)) * 3;
+      X0 = X[0];
+      X1 = X[1];
+      X2 = X[2];
+    }
+    const int my_cam = lane < r.t.n ? r.cam : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int rr = 4 * k + (lane >> 3), piece = lane & 7;
+      const int cam = __shfl_sync(0xffffffffu, my_cam, rr);
+      if (rr < r.t.n) cp_async16(pst + rr * 9 + piece, reinterpret_cast<const double2*>(prep + (int64_t)cam * 16) + piece);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  LinW1 a, b, c;
+  double XA0, XA1, XA2, XB0 = 0.0, XB1 = 0.0, XB2 = 0.0;
+  wave1(ti, a);
+  wave1(ti + stride, b);
+  wave2(a, stage(0), XA0, XA1, XA2);
+  int buf = 0;
+  for (; ti < tile_end; ti += stride) {
+    wave1(ti + 2 * stride, c);
+    const bool has_next = ti + stride < tile_end;
+    if (has_next) wave2(b, stage(buf ^ 1), XB0, XB1, XB2);
+    else asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count uniform
+    asm volatile("cp.async.wait_group 1;" ::: "memory");       // tile i's records have landed
+    __syncwarp();
+    const Tile t = a.t;
+    const int64_t o = (int64_t)ti * kTile + lane;
+    const bool is_long = t.flags & kTileLong;
+    const int prev_li = __shfl_up_sync(0xffffffffu, a.li, 1);
+    bool bad = false;
+    if (lane < t.n) {
+      double cp[16];
+      const double2* pst = stage(buf);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double2 v = pst[lane * 9 + k];
+        cp[2 * k] = v.x;
+        cp[2 * k + 1] = v.y;
+      }
+      ObsModel m;
+      evaluate_obs<true>(cp, XA0, XA1, XA2, a.pix, m);
+      bad = !m.valid;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        m.jp0[j] = stored<F32>(m.jp0[j]);
+        m.jp1[j] = stored<F32>(m.jp1[j]);
+        jstore<F32>(J, o, j, m.jp0[j], m.jp1[j]);
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        m.jl0[q] = stored<F32>(m.jl0[q]);
+        m.jl1[q] = stored<F32>(m.jl1[q]);
+        jstore<F32>(J, o, 9 + q, m.jl0[q], m.jl1[q]);
+      }
+      m.r0 = stored<F32>(m.r0);
+      m.r1 = stored<F32>(m.r1);
+      Rz[o] = make_double2(m.r0, m.r1);
+      double* cc = contrib + lane * 9;
+      cc[0] = m.jl0[0] * m.jl0[0] + m.jl1[0] * m.jl1[0];
+      cc[1] = m.jl0[0] * m.jl0[1] + m.jl1[0] * m.jl1[1];
+      cc[2] = m.jl0[0] * m.jl0[2] + m.jl1[0] * m.jl1[2];
+      cc[3] = m.jl0[1] * m.jl0[1] + m.jl1[1] * m.jl1[1];
+      cc[4] = m.jl0[1] * m.jl0[2] + m.jl1[1] * m.jl1[2];
+      cc[5] = m.jl0[2] * m.jl0[2] + m.jl1[2] * m.jl1[2];
+      cc[6] = m.jl0[0] * m.r0 + m.jl1[0] * m.r1;
+      cc[7] = m.jl0[1] * m.r0 + m.jl1[1] * m.r1;
+      cc[8] = m.jl0[2] * m.r0 + m.jl1[2] * m.r1;
+      if (!is_long && (lane == 0 || prev_li != a.li)) lstart[a.li] = lane;
+    }
+    if (lane == 0) lstart[t.nlm] = t.n;
+    __syncwarp();
+    const unsigned nbad = __popc(__ballot_sync(0xffffffffu, bad));
+    if (lane == 0 && nbad) atomicAdd(n_invalid, (unsigned long long)nbad);
+    if (!is_long) {  // long landmarks are reduced by k_lin_long
+      for (int q = lane; q < t.nlm * 9; q += kTile) {
+        const int j = q / 9, comp = q - j * 9;
+        double acc = 0.0;
+        for (int r = lstart[j]; r < lstart[j + 1]; ++r) acc += contrib[r * 9 + comp];
+        const int lm = t.lm0 + j;
+        if (comp < 6) V0[(int64_t)lm * 6 + comp] = acc; else bl[(int64_t)lm * 3 + comp - 6] = acc;
+        if (comp == 0 || comp == 3 || comp == 5) {
+          const double c2 = fmin(fmax(acc, kClampLo * kClampLo), kClampHi * kClampHi);
+          Dl[(int64_t)lm * 3 + (comp == 0 ? 0 : comp == 3 ? 1 : 2)] = sqrt(c2);
+        }
+      }
+    }
+    __syncwarp();  // contrib / lstart / this stage half are reused by the next tiles
+    a = b;
+    b = c;
+    XA0 = XB0;
+    XA1 = XB1;
+    XA2 = XB2;
+    buf ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // V0/b_l of landmarks longer than a tile, straight from the stored rows: one
@@ -578,10 +736,30 @@ int linearize_device(Ctx& c, bool expl, const double* h_jp, const double* h_jl, 
         c.Dl.as<double>(), d_bad);
     c.launches++;
   };
+  // Tile pass: the software-pipelined kernel (12 warps per SM, two tiles of loads
+  // in flight per warp) wins when the camera records come from L2 (C5, 13,700
+  // cameras: 3.02 -> 2.72 ms); with ~1,100 cameras the records stay in L1, the
+  // load waves are short and the one-tile-per-warp kernel's 16 warps per SM hide
+  // the fp64 dependency chain better (C4: 1.15 vs 1.25 ms).  POBA_LIN_PIPE=0/1 forces.
+  const bool pipe = getenv("POBA_LIN_PIPE") ? atoi(getenv("POBA_LIN_PIPE")) != 0 : c.n_cam > 4096;
   auto lin_range = [&](int t0, int t1) {
     if (expl) {
       if (f32) lin(k_lin_tile<true, true>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>(), t0, t1);
       else lin(k_lin_tile<true, false>, nullptr, nullptr, ejp.as<double>(), ejl.as<double>(), eres.as<double>(), t0, t1);
+    } else if (pipe) {
+      if (t1 <= t0) return;
+      const int nblk = std::min((t1 - t0 + kPipeWarps - 1) / kPipeWarps, c.n_sm * POBA_LIN_PIPE_BLOCKS);
+      auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmem);
+        kern<<<nblk, kPipeWarps * kTile, kPipeSmem, s>>>(c.tiles.as<Tile>(), t0, t1, c.cam_s.as<int>(),
+                                                        c.pix_s.as<double2>(), c.lidx_s.as<uint8_t>(),
+                                                        c.cams_prep.as<double>(), c.points.as<double>(), c.J.p,
+                                                        c.Rz.as<double2>(), c.V0.as<double>(), c.bl.as<double>(),
+                                                        c.Dl.as<double>(), d_bad);
+        c.launches++;
+      };
+      if (f32) go(k_lin_tile_pipe<true>);
+      else go(k_lin_tile_pipe<false>);
     } else {
       if (f32) lin(k_lin_tile<false, true>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr, t0, t1);
       else lin(k_lin_tile<false, false>, c.cams_prep.as<double>(), c.points.as<double>(), nullptr, nullptr, nullptr, t0, t1);
