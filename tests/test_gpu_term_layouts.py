@@ -113,3 +113,54 @@ def test_automatic_choice(P):
     s._activate()
     assert s._dp.dev.info()["term_layout"] == "table"
     blocks.invalidate(p)
+
+
+def test_sharded_virtual_ranks_in_both_layouts(P):
+    """Two virtual ranks (the sharded path on one device) under each forced layout
+    against the single context: same increments, each rank writes its own landmarks."""
+    import threading
+
+    from paper_2204_12834_b200 import _lib, blocks
+    p = _problem("c3:0.1")
+    ref = _solve(P, p, "table", 5)
+    x_ref, dl_ref = ref[3].delta_p, ref[4]
+    for layout in ("gather", "table"):
+        os.environ["POBA_TERM_CHUNK_T"] = "1" if layout == "table" else "0"
+        try:
+            g = _lib.LocalGroup(2)
+            out, errs = [None, None], []
+
+            def worker(r):
+                try:
+                    dp = blocks.DeviceProblem(p.cam_indices, p.pt_indices, p.pixels, p.n_cameras, p.n_points,
+                                              rank=r, nranks=2, group=g)
+                    dev = dp.dev
+                    assert dev.info()["term_layout"] == layout
+                    dev.set_points(p.points)
+                    dev.linearize(p.camera_params)
+                    dev.damp(1e-4)
+                    x, order, _, _ = dev.series_solve(1e-300, 5)
+                    dl, _ = dev.back_substitute()
+                    out[r] = (x, order, dl, dev.info())
+                except BaseException as e:  # noqa: BLE001 - reported below
+                    errs.append(e)
+
+            th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join(timeout=600)
+            assert not any(t.is_alive() for t in th), "a virtual rank hung"
+            if errs:
+                raise errs[0]
+            g.close()
+        finally:
+            os.environ.pop("POBA_TERM_CHUNK_T", None)
+        assert np.array_equal(out[0][0], out[1][0])  # camera side bitwise identical on both ranks
+        assert out[0][1] == out[1][1] == 5
+        assert rel(out[0][0], x_ref) <= INC_TOL, layout
+        dl = np.zeros_like(dl_ref)
+        for r in range(2):
+            lo, hi = out[r][3]["lm_lo"], out[r][3]["lm_hi"]
+            dl.reshape(-1, 3)[lo:hi] = out[r][2].reshape(-1, 3)[lo:hi]
+        assert rel(dl, dl_ref) <= INC_TOL, layout
