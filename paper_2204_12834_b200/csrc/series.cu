@@ -236,8 +236,11 @@ struct TermArgs {
 // takes tiles range.x + w, + w + kTermWarps, ... through its own one-stage bulk-copy
 // pipeline (the stage is released as soon as the tile's rows are in
 // registers, so the next tile's copy overlaps the whole tile's math).
-//   phase 1  u_o = J_p t_c with t_c from the warp's gathered camera records
-//            (five lanes per 80-B record, 16-B loads, one tile ahead),
+//   phase 1  u_o = J_p t_c, with t_c either from the warp's gathered camera
+//            records (CT = false: five lanes per 80-B record, 16-B loads, one
+//            tile ahead) or read by slot from the chunk's term-record table
+//            (CT = true: loaded by all warps at the chunk's first round,
+//            between two CTA barriers); see TermShape in poba_internal.h,
 //            w_o = J_l^T u_o, landmark sums y_l by a segmented warp scan
 //   phase 2  z_l = V_l^-1 y_l on each landmark's last lane, shuffled back
 //   phase 3  g_o = J_p^T (J_l z_l), nine doubles in registers
@@ -249,7 +252,9 @@ struct TermArgs {
 //            holds its tile's g_o in registers and applies it only after it
 //            has computed its NEXT tile, so the turn's round trip overlaps a
 //            whole tile of math.  A camera seen twice in one tile is
-//            pre-summed in lane order.
+//            pre-summed in lane order; each distinct camera's contribution is
+//            then shuffled to its apply lane (host-planned per tile so that the
+//            slots of an eight-lane quarter differ mod 8: no bank replays).
 // After the last tile of a chunk its warp writes the table out once (one 80-B
 // partial per (chunk, camera)) and clears it before passing the turn on.
 template <int MODE, bool F32, bool CT>
