@@ -279,6 +279,7 @@ struct Ctx {
   int64_t cam_ls = 0;           // sharded: cameras per rank slice of the camera step (>= 4)
   int n_sm = 148;
   bool chunk_t = false;         // term-kernel camera-side layout of this store (TermShape<chunk_t>)
+  bool graph_off = false;       // sharded NCCL context whose series capture failed once: enqueue from then on
   int64_t launches = 0;
 
   // global sizes

@@ -1233,7 +1233,7 @@ int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_use
   // and on NCCL-sharded contexts (the per-term exchange / all-gather are
   // captured with the kernels, every rank launches the same graph).  Virtual
   // ranks meet at host barriers inside their collectives, so they enqueue.
-  if ((c.nranks > 1 && c.group) || getenv("POBA_NO_GRAPH")) {
+  if ((c.nranks > 1 && c.group) || c.graph_off || getenv("POBA_NO_GRAPH")) {
     PTRY(enqueue_series(c, eps, max_order, forced));
   } else {
     SeriesGraph* g = nullptr;
@@ -1255,21 +1255,34 @@ int series_device(Ctx& c, double eps, int max_order, bool forced, int* order_use
       const int st_enq = enqueue_series(c, eps, max_order, forced);
       cudaGraph_t graph = nullptr;
       const cudaError_t e_end = cudaStreamEndCapture(s, &graph);
-      if (st_enq != POBA_OK) {
-        if (graph) cudaGraphDestroy(graph);
-        return st_enq;
+      cudaError_t e_inst = cudaSuccess;
+      if (st_enq == POBA_OK && e_end == cudaSuccess) e_inst = cudaGraphInstantiate(&ng.exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (st_enq != POBA_OK || e_end != cudaSuccess || e_inst != cudaSuccess) {
+        c.launches = l0;
+        if (c.nranks > 1) {
+          // an NCCL build / topology that cannot capture its collectives: the
+          // same launches, enqueued (nothing of the failed capture has run)
+          cudaGetLastError();
+          c.graph_off = true;
+          fprintf(stderr, "libpoba: rank %d: series capture failed, enqueueing the sharded series instead\n", c.rank);
+          PTRY(enqueue_series(c, eps, max_order, forced));
+        } else {
+          if (st_enq != POBA_OK) return st_enq;
+          PCK(e_end);
+          PCK(e_inst);
+        }
+      } else {
+        ng.launches = c.launches - l0;
+        c.launches = l0;
+        c.graphs.push_back(ng);
+        g = &c.graphs.back();
       }
-      PCK(e_end);
-      const cudaError_t e_inst = cudaGraphInstantiate(&ng.exec, graph, 0);
-      cudaGraphDestroy(graph);
-      PCK(e_inst);
-      ng.launches = c.launches - l0;
-      c.launches = l0;
-      c.graphs.push_back(ng);
-      g = &c.graphs.back();
     }
-    PCK(cudaGraphLaunch(g->exec, s));
-    c.launches += g->launches;
+    if (g) {
+      PCK(cudaGraphLaunch(g->exec, s));
+      c.launches += g->launches;
+    }
   }
   SeriesState st;
   PCK(cudaMemcpyAsync(&st, c.state.p, sizeof(st), cudaMemcpyDeviceToHost, s));
