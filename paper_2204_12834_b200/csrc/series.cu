@@ -1118,19 +1118,24 @@ int launch_cam(Ctx& c, int mode, int order, double eps, bool check_stop, const C
     else if (mode == kCamBt) k_cam<kCamBt, kSrcPartials><<<nb, 256, 0, c.stream>>>(a);
     else k_cam<kCamMerge, kSrcPartials><<<nb, 256, 0, c.stream>>>(a);
     c.launches++;
-  } else {
+  } else if (mode == kCamMerge) {
     k_cam<kCamMerge, kSrcPartials><<<nb, 256, 0, c.stream>>>(a);
     c.launches++;
-    if (mode == kCamMerge) {
-      PTRY(allreduce_sum(c, c.rvec.as<double>(), c.n_cam * 9));
-    } else {
+    PTRY(allreduce_sum(c, c.rvec.as<double>(), c.n_cam * 9));
+  } else {
+    {
+      // the merge of this rank's partials writes straight into the padded
+      // send buffer of the slice exchange (no copy of the camera vector)
       const size_t per = (size_t)c.cam_ls * 9;
       PTRY(c.xch_send.alloc(per * c.nranks * 8));
       PTRY(c.xch_recv.alloc(per * c.nranks * 8));
       double* snd = c.xch_send.as<double>();
       if ((int64_t)per * c.nranks > c.n_cam * 9)
         PCK(cudaMemsetAsync(snd + c.n_cam * 9, 0, (per * c.nranks - c.n_cam * 9) * 8, c.stream));
-      PCK(cudaMemcpyAsync(snd, c.rvec.p, c.n_cam * 9 * 8, cudaMemcpyDeviceToDevice, c.stream));
+      CamArgs m = a;
+      m.rout = snd;
+      k_cam<kCamMerge, kSrcPartials><<<nb, 256, 0, c.stream>>>(m);
+      c.launches++;
       PTRY(exchange_slices(c, snd, c.xch_recv.as<double>(), per));
       a.recv = c.xch_recv.as<double>();
       a.nranks = c.nranks;
